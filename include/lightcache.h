@@ -1,0 +1,129 @@
+/*
+ * lightcache.h -- C-ABI of the B200-native LightCache hot path
+ * (paper_2510_05367_b200/liblightcache.so).
+ *
+ * The reference ("stagecache", /root/reference/proj) exposes this path only
+ * as C++ API of a static library; it has no plugin registry or FFI.  Each
+ * entry point below is the flat C form of the reference call it replaces
+ * (cited as proj/<file>:<line>), with plain pointers and sizes.  All
+ * functions return 0 on success or the reference CLI exit code of the
+ * exception the reference would throw (proj/tools/main.cpp:157-169):
+ *   1 ShapeError (and other std::exception), 2 ConfigError,
+ *   3 BudgetError, 4 InvariantError; 5 = CUDA failure (no reference analogue).
+ * lc_last_error() returns the thread-local message of the last failure.
+ *
+ * Config text uses the reference grammar (proj/src/config.cpp:206-224):
+ * one "key = value" per line over default_config(), '#' comments, every key
+ * of apply_override (proj/src/config.cpp:158-204); unknown keys -> 2.
+ *
+ * Host tensors are row-major {b,t,c,h,w} fp32 exactly as stagecache::Tensor5
+ * (proj/include/stagecache/tensor.hpp:60-62).
+ */
+#ifndef LIGHTCACHE_H
+#define LIGHTCACHE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lc_ctx lc_ctx;
+
+/* Library / context ------------------------------------------------------ */
+int lc_version(void);
+const char* lc_last_error(void);
+/* One context per GPU: streams, packed weights, device buffers. */
+int lc_ctx_create(int device, lc_ctx** out);
+int lc_ctx_destroy(lc_ctx* ctx);
+
+/* Configuration (host only) ---------------------------------------------- */
+/* RunConfig parse + validate (proj/src/config.cpp:100-141, :158-224). */
+int lc_config_check(const char* config_text);
+/* config_to_text (proj/src/config.cpp:226-264) of the parsed config. */
+int lc_config_to_text(const char* config_text, char* out, int64_t cap);
+/* Prepare a context for a config: weights (init_weights, proj/src/unet.cpp:153;
+ * init_codec, proj/src/codec.cpp:45), packed for the tensor cores, and buffers. */
+int lc_configure(lc_ctx* ctx, const char* config_text);
+int64_t lc_latent_elems(lc_ctx* ctx); /* T*C*h*w of the b=1 latent */
+int64_t lc_video_elems(lc_ctx* ctx);  /* T*3*H*W of the b=1 video */
+
+/* Whole pipeline: replaces run_pipeline (proj/include/stagecache/pipeline.hpp:42,
+ * proj/src/pipeline.cpp:64-228).  x0: initial latent (1,T,C,h,w) or NULL to
+ * draw it as the reference does (randn(derive_seed(seed,1)), pipeline.cpp:115).
+ * video (1,T,3,H,W) and latent_out (final x) may be NULL.  report receives a
+ * JSON object (device-timed stage ms, MAC counters, cache bytes, swap
+ * timeline makespan/stall, per-stage HBM/pinned peaks). */
+int lc_run_pipeline(lc_ctx* ctx, const float* x0, float* video, float* latent_out,
+                    char* report, int64_t report_cap);
+
+/* Device-resident variant for throughput measurement: the initial latent
+ * must have been staged with lc_upload_latent; the video stays in HBM
+ * (fetch with lc_download_video). */
+int lc_upload_latent(lc_ctx* ctx, const float* x0);
+int lc_run_resident(lc_ctx* ctx, char* report, int64_t report_cap);
+int lc_download_video(lc_ctx* ctx, float* video);
+/* Frames decoded per launch group in sliced decode (tool flag, not a config
+ * key; the output is identical for every value). */
+int lc_set_decode_slice(lc_ctx* ctx, int64_t frames);
+
+/* Operators -------------------------------------------------------------- */
+/* forward_full (deep_in == NULL; proj/src/unet.cpp:188-230) or
+ * forward_cached (proj/src/unet.cpp:232-276) on x (2,T,C,h,w).  deep_in /
+ * deep_out use the reference geometry u_next = upsample2(U_{m+1})
+ * (cache_feature_shape, proj/src/unet.cpp:302-309).  eps has x's shape. */
+int lc_forward(lc_ctx* ctx, const float* x, int64_t T, int64_t timestep, const float* deep_in,
+               float* deep_out, float* eps);
+/* decode_batch / decode_sliced (proj/src/codec.cpp:117-145) of n latents
+ * (n,1,C,h,w) -> (n,1,3,H,W); `slice` frames per launch group. */
+int lc_decode(lc_ctx* ctx, const float* latents, int64_t n, int64_t slice, float* video);
+/* conv2d (proj/src/tensor.cpp:151-197) of affine(x, s, o) with optional SiLU
+ * on the tensor-core kernel: x (b,t,c_in,h,w), taps [c_out][c_in][k][k]. */
+int lc_conv2d(lc_ctx* ctx, const float* x, int64_t b, int64_t t, int64_t c_in, int64_t h,
+              int64_t w, const float* taps, const float* bias, int64_t c_out, int64_t k,
+              float s, float o, int silu, float* out);
+/* Up block (proj/src/unet.cpp:101-122): silu(conv3x3(concat(affine(skip),
+ * affine(upsample2(u))))) with the upsample fused (sub-pixel).  skip
+ * (b,t,c_a,h,w), u (b,t,c_b,h/2,w/2), taps [c_out][c_a+c_b][3][3]. */
+int lc_up_conv2d(lc_ctx* ctx, const float* skip, const float* u, int64_t b, int64_t t,
+                 int64_t c_a, int64_t c_b, int64_t h, int64_t w, const float* taps,
+                 const float* bias, int64_t c_out, float s, float o, float* out);
+
+/* Host logic (bit-exact contracts) ---------------------------------------- */
+/* plan_steps (proj/src/cache.cpp:25-33): kinds[s] 1 = Full; flags bit0
+ * has_consumers (cache.cpp:19-23), bit1 is_last_consumer (cache.cpp:15-18). */
+int lc_plan_steps(int64_t total, int64_t interval_n, int8_t* kinds, int8_t* flags);
+/* split (proj/src/chunk.cpp:145-181) for a single-conv chain of kernel k;
+ * halo_kind 0 exact, 1 fixed, 2 none; regions 12 int64 per tile:
+ * core, padded, out_window as (y0,y1,x0,x1). */
+int lc_split(int64_t h, int64_t w, int64_t eta, int64_t omega, int halo_kind, int64_t halo_px,
+             int64_t k, int64_t* regions, int64_t* halo_out);
+/* flops_estimate (proj/src/unet.cpp:287-300) MACs for the config's model
+ * input, Full (cached=0) or Cached (cached=1); cache_bytes
+ * (proj/src/cache.cpp:124-130) in the reference fp32 geometry. */
+int lc_model_numbers(const char* config_text, int64_t* macs_full, int64_t* macs_cached,
+                     int64_t* cache_bytes);
+/* derive_seed / NormalStream (proj/include/stagecache/rng.hpp:11-45). */
+uint64_t lc_derive_seed(uint64_t seed, uint64_t stream);
+int lc_randn(uint64_t seed, int64_t n, float* out);
+
+/* Multi-GPU sliced decode (one process per GPU) --------------------------- */
+/* Frame shard of rank r out of g for T frames: contiguous blocks of
+ * ceil(T/g). */
+int lc_shard_frames(int64_t T, int world, int rank, int64_t* first, int64_t* count);
+/* NCCL communicator for the decode gather.  lc_nccl_unique_id writes
+ * 128 bytes; the caller distributes them (e.g. over torch.distributed). */
+int lc_nccl_unique_id(uint8_t* id128);
+int lc_nccl_init(lc_ctx* ctx, const uint8_t* id128, int world, int rank);
+/* Decode this rank's shard of `latents` (T,1,C,h,w, replicated) and gather
+ * every frame on rank 0 over NVLink (ncclGather emulated with grouped
+ * send/recv); video (T,1,3,H,W) is written on rank 0 only (may be NULL
+ * elsewhere).  ms_out (nullable) receives the device time of decode+gather. */
+int lc_decode_sharded(lc_ctx* ctx, const float* latents, int64_t T, int64_t slice, float* video,
+                      float* ms_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LIGHTCACHE_H */

@@ -1,0 +1,334 @@
+"""B200-native LightCache hot path (arXiv 2510.05367) behind the reference's
+operator and config API.
+
+The product is the native library ``liblightcache.so`` (CUDA kernels for
+sm_100a + C++ host runtime) with the C-ABI declared in ``include/lightcache.h``.
+This module is a thin ctypes binding over that C-ABI for tests and the
+benchmark; it contains no compute and no fallback: if the shared object is
+missing or the GPU is unavailable, calls raise.
+
+Error classes mirror the reference exception hierarchy
+(proj/include/stagecache/common.hpp:33-57) and its CLI exit codes
+(proj/tools/main.cpp:157-169).
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblightcache.so")
+REPO_ROOT = os.path.dirname(_HERE)
+HEADER_PATH = os.path.join(REPO_ROOT, "include", "lightcache.h")
+
+
+class LightCacheError(RuntimeError):
+    code = 1
+
+
+class ShapeError(LightCacheError):
+    code = 1
+
+
+class ConfigError(LightCacheError):
+    code = 2
+
+
+class BudgetError(LightCacheError):
+    code = 3
+
+
+class InvariantError(LightCacheError):
+    code = 4
+
+
+class DeviceError(LightCacheError):
+    code = 5
+
+
+_ERRORS = {1: ShapeError, 2: ConfigError, 3: BudgetError, 4: InvariantError, 5: DeviceError}
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load liblightcache.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run __graft_entry__.build() (make -C "
+                              f"paper_2510_05367_b200/csrc)")
+        L = ctypes.CDLL(LIB_PATH)
+        L.lc_last_error.restype = ctypes.c_char_p
+        L.lc_latent_elems.restype = ctypes.c_int64
+        L.lc_video_elems.restype = ctypes.c_int64
+        L.lc_derive_seed.restype = ctypes.c_uint64
+        L.lc_derive_seed.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = lib().lc_last_error().decode()
+        raise _ERRORS.get(rc, LightCacheError)(msg)
+
+
+def _p(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+I64 = ctypes.c_int64
+
+# Every symbol include/lightcache.h declares (checked by tests/test_capi.py).
+EXPORTS = [
+    "lc_version", "lc_last_error", "lc_ctx_create", "lc_ctx_destroy", "lc_config_check",
+    "lc_config_to_text", "lc_configure", "lc_latent_elems", "lc_video_elems", "lc_run_pipeline",
+    "lc_upload_latent", "lc_run_resident", "lc_download_video", "lc_set_decode_slice",
+    "lc_forward", "lc_decode", "lc_conv2d", "lc_up_conv2d", "lc_plan_steps", "lc_split",
+    "lc_model_numbers", "lc_derive_seed", "lc_randn", "lc_shard_frames", "lc_nccl_unique_id",
+    "lc_nccl_init", "lc_decode_sharded",
+]
+
+# ----------------------------------------------------------------- config
+DEFAULT_CONFIG = """\
+run.frames = 8
+run.height = 64
+run.width = 64
+run.seed = 42
+run.mode = text
+unet.depth = 3
+unet.base_channels = 8
+unet.kernel = 3
+unet.cache_depth = 0
+unet.weight_seed = 1234
+codec.latent_channels = 4
+codec.stages = 2
+codec.width = 8
+codec.weight_seed = 77
+schedule.train_steps = 50
+schedule.beta_min = 0.002
+schedule.beta_max = 0.25
+sampler.kind = euler
+sampler.steps = 25
+sampler.guidance = 1.5
+cache.enabled = true
+cache.n = 2
+swap.mode = async
+swap.simulate = false
+chunk.enabled = true
+chunk.eta = 2
+chunk.omega = 2
+chunk.halo = exact
+chunk.targets = u0
+decode.sliced = true
+budget.fast_bytes = 0
+"""
+
+
+def config_text(overrides: Optional[dict] = None, base: str = "") -> str:
+    """Reference-grammar config text: `base` lines then `key = value` overrides."""
+    lines = [base] if base else []
+    for k, v in (overrides or {}).items():
+        lines.append(f"{k} = {v}")
+    return "\n".join(lines) + "\n"
+
+
+def check_config(text: str) -> None:
+    _check(lib().lc_config_check(text.encode()))
+
+
+def normalize_config(text: str) -> str:
+    buf = ctypes.create_string_buffer(1 << 16)
+    _check(lib().lc_config_to_text(text.encode(), buf, I64(1 << 16)))
+    return buf.value.decode()
+
+
+def parse_config(text: str) -> dict:
+    out = {}
+    for line in normalize_config(text).splitlines():
+        k, v = line.split("=", 1)
+        out[k.strip()] = v.strip()
+    return out
+
+
+def model_numbers(text: str):
+    mf, mc, cb = I64(), I64(), I64()
+    _check(lib().lc_model_numbers(text.encode(), ctypes.byref(mf), ctypes.byref(mc), ctypes.byref(cb)))
+    return mf.value, mc.value, cb.value
+
+
+def plan_steps(total: int, n: int):
+    kinds = np.empty(total, np.int8)
+    flags = np.empty(total, np.int8)
+    _check(lib().lc_plan_steps(I64(total), I64(n), _p(kinds), _p(flags)))
+    return kinds, flags
+
+
+HALO = {"exact": 0, "fixed": 1, "none": 2}
+
+
+def split(h: int, w: int, eta: int, omega: int, halo: str = "exact", halo_px: int = 0, k: int = 3):
+    regions = np.empty(12 * max(1, eta * omega), np.int64)
+    halo_out = I64()
+    _check(lib().lc_split(I64(h), I64(w), I64(eta), I64(omega), ctypes.c_int(HALO[halo]), I64(halo_px),
+                          I64(k), _p(regions), ctypes.byref(halo_out)))
+    return regions.reshape(-1, 3, 4), halo_out.value
+
+
+def derive_seed(seed: int, stream: int) -> int:
+    return lib().lc_derive_seed(seed, stream)
+
+
+def randn(seed: int, n: int) -> np.ndarray:
+    out = np.empty(n, np.float32)
+    _check(lib().lc_randn(ctypes.c_uint64(seed), I64(n), _p(out)))
+    return out
+
+
+def shard_frames(T: int, world: int, rank: int):
+    f0, cnt = I64(), I64()
+    _check(lib().lc_shard_frames(I64(T), ctypes.c_int(world), ctypes.c_int(rank), ctypes.byref(f0),
+                                 ctypes.byref(cnt)))
+    return f0.value, cnt.value
+
+
+# ----------------------------------------------------------------- context
+class Context:
+    """One GPU: streams, packed weights and device buffers (lc_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self._h = ctypes.c_void_p()
+        _check(lib().lc_ctx_create(ctypes.c_int(device), ctypes.byref(self._h)))
+        self.device = device
+        self._text = None
+
+    def close(self):
+        if self._h:
+            lib().lc_ctx_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- configuration
+    def configure(self, text: str):
+        _check(lib().lc_configure(self._h, text.encode()))
+        self._text = text
+        return self
+
+    def latent_elems(self) -> int:
+        return lib().lc_latent_elems(self._h)
+
+    def video_elems(self) -> int:
+        return lib().lc_video_elems(self._h)
+
+    def set_decode_slice(self, frames: int):
+        _check(lib().lc_set_decode_slice(self._h, I64(frames)))
+
+    # -- run_pipeline (proj/src/pipeline.cpp:64)
+    def run_pipeline(self, x0: Optional[np.ndarray] = None, want_video=True, want_latent=False):
+        cfg = parse_config(self._text)
+        T, H, W = int(cfg["run.frames"]), int(cfg["run.height"]), int(cfg["run.width"])
+        video = np.empty((1, T, 3, H, W), np.float32) if want_video else None
+        lat = np.empty(self.latent_elems(), np.float32) if want_latent else None
+        x = None if x0 is None else _f32(x0)
+        rep = ctypes.create_string_buffer(1 << 22)
+        _check(lib().lc_run_pipeline(self._h, _p(x), _p(video), _p(lat), rep, I64(1 << 22)))
+        report = json.loads(rep.value.decode())
+        if lat is not None:
+            s = 1 << int(cfg["codec.stages"])
+            lat = lat.reshape(1, T, int(cfg["codec.latent_channels"]), H // s, W // s)
+        return video, lat, report
+
+    def upload_latent(self, x0: np.ndarray):
+        _check(lib().lc_upload_latent(self._h, _p(_f32(x0))))
+
+    def run_resident(self) -> dict:
+        rep = ctypes.create_string_buffer(1 << 22)
+        _check(lib().lc_run_resident(self._h, rep, I64(1 << 22)))
+        return json.loads(rep.value.decode())
+
+    def download_video(self) -> np.ndarray:
+        out = np.empty(self.video_elems(), np.float32)
+        _check(lib().lc_download_video(self._h, _p(out)))
+        return out
+
+    # -- operators
+    def forward(self, x: np.ndarray, timestep: int, deep_in: Optional[np.ndarray] = None,
+                want_deep: bool = False, deep_shape=None):
+        """forward_full / forward_cached (proj/src/unet.cpp:188-276) on x (2,T,C,h,w)."""
+        x = _f32(x)
+        T = x.shape[1]
+        eps = np.empty_like(x)
+        deep_out = np.empty(deep_shape, np.float32) if want_deep else None
+        din = None if deep_in is None else _f32(deep_in)
+        _check(lib().lc_forward(self._h, _p(x), I64(T), I64(timestep), _p(din), _p(deep_out), _p(eps)))
+        return eps, deep_out
+
+    def decode(self, latents: np.ndarray, slice_frames: int = 1) -> np.ndarray:
+        lat = _f32(latents)
+        cfg = parse_config(self._text)
+        s = 1 << int(cfg["codec.stages"])
+        n = lat.shape[0] * lat.shape[1]
+        out = np.empty((lat.shape[0], lat.shape[1], 3, lat.shape[3] * s, lat.shape[4] * s), np.float32)
+        _check(lib().lc_decode(self._h, _p(lat), I64(n), I64(slice_frames), _p(out)))
+        return out
+
+    def conv2d(self, x, taps, bias, s=1.0, o=0.0, silu=False):
+        x, taps, bias = _f32(x), _f32(taps), _f32(bias)
+        b, t, c, h, w = x.shape
+        c_out, k = taps.shape[0], taps.shape[-1]
+        out = np.empty((b, t, c_out, h, w), np.float32)
+        _check(lib().lc_conv2d(self._h, _p(x), I64(b), I64(t), I64(c), I64(h), I64(w), _p(taps), _p(bias),
+                               I64(c_out), I64(k), ctypes.c_float(s), ctypes.c_float(o), ctypes.c_int(int(silu)),
+                               _p(out)))
+        return out
+
+    def up_conv2d(self, skip, u, taps, bias, s=1.0, o=0.0):
+        skip, u, taps, bias = _f32(skip), _f32(u), _f32(taps), _f32(bias)
+        b, t, ca, h, w = skip.shape
+        cb = u.shape[2]
+        c_out = taps.shape[0]
+        out = np.empty((b, t, c_out, h, w), np.float32)
+        _check(lib().lc_up_conv2d(self._h, _p(skip), _p(u), I64(b), I64(t), I64(ca), I64(cb), I64(h), I64(w),
+                                  _p(taps), _p(bias), I64(c_out), ctypes.c_float(s), ctypes.c_float(o), _p(out)))
+        return out
+
+    # -- multi-GPU sliced decode
+    def nccl_init(self, uid: bytes, world: int, rank: int):
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib().lc_nccl_init(self._h, buf, ctypes.c_int(world), ctypes.c_int(rank)))
+
+    def decode_sharded(self, latents: np.ndarray, slice_frames: int = 4):
+        lat = _f32(latents)
+        cfg = parse_config(self._text)
+        s = 1 << int(cfg["codec.stages"])
+        T = lat.shape[0] * lat.shape[1]
+        out = np.empty((1, T, 3, lat.shape[3] * s, lat.shape[4] * s), np.float32)
+        ms = ctypes.c_float()
+        _check(lib().lc_decode_sharded(self._h, _p(lat), I64(T), I64(slice_frames), _p(out), ctypes.byref(ms)))
+        return out, ms.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().lc_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def rel_l2(a: np.ndarray, b: np.ndarray) -> float:
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))

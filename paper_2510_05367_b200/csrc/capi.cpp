@@ -1,0 +1,334 @@
+// extern "C" boundary of liblightcache.so; see include/lightcache.h.
+#include "../../include/lightcache.h"
+
+#include <nccl.h>
+
+#include <cmath>
+#include <cstring>
+#include <sstream>
+#include <string>
+
+#include "engine.hpp"
+
+struct lc_ctx {
+    explicit lc_ctx(int dev) : device(dev), engine(dev) {}
+    int device;
+    lc::Engine engine;
+    ncclComm_t comm = nullptr;
+    int world = 1, rank = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const lc::LcError& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return lc::kShapeError;
+    }
+}
+
+void put(char* dst, int64_t cap, const std::string& s) {
+    if (!dst || cap <= 0) return;
+    const size_t n = std::min<size_t>(s.size(), static_cast<size_t>(cap - 1));
+    std::memcpy(dst, s.data(), n);
+    dst[n] = 0;
+}
+
+std::string report_json(const lc::Engine& e, const lc::RunStats& st) {
+    static const char* stages[4] = {"setup", "encode", "denoise", "decode"};
+    static const char* kinds[6] = {"compute_start", "compute_end", "xfer_start",
+                                   "xfer_end",      "await_start", "await_end"};
+    std::ostringstream os;
+    os.precision(10);
+    os << "{\"device_ms\":{\"denoise\":" << st.ms_denoise << ",\"decode\":" << st.ms_decode
+       << ",\"total\":" << st.ms_total << "},";
+    os << "\"peaks\":{";
+    for (int s = 0; s < 4; ++s)
+        os << (s ? "," : "") << "\"" << stages[s] << "\":{\"fast\":" << st.peak[s][0]
+           << ",\"slow\":" << st.peak[s][1] << "}";
+    os << "},\"hbm_peak_bytes\":" << st.hbm_peak << ",";
+    os << "\"mac\":{\"denoiser_total\":" << st.denoiser_macs << ",\"per_full_step\":" << st.macs_full
+       << ",\"per_cached_step\":" << st.macs_cached << ",\"full_steps\":" << st.full_steps
+       << ",\"cached_steps\":" << st.cached_steps << "},";
+    os << "\"cache_bytes\":" << st.cache_bytes_planned << ",\"cache_bytes_physical\":"
+       << st.cache_bytes_physical << ",";
+    os << "\"swap\":{\"bytes\":" << st.swap_bytes << ",\"calls\":" << st.swap_calls << "},";
+    os << "\"timeline\":{\"makespan_ms\":" << st.makespan_ms << ",\"stall_ms\":" << st.stall_ms
+       << ",\"events\":[";
+    for (size_t i = 0; i < st.timeline.size(); ++i) {
+        const auto& t = st.timeline[i];
+        os << (i ? "," : "") << "[\"" << kinds[static_cast<int>(t[0])] << "\"," << static_cast<int64_t>(t[1])
+           << "," << static_cast<int64_t>(t[2]) << "," << t[3] << "]";
+    }
+    os << "]},\"kernel_launches\":" << st.kernel_launches << ",";
+    const auto& c = e.config();
+    os << "\"video\":{\"frames\":" << c.frames << ",\"channels\":" << c.image_channels
+       << ",\"height\":" << c.height << ",\"width\":" << c.width << "}}";
+    return os.str();
+}
+
+// fp32 NCHW (n,c,h,w) -> fp16 NHWC with channel stride cs
+std::vector<__half> to_nhwc(const float* x, int n, int c, int h, int w, int cs) {
+    std::vector<__half> out(static_cast<size_t>(n) * h * w * cs, __float2half_rn(0.0f));
+    for (int i = 0; i < n; ++i)
+        for (int ch = 0; ch < c; ++ch)
+            for (int y = 0; y < h; ++y)
+                for (int xx = 0; xx < w; ++xx)
+                    out[((static_cast<size_t>(i) * h + y) * w + xx) * cs + ch] =
+                        __float2half_rn(x[((static_cast<size_t>(i) * c + ch) * h + y) * w + xx]);
+    return out;
+}
+void from_nhwc(const std::vector<__half>& in, int n, int c, int h, int w, int cs, float* out) {
+    for (int i = 0; i < n; ++i)
+        for (int ch = 0; ch < c; ++ch)
+            for (int y = 0; y < h; ++y)
+                for (int xx = 0; xx < w; ++xx)
+                    out[((static_cast<size_t>(i) * c + ch) * h + y) * w + xx] =
+                        __half2float(in[((static_cast<size_t>(i) * h + y) * w + xx) * cs + ch]);
+}
+lc::Act upload_act(lc::DevBuf& buf, const float* x, int n, int c, int h, int w) {
+    lc::Act a;
+    a.n = n;
+    a.c = c;
+    a.h = h;
+    a.w = w;
+    a.cs = (c + 63) / 64 * 64;
+    const auto hv = to_nhwc(x, n, c, h, w, a.cs);
+    buf = lc::dev_alloc(nullptr, static_cast<int64_t>(hv.size()) * 2, false);
+    LC_CUDA(cudaMemcpy(buf.p, hv.data(), hv.size() * 2, cudaMemcpyHostToDevice));
+    a.p = buf.as<__half>();
+    return a;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw lc::LcError(lc::kCudaError, std::string("NCCL error ") + ncclGetErrorString(r) + " at " + what);
+}
+
+}  // namespace
+
+extern "C" {
+
+int lc_version(void) { return 1; }
+const char* lc_last_error(void) { return g_err.c_str(); }
+
+int lc_ctx_create(int device, lc_ctx** out) {
+    return guarded([&] { *out = new lc_ctx(device); });
+}
+int lc_ctx_destroy(lc_ctx* ctx) {
+    return guarded([&] {
+        if (ctx && ctx->comm) ncclCommDestroy(ctx->comm);
+        delete ctx;
+    });
+}
+
+int lc_config_check(const char* text) {
+    return guarded([&] { lc::parse_config_text(text ? text : "").validate(); });
+}
+int lc_config_to_text(const char* text, char* out, int64_t cap) {
+    return guarded([&] { put(out, cap, lc::config_to_text(lc::parse_config_text(text ? text : ""))); });
+}
+int lc_configure(lc_ctx* ctx, const char* text) {
+    return guarded([&] { ctx->engine.configure(lc::parse_config_text(text ? text : "")); });
+}
+int64_t lc_latent_elems(lc_ctx* ctx) { return ctx->engine.latent_elems(); }
+int64_t lc_video_elems(lc_ctx* ctx) { return ctx->engine.video_elems(); }
+
+int lc_run_pipeline(lc_ctx* ctx, const float* x0, float* video, float* latent_out, char* report,
+                    int64_t cap) {
+    return guarded([&] {
+        const lc::RunStats st = ctx->engine.run(x0, video, latent_out, false);
+        put(report, cap, report_json(ctx->engine, st));
+    });
+}
+int lc_upload_latent(lc_ctx* ctx, const float* x0) {
+    return guarded([&] {
+        ctx->engine.run_prepare();
+        LC_CUDA(cudaMemcpy(ctx->engine.latent_dev(), x0, static_cast<size_t>(ctx->engine.latent_elems()) * 4,
+                           cudaMemcpyHostToDevice));
+    });
+}
+int lc_run_resident(lc_ctx* ctx, char* report, int64_t cap) {
+    return guarded([&] {
+        const lc::RunStats st = ctx->engine.run(nullptr, nullptr, nullptr, true);
+        put(report, cap, report_json(ctx->engine, st));
+    });
+}
+int lc_download_video(lc_ctx* ctx, float* video) {
+    return guarded([&] {
+        LC_CUDA(cudaMemcpy(video, ctx->engine.video_dev(), static_cast<size_t>(ctx->engine.video_elems()) * 4,
+                           cudaMemcpyDeviceToHost));
+    });
+}
+int lc_set_decode_slice(lc_ctx* ctx, int64_t frames) {
+    return guarded([&] {
+        if (frames < 1) lc::throw_config("decode slice must be >= 1");
+        ctx->engine.decode_slice = frames;
+    });
+}
+
+int lc_forward(lc_ctx* ctx, const float* x, int64_t T, int64_t timestep, const float* deep_in,
+               float* deep_out, float* eps) {
+    return guarded([&] { ctx->engine.forward(x, T, timestep, deep_in, deep_out, eps); });
+}
+int lc_decode(lc_ctx* ctx, const float* latents, int64_t n, int64_t slice, float* video) {
+    return guarded([&] { ctx->engine.decode(latents, n, video, slice); });
+}
+
+int lc_conv2d(lc_ctx* ctx, const float* x, int64_t b, int64_t t, int64_t c_in, int64_t h, int64_t w,
+              const float* taps, const float* bias, int64_t c_out, int64_t k, float s, float o, int silu,
+              float* out) {
+    return guarded([&] {
+        if (k < 1 || k % 2 == 0) lc::throw_shape("kernel size must be odd");
+        lc::Bank bank;
+        bank.c_in = c_in;
+        bank.c_out = c_out;
+        bank.k = k;
+        bank.taps.assign(taps, taps + c_out * c_in * k * k);
+        bank.bias.assign(bias, bias + c_out);
+        auto L = lc::pack_tc_layer(nullptr, bank, static_cast<int>(c_in), 0);
+        const int n = static_cast<int>(b * t);
+        lc::DevBuf xb, ob;
+        const lc::Act xa = upload_act(xb, x, n, static_cast<int>(c_in), static_cast<int>(h), static_cast<int>(w));
+        lc::Act oa;
+        oa.n = n;
+        oa.c = static_cast<int>(c_out);
+        oa.h = static_cast<int>(h);
+        oa.w = static_cast<int>(w);
+        oa.cs = (oa.c + 63) / 64 * 64;
+        ob = lc::dev_alloc(nullptr, oa.elems() * 2, true);
+        oa.p = ob.as<__half>();
+        const int H = static_cast<int>(h), W = static_cast<int>(w);
+        lc::run_tc_conv(*L, &xa, oa, lc::Window{0, H, 0, W, 0, H, 0, W}, s, o, silu != 0,
+                        ctx->engine.stream());
+        LC_CUDA(cudaStreamSynchronize(ctx->engine.stream()));
+        std::vector<__half> hv(static_cast<size_t>(oa.elems()));
+        LC_CUDA(cudaMemcpy(hv.data(), oa.p, hv.size() * 2, cudaMemcpyDeviceToHost));
+        from_nhwc(hv, n, oa.c, H, W, oa.cs, out);
+    });
+}
+
+int lc_up_conv2d(lc_ctx* ctx, const float* skip, const float* u, int64_t b, int64_t t, int64_t c_a,
+                 int64_t c_b, int64_t h, int64_t w, const float* taps, const float* bias, int64_t c_out,
+                 float s, float o, float* out) {
+    return guarded([&] {
+        if (h % 2 || w % 2) lc::throw_shape("up block needs even extents");
+        lc::Bank bank;
+        bank.c_in = c_a + c_b;
+        bank.c_out = c_out;
+        bank.k = 3;
+        bank.taps.assign(taps, taps + c_out * (c_a + c_b) * 9);
+        bank.bias.assign(bias, bias + c_out);
+        auto L = lc::pack_tc_layer(nullptr, bank, static_cast<int>(c_a), 1);
+        const int n = static_cast<int>(b * t), H = static_cast<int>(h), W = static_cast<int>(w);
+        lc::DevBuf sb, ub, ob;
+        lc::Act srcs[2];
+        srcs[0] = upload_act(sb, skip, n, static_cast<int>(c_a), H, W);
+        srcs[1] = upload_act(ub, u, n, static_cast<int>(c_b), H / 2, W / 2);
+        lc::Act oa;
+        oa.n = n;
+        oa.c = static_cast<int>(c_out);
+        oa.h = H;
+        oa.w = W;
+        oa.cs = (oa.c + 63) / 64 * 64;
+        ob = lc::dev_alloc(nullptr, oa.elems() * 2, true);
+        oa.p = ob.as<__half>();
+        lc::run_tc_conv(*L, srcs, oa, lc::Window{0, H, 0, W, 0, H, 0, W}, s, o, true, ctx->engine.stream());
+        LC_CUDA(cudaStreamSynchronize(ctx->engine.stream()));
+        std::vector<__half> hv(static_cast<size_t>(oa.elems()));
+        LC_CUDA(cudaMemcpy(hv.data(), oa.p, hv.size() * 2, cudaMemcpyDeviceToHost));
+        from_nhwc(hv, n, oa.c, H, W, oa.cs, out);
+    });
+}
+
+int lc_plan_steps(int64_t total, int64_t n, int8_t* kinds, int8_t* flags) {
+    return guarded([&] {
+        const lc::StepPlan p = lc::plan_steps(total, n);
+        for (int64_t s = 0; s < total; ++s) {
+            kinds[s] = p.is_full(s) ? 1 : 0;
+            if (flags)
+                flags[s] = static_cast<int8_t>((p.has_consumers(s) ? 1 : 0) | (p.is_last_consumer(s) ? 2 : 0));
+        }
+    });
+}
+
+int lc_split(int64_t h, int64_t w, int64_t eta, int64_t omega, int halo_kind, int64_t halo_px, int64_t k,
+             int64_t* regions, int64_t* halo_out) {
+    return guarded([&] {
+        if (halo_kind < 0 || halo_kind > 2) lc::throw_config("halo kind must be 0, 1 or 2");
+        const auto tiles = lc::split(h, w, eta, omega, static_cast<lc::HaloKind>(halo_kind), halo_px, k, halo_out);
+        int64_t i = 0;
+        for (const auto& t : tiles)
+            for (const lc::Region* r : {&t.core, &t.padded, &t.out_window}) {
+                regions[i++] = r->y0;
+                regions[i++] = r->y1;
+                regions[i++] = r->x0;
+                regions[i++] = r->x1;
+            }
+    });
+}
+
+int lc_model_numbers(const char* text, int64_t* macs_full, int64_t* macs_cached, int64_t* cache_bytes) {
+    return guarded([&] {
+        const lc::RunConfig c = lc::parse_config_text(text ? text : "");
+        c.validate();
+        const int64_t lh = c.latent_h(), lw = c.latent_w();
+        if (macs_full) *macs_full = lc::flops_estimate(c, 2, c.frames, lh, lw, false);
+        if (macs_cached) *macs_cached = lc::flops_estimate(c, 2, c.frames, lh, lw, true);
+        if (cache_bytes)
+            *cache_bytes = 2 * c.frames * lc::cache_channels(c) * (lh >> c.cache_depth) * (lw >> c.cache_depth) * 4;
+    });
+}
+
+uint64_t lc_derive_seed(uint64_t seed, uint64_t stream) { return lc::derive_seed(seed, stream); }
+int lc_randn(uint64_t seed, int64_t n, float* out) {
+    return guarded([&] { lc::randn(seed, n, out); });
+}
+
+int lc_shard_frames(int64_t T, int world, int rank, int64_t* first, int64_t* count) {
+    return guarded([&] {
+        if (world < 1 || rank < 0 || rank >= world) lc::throw_config("bad world/rank");
+        const int64_t per = (T + world - 1) / world;
+        const int64_t f0 = std::min<int64_t>(T, per * rank);
+        const int64_t f1 = std::min<int64_t>(T, f0 + per);
+        *first = f0;
+        *count = f1 - f0;
+    });
+}
+
+int lc_nccl_unique_id(uint8_t* id128) {
+    return guarded([&] {
+        ncclUniqueId id;
+        nccl_check(ncclGetUniqueId(&id), "ncclGetUniqueId");
+        std::memcpy(id128, &id, sizeof(id));
+    });
+}
+
+int lc_nccl_init(lc_ctx* ctx, const uint8_t* id128, int world, int rank) {
+    return guarded([&] {
+        ncclUniqueId id;
+        std::memcpy(&id, id128, sizeof(id));
+        LC_CUDA(cudaSetDevice(ctx->device));
+        nccl_check(ncclCommInitRank(&ctx->comm, world, id, rank), "ncclCommInitRank");
+        ctx->world = world;
+        ctx->rank = rank;
+    });
+}
+
+int lc_decode_sharded(lc_ctx* ctx, const float* latents, int64_t T, int64_t slice, float* video, float* ms_out) {
+    return guarded([&] {
+        if (!ctx->comm && ctx->world > 1) lc::throw_config("lc_nccl_init first");
+        ctx->engine.decode_sharded(latents, T, slice, video, ctx->comm, ctx->world, ctx->rank, ms_out);
+    });
+}
+
+}  // extern "C"

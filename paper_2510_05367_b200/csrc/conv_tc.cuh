@@ -1,0 +1,77 @@
+// Implicit-GEMM convolution on tcgen05 tensor cores (sm_100a).
+//
+// Replaces the reference's scalar conv2d_window hot loop
+// (proj/src/tensor.cpp:155-197), fused with the block prologue/epilogue of
+// run_conv_block / run_up_block (proj/src/unet.cpp:78-122):
+//   * the per-block conditioning affine x*s+o is folded algebraically:
+//       conv(affine(x)) = s * conv_nobias(x) + o * sum_{in-bound taps} w + bias
+//     so zero padding stays literal zeros exactly as in the reference;
+//   * channel concat (up blocks) is a two-segment K loop, never materialised;
+//   * nearest-upsample + conv3x3 runs "sub-pixel": per output parity class
+//     the upsampled operand is a 2x2 conv over the low-res tensor with merged
+//     taps, and the full-res skip operand is read with TMA element stride 2;
+//   * bias, conditioning shift and SiLU run in the TMEM->register epilogue.
+//
+// GEMM view: M = output pixels (a TI x TH x TW spatial tile of <=128 pixels),
+// N = output channels (BN <= 256 per CTA), K = segment x tap x channel.
+// Activations are fp16 NHWC ("channels-last"), channel stride a multiple of
+// 64 so one K block is one 128-byte SW128 row per pixel.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace lc {
+
+constexpr int kMaxTaps = 49;  // odd kernels up to 7x7
+
+// One K segment: one source tensor read through one TMA descriptor.
+struct ConvSegDev {
+    int ntaps;  // taps of this segment
+    int ncb;    // 64-channel blocks per tap
+    int kbase;  // first K element of this segment in a weight row
+    int mx, my; // source coordinate = lattice * m + offset
+    int wx0, wy0;  // origin of the tensor map window in source coordinates
+    int8_t ox[4][kMaxTaps];  // per parity class, per tap
+    int8_t oy[4][kMaxTaps];
+};
+
+struct alignas(64) ConvParams {
+    CUtensorMap tmA[2];  // activations, per segment: dims {C, W, H, N}
+    CUtensorMap tmB;     // weights: dims {K_total, N_pad, P}
+    ConvSegDev seg[2];
+    int nseg;
+    int n_img;                    // images = b*t
+    int ly0, ly1, lx0, lx1;       // output region in lattice coordinates
+    int TI, TH, TW;               // pixel tile
+    int tiles_x, tiles_y, tiles_i;
+    int BN;                       // N tile
+    int n_pad;                    // weight rows per parity class
+    int c_out, cs_out;            // real output channels, output channel stride
+    int out_h, out_w;             // output image extents (pixels)
+    int sy, sx;                   // lattice -> output pixel multiplier (1 or 2)
+    int py[4], px[4];             // per parity output offset
+    __half* out;
+    const float* bias;            // [n_pad]
+    const float* corr;            // [P][ncls][n_pad]   sum of in-bound tap weights
+    int rc;                       // class radius (lattice units)
+    int cy0, cy1, cx0, cx1;       // class window (lattice units)
+    float scale;                  // s / weight_scale
+    float shift;                  // o
+    int silu;
+};
+
+struct ConvTcConfig {
+    int stages;
+    int tmem_cols;
+    size_t smem_bytes;
+};
+
+// Host launcher (conv_tc.cu).
+cudaError_t launch_conv_tc(const ConvParams& p, int parities, cudaStream_t stream);
+size_t conv_tc_smem_bytes(int BN);
+
+}  // namespace lc

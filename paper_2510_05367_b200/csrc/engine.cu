@@ -1,0 +1,1087 @@
+// GPU execution engine; see engine.hpp.
+#include "engine.hpp"
+
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace lc {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw LcError(kCudaError, std::string("CUDA error ") + cudaGetErrorString(e) + " at " + what);
+}
+
+// ---------------------------------------------------------------- ledger
+void Ledger::enter(int s) {
+    stage = s;
+    for (int t = 0; t < 2; ++t) peak[s][t] = std::max(peak[s][t], occ[t]);
+}
+void Ledger::alloc(int tier, int64_t bytes) {
+    if (tier == 0 && budget_fast > 0 && occ[0] + bytes > budget_fast) {
+        static const char* names[4] = {"setup", "encode", "denoise", "decode"};
+        throw LcError(kBudgetError, std::string("fast-tier budget exceeded in stage ") + names[stage] +
+                                        ": " + std::to_string(occ[0]) + " + " + std::to_string(bytes) +
+                                        " > " + std::to_string(budget_fast) + " bytes");
+    }
+    occ[tier] += bytes;
+    peak[stage][tier] = std::max(peak[stage][tier], occ[tier]);
+}
+void Ledger::free(int tier, int64_t bytes) { occ[tier] -= bytes; }
+
+DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+        reset();
+        p = o.p;
+        bytes = o.bytes;
+        ledger = o.ledger;
+        tier = o.tier;
+        o.p = nullptr;
+        o.bytes = 0;
+    }
+    return *this;
+}
+void DevBuf::reset() {
+    if (p) {
+        if (tier == 0) cudaFree(p);
+        else cudaFreeHost(p);
+        if (ledger) ledger->free(tier, bytes);
+    }
+    p = nullptr;
+    bytes = 0;
+}
+DevBuf dev_alloc(Ledger* l, int64_t bytes, bool zero) {
+    DevBuf b;
+    if (bytes <= 0) return b;
+    if (l) l->alloc(0, bytes);
+    LC_CUDA(cudaMalloc(&b.p, static_cast<size_t>(bytes)));
+    if (zero) LC_CUDA(cudaMemset(b.p, 0, static_cast<size_t>(bytes)));
+    b.bytes = bytes;
+    b.ledger = l;
+    b.tier = 0;
+    return b;
+}
+DevBuf host_alloc(Ledger* l, int64_t bytes) {
+    DevBuf b;
+    if (bytes <= 0) return b;
+    if (l) l->alloc(1, bytes);
+    LC_CUDA(cudaHostAlloc(&b.p, static_cast<size_t>(bytes), cudaHostAllocDefault));
+    b.bytes = bytes;
+    b.ledger = l;
+    b.tier = 1;
+    return b;
+}
+
+namespace {
+
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        LC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p)
+            throw LcError(kCudaError, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+void encode_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
+                const uint64_t* dims, const uint64_t* strides_bytes, const uint32_t* box,
+                const uint32_t* estr) {
+    const CUresult r = encode_fn()(m, dt, static_cast<cuuint32_t>(rank), const_cast<void*>(base), dims,
+                                   strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw LcError(kCudaError, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
+
+// Border-class geometry: lattice window length L and position Y with the
+// requested distances (capped at rc) to the low/high window edges.
+void class_geom(int d_lo, int d_hi, int rc, int* L, int* Y) {
+    if (rc == 0) {
+        *L = 1, *Y = 0;
+    } else if (d_lo < rc && d_hi < rc) {
+        *L = d_lo + d_hi + 1, *Y = d_lo;
+    } else if (d_lo < rc) {
+        *Y = d_lo, *L = d_lo + rc + 2;
+    } else if (d_hi < rc) {
+        *Y = rc + 1, *L = rc + 2 + d_hi;
+    } else {
+        *Y = rc + 1, *L = 2 * rc + 3;
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------- layer packing
+std::unique_ptr<TcLayer> pack_tc_layer(Ledger* l, const Bank& b, int c_split, int mode) {
+    auto L = std::make_unique<TcLayer>();
+    L->mode = mode;
+    L->k = static_cast<int>(b.k);
+    L->r = (L->k - 1) / 2;
+    L->c_out = static_cast<int>(b.c_out);
+    const int c_in = static_cast<int>(b.c_in), k = L->k, r = L->r;
+    if (k * k > kMaxTaps) throw_config("unet.kernel larger than 7 is not supported on the GPU path");
+    int ch0 = 0;  // first input channel of each segment
+    int seg_ch0[2] = {0, 0};
+    if (mode == 0) {
+        L->P = 1;
+        L->rc = r;
+        if (c_split > 0 && c_split < c_in) {
+            L->nseg = 2;
+            L->seg_c[0] = c_split;
+            L->seg_c[1] = c_in - c_split;
+        } else {
+            L->nseg = 1;
+            L->seg_c[0] = c_in;
+        }
+        for (int s = 0; s < L->nseg; ++s) {
+            L->seg_ntaps[s] = k * k;
+            L->seg_m[s] = 1;
+            for (int t = 0; t < k * k; ++t) {
+                L->ox[s][0][t] = static_cast<int8_t>(t % k - r);
+                L->oy[s][0][t] = static_cast<int8_t>(t / k - r);
+            }
+        }
+    } else {
+        if (k != 3) throw_invariant("sub-pixel packing needs k == 3");
+        L->P = 4;
+        L->rc = 1;
+        int s = 0;
+        if (c_split > 0) {  // full-res skip, stride-2 taps
+            L->seg_c[s] = c_split;
+            L->seg_ntaps[s] = 9;
+            L->seg_m[s] = 2;
+            for (int p = 0; p < 4; ++p)
+                for (int t = 0; t < 9; ++t) {
+                    L->oy[s][p][t] = static_cast<int8_t>(p / 2 + t / 3 - 1);
+                    L->ox[s][p][t] = static_cast<int8_t>(p % 2 + t % 3 - 1);
+                }
+            ++s;
+        }
+        L->seg_c[s] = c_in - c_split;  // low-res operand, merged 2x2 taps
+        L->seg_ntaps[s] = 4;
+        L->seg_m[s] = 1;
+        for (int p = 0; p < 4; ++p)
+            for (int t = 0; t < 4; ++t) {
+                L->oy[s][p][t] = static_cast<int8_t>(t / 2 - 1 + p / 2);
+                L->ox[s][p][t] = static_cast<int8_t>(t % 2 - 1 + p % 2);
+            }
+        L->nseg = s + 1;
+    }
+    for (int s = 0; s < L->nseg; ++s) {
+        seg_ch0[s] = ch0;
+        ch0 += L->seg_c[s];
+        L->seg_cpad[s] = round_up(L->seg_c[s], 64);
+        L->seg_kbase[s] = L->k_total;
+        L->k_total += L->seg_ntaps[s] * L->seg_cpad[s];
+    }
+    // N tiling
+    int nt = 1;
+    while (round_up((L->c_out + nt - 1) / nt, 16) > 256) ++nt;
+    L->BN = round_up((L->c_out + nt - 1) / nt, 16);
+    L->n_pad = nt * L->BN;
+    // power-of-two weight scale ~ sqrt(fan_in): exact to undo in fp32
+    const double fan_in = static_cast<double>(k) * k * c_in;
+    L->wscale = std::ldexp(1.0f, static_cast<int>(std::lround(0.5 * std::log2(fan_in))));
+
+    // fp32 packed weights [P][n_pad][k_total]
+    const size_t nW = static_cast<size_t>(L->P) * L->n_pad * L->k_total;
+    std::vector<float> wf(nW, 0.0f);
+    auto tap = [&](int oc, int ic, int ky, int kx) {
+        return b.taps[((static_cast<size_t>(oc) * c_in + ic) * k + ky) * k + kx];
+    };
+    // merged-row sets of the sub-pixel decomposition: rows(py, dy)
+    auto rows = [](int par, int d, int* lo, int* hi) {
+        if (par == 0) {
+            *lo = d == 0 ? 0 : 1;
+            *hi = d == 0 ? 1 : 3;
+        } else {
+            *lo = d == 0 ? 0 : 2;
+            *hi = d == 0 ? 2 : 3;
+        }
+    };
+    for (int p = 0; p < L->P; ++p)
+        for (int oc = 0; oc < L->c_out; ++oc) {
+            float* row = wf.data() + (static_cast<size_t>(p) * L->n_pad + oc) * L->k_total;
+            for (int s = 0; s < L->nseg; ++s) {
+                const bool merged = mode == 1 && L->seg_ntaps[s] == 4;
+                for (int t = 0; t < L->seg_ntaps[s]; ++t)
+                    for (int c = 0; c < L->seg_c[s]; ++c) {
+                        const int ic = seg_ch0[s] + c;
+                        float v;
+                        if (!merged) {
+                            v = tap(oc, ic, t / k, t % k);
+                        } else {
+                            int y0, y1, x0, x1;
+                            rows(p / 2, t / 2, &y0, &y1);
+                            rows(p % 2, t % 2, &x0, &x1);
+                            double acc = 0.0;
+                            for (int ky = y0; ky < y1; ++ky)
+                                for (int kx = x0; kx < x1; ++kx) acc += tap(oc, ic, ky, kx);
+                            v = static_cast<float>(acc);
+                        }
+                        row[L->seg_kbase[s] + t * L->seg_cpad[s] + c] = v;
+                    }
+            }
+        }
+    std::vector<__half> wh(nW);
+    for (size_t i = 0; i < nW; ++i) wh[i] = __float2half_rn(wf[i] * L->wscale);
+    L->w = dev_alloc(l, static_cast<int64_t>(nW * sizeof(__half)), false);
+    LC_CUDA(cudaMemcpy(L->w.p, wh.data(), nW * sizeof(__half), cudaMemcpyHostToDevice));
+
+    std::vector<float> bias(static_cast<size_t>(L->n_pad), 0.0f);
+    for (int oc = 0; oc < L->c_out; ++oc) bias[oc] = b.bias[oc];
+    L->bias = dev_alloc(l, L->n_pad * 4, false);
+    LC_CUDA(cudaMemcpy(L->bias.p, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice));
+
+    // conditioning-shift tables: sum of in-bound tap weights per class
+    const int rc = L->rc, rr = rc + 1, ncls = rr * rr * rr * rr;
+    std::vector<float> corr(static_cast<size_t>(L->P) * ncls * L->n_pad, 0.0f);
+    for (int p = 0; p < L->P; ++p)
+        for (int cls = 0; cls < ncls; ++cls) {
+            const int dt = cls / (rr * rr * rr), db = (cls / (rr * rr)) % rr;
+            const int dl = (cls / rr) % rr, dr = cls % rr;
+            int Ly, Y, Lx, X;
+            class_geom(dt, db, rc, &Ly, &Y);
+            class_geom(dl, dr, rc, &Lx, &X);
+            for (int oc = 0; oc < L->c_out; ++oc) {
+                const float* row = wf.data() + (static_cast<size_t>(p) * L->n_pad + oc) * L->k_total;
+                double acc = 0.0;
+                for (int s = 0; s < L->nseg; ++s) {
+                    const int m = L->seg_m[s];
+                    for (int t = 0; t < L->seg_ntaps[s]; ++t) {
+                        const int sy = Y * m + L->oy[s][p][t], sx = X * m + L->ox[s][p][t];
+                        if (sy < 0 || sy >= Ly * m || sx < 0 || sx >= Lx * m) continue;
+                        for (int c = 0; c < L->seg_c[s]; ++c) acc += row[L->seg_kbase[s] + t * L->seg_cpad[s] + c];
+                    }
+                }
+                corr[(static_cast<size_t>(p) * ncls + cls) * L->n_pad + oc] = static_cast<float>(acc);
+            }
+        }
+    L->corr = dev_alloc(l, static_cast<int64_t>(corr.size() * 4), false);
+    LC_CUDA(cudaMemcpy(L->corr.p, corr.data(), corr.size() * 4, cudaMemcpyHostToDevice));
+    return L;
+}
+
+std::unique_ptr<ThinLayer> pack_thin_layer(Ledger* l, const Bank& b) {
+    auto L = std::make_unique<ThinLayer>();
+    L->c_in = static_cast<int>(b.c_in);
+    L->c_out = static_cast<int>(b.c_out);
+    L->k = static_cast<int>(b.k);
+    L->w = dev_alloc(l, static_cast<int64_t>(b.taps.size() * 4), false);
+    LC_CUDA(cudaMemcpy(L->w.p, b.taps.data(), b.taps.size() * 4, cudaMemcpyHostToDevice));
+    L->bias = dev_alloc(l, static_cast<int64_t>(b.bias.size() * 4), false);
+    LC_CUDA(cudaMemcpy(L->bias.p, b.bias.data(), b.bias.size() * 4, cudaMemcpyHostToDevice));
+    return L;
+}
+
+// ------------------------------------------------------- conv launch
+void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window& win, float s,
+                 float o, bool silu, cudaStream_t st) {
+    ConvParams p;
+    std::memset(&p, 0, sizeof(p));
+    const int sub = L.mode == 1 ? 2 : 1;
+    p.ly0 = win.oy0 / sub;
+    p.ly1 = win.oy1 / sub;
+    p.lx0 = win.ox0 / sub;
+    p.lx1 = win.ox1 / sub;
+    p.cy0 = win.vy0 / sub;
+    p.cy1 = win.vy1 / sub;
+    p.cx0 = win.vx0 / sub;
+    p.cx1 = win.vx1 / sub;
+    const int Lh = p.ly1 - p.ly0, Lw = p.lx1 - p.lx0;
+    p.n_img = out.n;
+    p.TW = std::min(Lw, 128);
+    p.TH = std::max(1, std::min(Lh, 128 / p.TW));
+    p.TI = std::max(1, std::min(out.n, 128 / (p.TW * p.TH)));
+    p.tiles_x = (Lw + p.TW - 1) / p.TW;
+    p.tiles_y = (Lh + p.TH - 1) / p.TH;
+    p.tiles_i = (out.n + p.TI - 1) / p.TI;
+    p.nseg = L.nseg;
+    for (int sgi = 0; sgi < L.nseg; ++sgi) {
+        const Act& a = srcs[sgi];
+        const int m = L.seg_m[sgi];
+        // operand window in its own coordinates
+        const int scale_num = (L.mode == 1) ? m : 1;  // full-res skip: x2 of lattice, low-res: x1
+        const int wy0 = p.cy0 * scale_num, wy1 = p.cy1 * scale_num;
+        const int wx0 = p.cx0 * scale_num, wx1 = p.cx1 * scale_num;
+        const int wy0s = L.mode == 1 ? wy0 : win.vy0, wy1s = L.mode == 1 ? wy1 : win.vy1;
+        const int wx0s = L.mode == 1 ? wx0 : win.vx0, wx1s = L.mode == 1 ? wx1 : win.vx1;
+        const __half* base = a.p + (static_cast<int64_t>(wy0s) * a.w + wx0s) * a.cs;
+        const uint64_t dims[4] = {static_cast<uint64_t>(a.cs), static_cast<uint64_t>(wx1s - wx0s),
+                                  static_cast<uint64_t>(wy1s - wy0s), static_cast<uint64_t>(a.n)};
+        const uint64_t strides[3] = {static_cast<uint64_t>(a.cs) * 2,
+                                     static_cast<uint64_t>(a.w) * a.cs * 2,
+                                     static_cast<uint64_t>(a.h) * a.w * a.cs * 2};
+        const uint32_t box[4] = {64, static_cast<uint32_t>(p.TW * m), static_cast<uint32_t>(p.TH * m),
+                                 static_cast<uint32_t>(p.TI)};
+        const uint32_t estr[4] = {1, static_cast<uint32_t>(m), static_cast<uint32_t>(m), 1};
+        encode_map(&p.tmA[sgi], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, base, dims, strides, box, estr);
+        ConvSegDev& sd = p.seg[sgi];
+        sd.ntaps = L.seg_ntaps[sgi];
+        sd.ncb = L.seg_cpad[sgi] / 64;
+        sd.kbase = L.seg_kbase[sgi];
+        sd.mx = sd.my = m;
+        sd.wx0 = wx0s;
+        sd.wy0 = wy0s;
+        std::memcpy(sd.ox, L.ox[sgi], sizeof(sd.ox));
+        std::memcpy(sd.oy, L.oy[sgi], sizeof(sd.oy));
+    }
+    {
+        const uint64_t dims[3] = {static_cast<uint64_t>(L.k_total), static_cast<uint64_t>(L.n_pad),
+                                  static_cast<uint64_t>(L.P)};
+        const uint64_t strides[2] = {static_cast<uint64_t>(L.k_total) * 2,
+                                     static_cast<uint64_t>(L.n_pad) * L.k_total * 2};
+        const uint32_t box[3] = {64, static_cast<uint32_t>(L.BN), 1};
+        const uint32_t estr[3] = {1, 1, 1};
+        encode_map(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, L.w.p, dims, strides, box, estr);
+    }
+    p.BN = L.BN;
+    p.n_pad = L.n_pad;
+    p.c_out = L.c_out;
+    p.cs_out = out.cs;
+    p.out_h = out.h;
+    p.out_w = out.w;
+    p.sy = p.sx = sub;
+    for (int q = 0; q < 4; ++q) {
+        p.py[q] = L.mode == 1 ? q / 2 : 0;
+        p.px[q] = L.mode == 1 ? q % 2 : 0;
+    }
+    p.out = out.p;
+    p.bias = L.bias.as<float>();
+    p.corr = L.corr.as<float>();
+    p.rc = L.rc;
+    p.scale = s / L.wscale;
+    p.shift = o;
+    p.silu = silu ? 1 : 0;
+    LC_CUDA(launch_conv_tc(p, L.P, st));
+}
+
+// ---------------------------------------------------------------- engine
+Engine::Engine(int device) : device_(device) {
+    LC_CUDA(cudaSetDevice(device));
+    LC_CUDA(cudaStreamCreateWithFlags(&s_compute_, cudaStreamNonBlocking));
+    LC_CUDA(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking));
+    LC_CUDA(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking));
+    LC_CUDA(cudaEventCreate(&ev_base_));
+    for (int b = 0; b < 2; ++b) {
+        LC_CUDA(cudaEventCreateWithFlags(&ev_evict_[b], cudaEventDisableTiming));
+        LC_CUDA(cudaEventCreateWithFlags(&ev_prefetch_[b], cudaEventDisableTiming));
+    }
+    LC_CUDA(cudaEventCreateWithFlags(&ev_cache_ready_, cudaEventDisableTiming));
+}
+
+Engine::~Engine() {
+    cudaDeviceSynchronize();
+    for (auto e : ev_pool_) cudaEventDestroy(e);
+    cudaEventDestroy(ev_base_);
+    for (int b = 0; b < 2; ++b) {
+        cudaEventDestroy(ev_evict_[b]);
+        cudaEventDestroy(ev_prefetch_[b]);
+    }
+    cudaEventDestroy(ev_cache_ready_);
+    cudaStreamDestroy(s_compute_);
+    cudaStreamDestroy(s_d2h_);
+    cudaStreamDestroy(s_h2d_);
+}
+
+cudaEvent_t Engine::next_event() {
+    if (ev_next_ == ev_pool_.size()) {
+        cudaEvent_t e;
+        LC_CUDA(cudaEventCreate(&e));
+        ev_pool_.push_back(e);
+    }
+    return ev_pool_[ev_next_++];
+}
+
+void Engine::record(int kind, int step, int64_t bytes, cudaStream_t st) {
+    cudaEvent_t e = next_event();
+    LC_CUDA(cudaEventRecord(e, st));
+    marks_.push_back({kind, step, bytes, e});
+}
+
+static std::string weights_key(const RunConfig& c) {
+    return std::to_string(c.depth) + "/" + std::to_string(c.base_channels) + "/" + std::to_string(c.kernel) +
+           "/" + std::to_string(c.cache_depth) + "/" + std::to_string(c.in_channels) + "/" +
+           std::to_string(c.unet_seed) + "/" + std::to_string(c.stages) + "/" + std::to_string(c.codec_width) +
+           "/" + std::to_string(c.codec_seed);
+}
+
+void Engine::configure(const RunConfig& cfg) {
+    cfg.validate();
+    const std::string key = weights_key(cfg);
+    const bool same_weights = configured_ && key == cfg_key_;
+    const bool same_geom = configured_ && cfg.frames == cfg_.frames && cfg.height == cfg_.height &&
+                           cfg.width == cfg_.width && same_weights &&
+                           cfg.cache_enabled == cfg_.cache_enabled;
+    cfg_ = cfg;
+    ledger_.budget_fast = 0;  // budget applies to runs, see run()
+    if (!same_weights) {
+        ledger_.enter(kSetup);
+        uw_ = init_unet(cfg);
+        cw_ = init_codec(cfg);
+        const auto plan = block_plans(cfg);
+        tc_.clear();
+        tc_.resize(plan.size());
+        tc_fb_.clear();
+        tc_fb_.resize(plan.size());
+        for (size_t j = 0; j < plan.size(); ++j) {
+            const auto& bp = plan[j];
+            if (bp.name == "stem" || bp.name == "head") continue;
+            if (bp.name[0] == 'u') {
+                const int i = std::stoi(bp.name.substr(1));
+                const int c_skip = static_cast<int>(cfg.base_channels << i);
+                if (cfg.kernel == 3) tc_[j] = pack_tc_layer(&ledger_, uw_.banks[j], c_skip, 1);
+                tc_fb_[j] = pack_tc_layer(&ledger_, uw_.banks[j], c_skip, 0);
+            } else {
+                tc_[j] = pack_tc_layer(&ledger_, uw_.banks[j], static_cast<int>(bp.c_in), 0);
+            }
+        }
+        stem_ = pack_thin_layer(&ledger_, uw_.banks.front());
+        head_ = pack_thin_layer(&ledger_, uw_.banks.back());
+        dec0_ = pack_thin_layer(&ledger_, cw_.dec[0]);
+        dec_last_ = pack_thin_layer(&ledger_, cw_.dec[static_cast<size_t>(cfg.stages)]);
+        dec_tc_.clear();
+        for (int64_t i = 1; i < cfg.stages; ++i) dec_tc_.push_back(pack_tc_layer(&ledger_, cw_.dec[i], 0, 1));
+        cfg_key_ = key;
+        T_alloc_ = -1;
+        dec_alloc_ = -1;
+    }
+    if (!same_geom) T_alloc_ = -1;
+    configured_ = true;
+}
+
+int64_t Engine::latent_elems() const {
+    return cfg_.frames * cfg_.latent_channels * cfg_.latent_h() * cfg_.latent_w();
+}
+int64_t Engine::video_elems() const { return cfg_.frames * cfg_.image_channels * cfg_.height * cfg_.width; }
+
+void Engine::alloc_activations(int64_t T) {
+    if (T_alloc_ == T) return;
+    act_bufs_.clear();
+    cache_buf_.reset();
+    cache_host_.reset();
+    const int n = static_cast<int>(2 * T);
+    const int M = static_cast<int>(cfg_.depth), m = static_cast<int>(cfg_.cache_depth);
+    const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
+    auto ch = [&](int l) { return static_cast<int>(cfg_.base_channels << l); };
+    auto make = [&](int h, int w, int c) {
+        Act a;
+        a.n = n;
+        a.h = h;
+        a.w = w;
+        a.c = c;
+        a.cs = round_up(c, 64);
+        act_bufs_.push_back(dev_alloc(&ledger_, a.elems() * 2, true));
+        a.p = act_bufs_.back().as<__half>();
+        return a;
+    };
+    lv_.assign(static_cast<size_t>(M + 1), Level{});
+    stem_out_ = make(lh, lw, ch(0));
+    for (int i = 0; i < M; ++i) {
+        const int h = lh >> i, w = lw >> i;
+        lv_[i].D = make(h, w, ch(i));
+        if (i >= 1) lv_[i].P = make(h, w, ch(i - 1));
+        if (!(cfg_.cache_enabled && i == m + 1)) lv_[i].U = make(h, w, ch(i));
+        const int cu = (i == M - 1) ? ch(M - 1) : ch(i + 1);
+        if (cfg_.kernel != 3 || (cfg_.chunk_enabled && cfg_.halo != HaloKind::Exact))
+            lv_[i].UP = make(h, w, cu);
+    }
+    lv_[M].P = make(lh >> M, lw >> M, ch(M - 1));
+    if (!(cfg_.cache_enabled && m + 1 == M)) mid_ = make(lh >> M, lw >> M, ch(M - 1));
+    if (cfg_.cache_enabled) {
+        const int cc = static_cast<int>(cache_channels(cfg_));
+        Act a;
+        a.n = n;
+        a.h = lh >> (m + 1);
+        a.w = lw >> (m + 1);
+        a.c = cc;
+        a.cs = round_up(cc, 64);
+        cache_buf_ = dev_alloc(&ledger_, a.elems() * 2, true);
+        a.p = cache_buf_.as<__half>();
+        cache_ = a;
+        if (m + 1 == M) mid_ = a;
+        else lv_[m + 1].U = a;
+        if (cfg_.swap_mode != SwapMode::Off) cache_host_ = host_alloc(&ledger_, a.elems() * 2);
+    }
+    const int64_t nl = T * cfg_.latent_channels * lh * lw;
+    x_ = dev_alloc(&ledger_, nl * 4, true);
+    xn_ = dev_alloc(&ledger_, nl * 4, true);
+    z_ = dev_alloc(&ledger_, nl * 4, true);
+    eps2_ = dev_alloc(&ledger_, 2 * nl * 4, true);
+    bad_ = dev_alloc(&ledger_, 16, true);
+    video_ = dev_alloc(&ledger_, T * cfg_.image_channels * cfg_.height * cfg_.width * 4, false);
+    T_alloc_ = T;
+}
+
+// Chunk windows for a block at a level (proj/src/chunk.cpp:145-181 split,
+// :69-92 plan_windows): output core + effective readable window.
+static std::vector<Window> block_windows(const RunConfig& c, const std::string& name, int h, int w) {
+    const bool chunked =
+        c.chunk_enabled && std::find(c.targets.begin(), c.targets.end(), name) != c.targets.end();
+    if (!chunked) return {Window{0, h, 0, w, 0, h, 0, w}};
+    int64_t halo = 0;
+    const auto tiles = split(h, w, c.eta, c.omega, c.halo, c.halo_px, c.kernel, &halo);
+    const int64_t r = (c.kernel - 1) / 2;
+    std::vector<Window> out;
+    for (const Tile& t : tiles) {
+        Window wd;
+        wd.oy0 = static_cast<int>(t.core.y0);
+        wd.oy1 = static_cast<int>(t.core.y1);
+        wd.ox0 = static_cast<int>(t.core.x0);
+        wd.ox1 = static_cast<int>(t.core.x1);
+        if (halo >= r) {
+            wd.vy0 = 0, wd.vy1 = h, wd.vx0 = 0, wd.vx1 = w;
+        } else {
+            wd.vy0 = static_cast<int>(std::max<int64_t>(t.core.y0 - halo, 0));
+            wd.vy1 = static_cast<int>(std::min<int64_t>(t.core.y1 + halo, h));
+            wd.vx0 = static_cast<int>(std::max<int64_t>(t.core.x0 - halo, 0));
+            wd.vx1 = static_cast<int>(std::min<int64_t>(t.core.x1 + halo, w));
+        }
+        out.push_back(wd);
+    }
+    return out;
+}
+
+void Engine::conv_block(int j, const Act& in, const Act& out, float s, float o, bool silu) {
+    const auto plan = block_plans(cfg_);
+    for (const Window& wd : block_windows(cfg_, plan[j].name, in.h, in.w)) {
+        run_tc_conv(*tc_[j], &in, out, wd, s, o, silu, s_compute_);
+        ++launches;
+    }
+}
+
+void Engine::up_block(int i, const Act& skip, const Act& u, const Act& out, float s, float o) {
+    const int j = static_cast<int>(block_index(cfg_, "u" + std::to_string(i)));
+    const auto wins = block_windows(cfg_, "u" + std::to_string(i), skip.h, skip.w);
+    bool subpixel = tc_[j] != nullptr;
+    for (const Window& wd : wins)
+        if ((wd.vy0 | wd.vy1 | wd.vx0 | wd.vx1 | wd.oy0 | wd.oy1 | wd.ox0 | wd.ox1) & 1) subpixel = false;
+    if (subpixel) {
+        const Act srcs[2] = {skip, u};
+        for (const Window& wd : wins) {
+            run_tc_conv(*tc_[j], srcs, out, wd, s, o, true, s_compute_);
+            ++launches;
+        }
+        return;
+    }
+    // Fallback: materialise the nearest upsample, then a two-segment conv.
+    const Act& up = lv_[i].UP;
+    if (!up.p) throw_invariant("upsample buffer missing for fallback path");
+    LC_CUDA(launch_up2(u.p, up.p, u.n, u.h, u.w, u.cs, s_compute_));
+    ++launches;
+    const Act srcs[2] = {skip, up};
+    for (const Window& wd : wins) {
+        run_tc_conv(*tc_fb_[j], srcs, out, wd, s, o, true, s_compute_);
+        ++launches;
+    }
+}
+
+void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t timestep, bool full,
+                         float* eps2_dev, int step, int seam) {
+    const int M = static_cast<int>(cfg_.depth), m = static_cast<int>(cfg_.cache_depth);
+    const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
+    auto cond = [&](int j, float* s, float* o) { block_conditioning(uw_, j, timestep, s, o); };
+    float s, o;
+    // stem: CFG pair built on the fly (pipeline.cpp:127-131), affine + conv + SiLU
+    {
+        const int j = 0;
+        cond(j, &s, &o);
+        for (const Window& wd : block_windows(cfg_, "stem", lh, lw)) {
+            ThinInArgs a{};
+            a.x = x_dev;
+            a.nsrc = static_cast<int>(stacked ? 2 * T : T);
+            a.c_in = stem_->c_in;
+            a.H = lh;
+            a.W = lw;
+            a.cfg_pair = stacked ? 0 : 1;
+            a.cond_bias = 0.15f;
+            a.s = s;
+            a.o = o;
+            a.apply_affine = 1;
+            a.w = stem_->w.as<float>();
+            a.bias = stem_->bias.as<float>();
+            a.c_out = stem_->c_out;
+            a.k = stem_->k;
+            a.silu = 1;
+            a.out = stem_out_.p;
+            a.cs_out = stem_out_.cs;
+            a.win = wd;
+            LC_CUDA(launch_thin_in(a, s_compute_));
+            ++launches;
+        }
+    }
+    cond(1, &s, &o);
+    conv_block(1, stem_out_, lv_[0].D, s, o, true);
+    const int deepest = full ? M - 1 : m;
+    for (int i = 1; i <= deepest; ++i) {
+        const Act& prev = lv_[i - 1].D;
+        LC_CUDA(launch_down2(prev.p, lv_[i].P.p, prev.n, prev.h, prev.w, prev.cs, s_compute_));
+        ++launches;
+        cond(1 + i, &s, &o);
+        conv_block(1 + i, lv_[i].P, lv_[i].D, s, o, true);
+    }
+    // U_l holder: output of u_l (l < M) or mid (l == M); the cache slot when
+    // l == m+1 and caching is on.
+    auto U_of = [&](int l) -> const Act& { return l == M ? mid_ : lv_[l].U; };
+    const bool writes_cache = full && cfg_.cache_enabled;
+    if (writes_cache && evict_pending_) {
+        // CacheStore::store awaits pending transfers before replacing
+        // entries (cache.cpp:48-52).
+        for (int b = 0; b < 2; ++b) LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_evict_[b], 0));
+        evict_pending_ = false;
+    }
+    if (full) {
+        const Act& prev = lv_[M - 1].D;
+        LC_CUDA(launch_down2(prev.p, lv_[M].P.p, prev.n, prev.h, prev.w, prev.cs, s_compute_));
+        ++launches;
+        cond(1 + M, &s, &o);
+        conv_block(1 + M, lv_[M].P, mid_, s, o, true);
+    } else if (seam > 0) {
+        seam_await(step);
+        // last consumer: evict_all right after assemble (pipeline.cpp:156-160)
+        if (seam == 2) issue_evict(step);
+    }
+    const int top = full ? M - 1 : m;
+    for (int i = top; i >= 0; --i) {
+        const int j = static_cast<int>(block_index(cfg_, "u" + std::to_string(i)));
+        cond(j, &s, &o);
+        up_block(i, lv_[i].D, U_of(i + 1), i == 0 ? lv_[0].U : U_of(i), s, o);
+    }
+    // head: affine + conv, no SiLU -> eps (2,T,C,h,w) fp32
+    {
+        const int j = static_cast<int>(block_index(cfg_, "head"));
+        cond(j, &s, &o);
+        for (const Window& wd : block_windows(cfg_, "head", lh, lw)) {
+            ThinOutArgs a{};
+            a.x = lv_[0].U.p;
+            a.nimg = lv_[0].U.n;
+            a.Hin = lh;
+            a.Win = lw;
+            a.cs_in = lv_[0].U.cs;
+            a.c_in = head_->c_in;
+            a.up2 = 0;
+            a.s = s;
+            a.o = o;
+            a.apply_affine = 1;
+            a.w = head_->w.as<float>();
+            a.bias = head_->bias.as<float>();
+            a.c_out = head_->c_out;
+            a.k = head_->k;
+            a.out = eps2_dev;
+            a.win = wd;
+            LC_CUDA(launch_thin_out(a, s_compute_));
+            ++launches;
+        }
+    }
+}
+
+void Engine::issue_evict(int step) {
+    if (!cache_host_.p) return;
+    const bool async = cfg_.swap_mode == SwapMode::Async;
+    cudaStream_t st = async ? s_d2h_ : s_compute_;
+    LC_CUDA(cudaEventRecord(ev_cache_ready_, s_compute_));
+    if (async) LC_CUDA(cudaStreamWaitEvent(st, ev_cache_ready_, 0));
+    const int64_t half = cache_.elems();  // halves in elements of one branch (n = 2T)
+    const int64_t bytes = half;           // elems()*2 bytes / 2 branches
+    for (int b = 0; b < 2; ++b) {
+        record(2, step, bytes, st);
+        LC_CUDA(cudaMemcpyAsync(cache_host_.as<char>() + b * bytes, reinterpret_cast<char*>(cache_.p) + b * bytes,
+                                static_cast<size_t>(bytes), cudaMemcpyDeviceToHost, st));
+        record(3, step, bytes, st);
+        LC_CUDA(cudaEventRecord(ev_evict_[b], st));
+        if (stats_) {
+            stats_->swap_bytes += bytes;
+        }
+    }
+    if (stats_) stats_->swap_calls += 1;
+    evict_pending_ = true;
+}
+
+void Engine::issue_prefetch(int issued, int needed) {
+    (void)issued;
+    if (!cache_host_.p) return;
+    const bool async = cfg_.swap_mode == SwapMode::Async;
+    cudaStream_t st = async ? s_h2d_ : s_compute_;
+    const int64_t bytes = cache_.elems();
+    for (int b = 0; b < 2; ++b) {
+        if (async) LC_CUDA(cudaStreamWaitEvent(st, ev_evict_[b], 0));
+        record(2, needed, bytes, st);
+        LC_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(cache_.p) + b * bytes, cache_host_.as<char>() + b * bytes,
+                                static_cast<size_t>(bytes), cudaMemcpyHostToDevice, st));
+        record(3, needed, bytes, st);
+        LC_CUDA(cudaEventRecord(ev_prefetch_[b], st));
+        if (stats_) stats_->swap_bytes += bytes;
+    }
+    if (stats_) stats_->swap_calls += 1;
+    prefetch_pending_ = true;
+}
+
+void Engine::seam_await(int step) {
+    // CacheStore::assemble -> fetch -> await_ready (cache.cpp:65-90): the
+    // compute stream waits for the prefetch only here, after the shallow path.
+    for (int b = 0; b < 2; ++b) {
+        record(4, step, 0, s_compute_);
+        if (prefetch_pending_) LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_prefetch_[b], 0));
+        record(5, step, 0, s_compute_);
+    }
+    prefetch_pending_ = false;
+}
+
+void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
+    const int S = static_cast<int>(cfg_.stages);
+    const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
+    const int G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cfg_.slice_decode ? decode_slice : n, n)));
+    if (dec_alloc_ != G) {
+        dec_bufs_.clear();
+        for (int i = 0; i < S; ++i) {
+            Act a;
+            a.n = G;
+            a.h = lh << i;
+            a.w = lw << i;
+            a.c = static_cast<int>(cfg_.codec_width);
+            a.cs = round_up(a.c, 64);
+            dec_bufs_.push_back(dev_alloc(&ledger_, a.elems() * 2, true));
+            a.p = dec_bufs_.back().as<__half>();
+            dec_act_[i] = a;
+        }
+        dec_alloc_ = G;
+    }
+    const int C = static_cast<int>(cfg_.latent_channels), IC = static_cast<int>(cfg_.image_channels);
+    const int H = static_cast<int>(cfg_.height), W = static_cast<int>(cfg_.width);
+    for (int64_t g0 = 0; g0 < n; g0 += G) {
+        const int gs = static_cast<int>(std::min<int64_t>(G, n - g0));
+        Act e[8];
+        for (int i = 0; i < S; ++i) {
+            e[i] = dec_act_[i];
+            e[i].n = gs;
+        }
+        ThinInArgs a{};
+        a.x = lat_dev + g0 * C * lh * lw;
+        a.nsrc = gs;
+        a.c_in = C;
+        a.H = lh;
+        a.W = lw;
+        a.cfg_pair = 0;
+        a.s = 1.0f;
+        a.o = 0.0f;
+        a.apply_affine = 0;
+        a.w = dec0_->w.as<float>();
+        a.bias = dec0_->bias.as<float>();
+        a.c_out = dec0_->c_out;
+        a.k = 3;
+        a.silu = 1;
+        a.out = e[0].p;
+        a.cs_out = e[0].cs;
+        a.win = Window{0, lh, 0, lw, 0, lh, 0, lw};
+        LC_CUDA(launch_thin_in(a, s_compute_));
+        ++launches;
+        for (int i = 1; i < S; ++i) {
+            const int h = lh << i, w = lw << i;
+            run_tc_conv(*dec_tc_[i - 1], &e[i - 1], e[i], Window{0, h, 0, w, 0, h, 0, w}, 1.0f, 0.0f, true,
+                        s_compute_);
+            ++launches;
+        }
+        ThinOutArgs t{};
+        t.x = e[S - 1].p;
+        t.nimg = gs;
+        t.Hin = lh << (S - 1);
+        t.Win = lw << (S - 1);
+        t.cs_in = e[S - 1].cs;
+        t.c_in = static_cast<int>(cfg_.codec_width);
+        t.up2 = 1;
+        t.s = 1.0f;
+        t.o = 0.0f;
+        t.apply_affine = 0;
+        t.w = dec_last_->w.as<float>();
+        t.bias = dec_last_->bias.as<float>();
+        t.c_out = IC;
+        t.k = 3;
+        t.out = video_dev + g0 * IC * H * W;
+        t.win = Window{0, H, 0, W, 0, H, 0, W};
+        LC_CUDA(launch_thin_out(t, s_compute_));
+        ++launches;
+    }
+}
+
+RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host, bool resident_input) {
+    if (cfg_.mode != "text") throw_config("run.mode=image: the encode stage is not built on the GPU path yet");
+    RunStats st;
+    stats_ = &st;
+    marks_.clear();
+    ev_next_ = 0;
+    launches = 0;
+    const int64_t T = cfg_.frames;
+    alloc_activations(T);
+    ledger_.budget_fast = cfg_.budget_fast_bytes;
+    if (cfg_.budget_fast_bytes > 0 && ledger_.occ[0] > cfg_.budget_fast_bytes)
+        throw LcError(kBudgetError, "fast-tier budget exceeded in stage denoise: " +
+                                        std::to_string(ledger_.occ[0]) + " > " +
+                                        std::to_string(cfg_.budget_fast_bytes) + " bytes");
+    const Schedule sc = make_schedule(cfg_);
+    const StepPlan plan = cfg_.cache_enabled ? plan_steps(cfg_.steps, cfg_.cache_n)
+                                             : StepPlan{std::vector<bool>(static_cast<size_t>(cfg_.steps), true)};
+    const int64_t nl = latent_elems();
+    const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
+    const bool swap = cfg_.cache_enabled && cfg_.swap_mode != SwapMode::Off;
+    evict_pending_ = prefetch_pending_ = false;
+
+    LC_CUDA(cudaEventRecord(ev_base_, s_compute_));
+    cudaEvent_t t_start = next_event(), t_den0 = next_event(), t_den1 = next_event(), t_end = next_event();
+    LC_CUDA(cudaEventRecord(t_start, s_compute_));
+    ledger_.enter(kEncode);
+    if (!resident_input) {
+        std::vector<float> gen;
+        const float* src = x0_host;
+        if (!src) {
+            gen.resize(static_cast<size_t>(nl));
+            randn(derive_seed(cfg_.seed, 1), nl, gen.data());
+            src = gen.data();
+        }
+        LC_CUDA(cudaMemcpyAsync(x_.p, src, static_cast<size_t>(nl) * 4, cudaMemcpyHostToDevice, s_compute_));
+        if (!x0_host) LC_CUDA(cudaStreamSynchronize(s_compute_));
+    }
+    LC_CUDA(cudaMemsetAsync(bad_.p, 0, 16, s_compute_));
+    LC_CUDA(launch_isfinite(x_.as<float>(), nl, bad_.as<int>(), s_compute_));
+    ++launches;
+
+    ledger_.enter(kDenoise);
+    LC_CUDA(cudaEventRecord(t_den0, s_compute_));
+    st.macs_full = flops_estimate(cfg_, 2, T, lh, lw, false);
+    st.macs_cached = flops_estimate(cfg_, 2, T, lh, lw, true);
+    const int64_t S = cfg_.steps;
+    std::vector<float> znoise;
+    for (int64_t s = 0; s < S; ++s) {
+        const int64_t j = S - 1 - s;
+        const int64_t t_orig = sc.src[j];
+        const bool full = plan.is_full(s);
+        record(0, static_cast<int>(s), 0, s_compute_);
+        const int seam = (!full && swap) ? (plan.is_last_consumer(s) ? 2 : 1) : 0;
+        forward_dev(x_.as<float>(), false, T, t_orig, full, eps2_.as<float>(), static_cast<int>(s), seam);
+        record(1, static_cast<int>(s), 0, s_compute_);
+        if (full) {
+            st.full_steps++;
+            st.denoiser_macs += st.macs_full;
+            if (swap) {
+                issue_evict(static_cast<int>(s));
+                if (plan.has_consumers(s)) issue_prefetch(static_cast<int>(s), static_cast<int>(s + 1));
+            }
+        } else {
+            st.cached_steps++;
+            st.denoiser_macs += st.macs_cached;
+        }
+        const StepCoeffs k = step_coeffs(cfg_, sc, s);
+        if (k.has_noise) {
+            znoise.resize(static_cast<size_t>(nl));
+            randn(k.noise_seed, nl, znoise.data());
+            LC_CUDA(cudaMemcpyAsync(z_.p, znoise.data(), static_cast<size_t>(nl) * 4, cudaMemcpyHostToDevice,
+                                    s_compute_));
+            LC_CUDA(cudaStreamSynchronize(s_compute_));
+        }
+        StepArgs a{};
+        a.eps2 = eps2_.as<float>();
+        a.x = x_.as<float>();
+        a.x_out = xn_.as<float>();
+        a.z = k.has_noise ? z_.as<float>() : nullptr;
+        a.n = nl;
+        a.g = static_cast<float>(cfg_.guidance);
+        a.a = k.a;
+        a.b = k.b;
+        a.c = k.noise;
+        a.bad = bad_.as<int>();
+        LC_CUDA(launch_step(a, s_compute_));
+        ++launches;
+        std::swap(x_, xn_);
+    }
+    LC_CUDA(cudaEventRecord(t_den1, s_compute_));
+    ledger_.enter(kDecode);
+    decode_dev(x_.as<float>(), T, video_.as<float>());
+    LC_CUDA(cudaEventRecord(t_end, s_compute_));
+    if (video_host)
+        LC_CUDA(cudaMemcpyAsync(video_host, video_.p, static_cast<size_t>(video_elems()) * 4,
+                                cudaMemcpyDeviceToHost, s_compute_));
+    if (latent_host)
+        LC_CUDA(cudaMemcpyAsync(latent_host, x_.p, static_cast<size_t>(nl) * 4, cudaMemcpyDeviceToHost,
+                                s_compute_));
+    int bad = 0;
+    LC_CUDA(cudaMemcpyAsync(&bad, bad_.p, 4, cudaMemcpyDeviceToHost, s_compute_));
+    LC_CUDA(cudaStreamSynchronize(s_compute_));
+    LC_CUDA(cudaStreamSynchronize(s_d2h_));
+    LC_CUDA(cudaStreamSynchronize(s_h2d_));
+    stats_ = nullptr;
+    if (bad) throw_shape("denoiser input contains non-finite values");
+
+    float ms = 0;
+    LC_CUDA(cudaEventElapsedTime(&ms, t_den0, t_den1));
+    st.ms_denoise = ms;
+    LC_CUDA(cudaEventElapsedTime(&ms, t_den1, t_end));
+    st.ms_decode = ms;
+    LC_CUDA(cudaEventElapsedTime(&ms, t_start, t_end));
+    st.ms_total = ms;
+    double open = 0, lo = 1e30, hi = -1e30;
+    for (const Mark& mk : marks_) {
+        float t = 0;
+        LC_CUDA(cudaEventElapsedTime(&t, ev_base_, mk.ev));
+        st.timeline.push_back({static_cast<double>(mk.kind), static_cast<double>(mk.step),
+                               static_cast<double>(mk.bytes), static_cast<double>(t)});
+        lo = std::min(lo, static_cast<double>(t));
+        hi = std::max(hi, static_cast<double>(t));
+        if (mk.kind == 4) open = t;
+        if (mk.kind == 5) st.stall_ms += t - open;
+    }
+    st.makespan_ms = marks_.empty() ? 0.0 : hi - lo;
+    st.cache_bytes_planned = cfg_.cache_enabled
+                                 ? 2 * T * cache_channels(cfg_) * (lh >> cfg_.cache_depth) *
+                                       (lw >> cfg_.cache_depth) * 4
+                                 : 0;
+    st.cache_bytes_physical = cfg_.cache_enabled ? cache_.elems() * 2 : 0;
+    std::memcpy(st.peak, ledger_.peak, sizeof(st.peak));
+    st.hbm_peak = 0;
+    for (int s = 0; s < 4; ++s) st.hbm_peak = std::max(st.hbm_peak, ledger_.peak[s][0]);
+    st.kernel_launches = launches;
+    ledger_.enter(kSetup);
+    return st;
+}
+
+void Engine::forward(const float* x_host, int64_t T, int64_t timestep, const float* deep_in_ref,
+                     float* deep_out_ref, float* eps_host) {
+    RunConfig c = cfg_;
+    if (c.frames != T) {
+        c.frames = T;
+        configure(c);
+    }
+    alloc_activations(T);
+    const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
+    const int C = static_cast<int>(cfg_.latent_channels);
+    const int64_t n1 = T * C * lh * lw;
+    // explicit (2,T,...) input: the stem reads both halves as given.
+    DevBuf xin = dev_alloc(nullptr, 2 * n1 * 4, false);
+    LC_CUDA(cudaMemcpy(xin.p, x_host, static_cast<size_t>(2 * n1) * 4, cudaMemcpyHostToDevice));
+    const bool full = deep_in_ref == nullptr;
+    if (!cfg_.cache_enabled) throw_config("forward(): cache.enabled must be true for seam access");
+    if (!full) {
+        // reference u_next = upsample2(U_{m+1}); keep every other pixel (exact).
+        const int m = static_cast<int>(cfg_.cache_depth);
+        const Act& a = cache_;
+        std::vector<__half> hbuf(static_cast<size_t>(a.elems()), __float2half_rn(0.0f));
+        const int Hr = lh >> m, Wr = lw >> m;
+        for (int n = 0; n < a.n; ++n)
+            for (int c2 = 0; c2 < a.c; ++c2)
+                for (int y = 0; y < a.h; ++y)
+                    for (int x = 0; x < a.w; ++x)
+                        hbuf[((static_cast<size_t>(n) * a.h + y) * a.w + x) * a.cs + c2] = __float2half_rn(
+                            deep_in_ref[((static_cast<size_t>(n) * a.c + c2) * Hr + 2 * y) * Wr + 2 * x]);
+        LC_CUDA(cudaMemcpy(a.p, hbuf.data(), hbuf.size() * 2, cudaMemcpyHostToDevice));
+    }
+    forward_dev(xin.as<float>(), true, T, timestep, full, eps2_.as<float>(), 0, 0);
+    LC_CUDA(cudaStreamSynchronize(s_compute_));
+    LC_CUDA(cudaMemcpy(eps_host, eps2_.p, static_cast<size_t>(2 * n1) * 4, cudaMemcpyDeviceToHost));
+    if (full && deep_out_ref) {
+        const int m = static_cast<int>(cfg_.cache_depth);
+        const Act& a = cache_;
+        std::vector<__half> hbuf(static_cast<size_t>(a.elems()));
+        LC_CUDA(cudaMemcpy(hbuf.data(), a.p, hbuf.size() * 2, cudaMemcpyDeviceToHost));
+        const int Hr = lh >> m, Wr = lw >> m;
+        for (int n = 0; n < a.n; ++n)
+            for (int c2 = 0; c2 < a.c; ++c2)
+                for (int y = 0; y < Hr; ++y)
+                    for (int x = 0; x < Wr; ++x)
+                        deep_out_ref[((static_cast<size_t>(n) * a.c + c2) * Hr + y) * Wr + x] = __half2float(
+                            hbuf[((static_cast<size_t>(n) * a.h + y / 2) * a.w + x / 2) * a.cs + c2]);
+    }
+}
+
+void Engine::decode(const float* lat_host, int64_t n, float* video_host, int64_t slice) {
+    const int C = static_cast<int>(cfg_.latent_channels);
+    const int64_t nl = n * C * cfg_.latent_h() * cfg_.latent_w();
+    const int64_t nv = n * cfg_.image_channels * cfg_.height * cfg_.width;
+    DevBuf lat = dev_alloc(nullptr, nl * 4, false);
+    DevBuf vid = dev_alloc(nullptr, nv * 4, false);
+    LC_CUDA(cudaMemcpy(lat.p, lat_host, static_cast<size_t>(nl) * 4, cudaMemcpyHostToDevice));
+    const int64_t keep = decode_slice;
+    decode_slice = slice;
+    const bool keep_sliced = cfg_.slice_decode;
+    cfg_.slice_decode = true;
+    dec_alloc_ = -1;
+    decode_dev(lat.as<float>(), n, vid.as<float>());
+    decode_slice = keep;
+    cfg_.slice_decode = keep_sliced;
+    dec_alloc_ = -1;
+    LC_CUDA(cudaStreamSynchronize(s_compute_));
+    LC_CUDA(cudaMemcpy(video_host, vid.p, static_cast<size_t>(nv) * 4, cudaMemcpyDeviceToHost));
+}
+
+}  // namespace lc
+
+namespace lc {
+
+void Engine::decode_sharded(const float* lat_host, int64_t T, int64_t slice, float* video_host,
+                            ncclComm_t comm, int world, int rank, float* ms_out) {
+    const int C = static_cast<int>(cfg_.latent_channels);
+    const int64_t lat_frame = C * cfg_.latent_h() * cfg_.latent_w();
+    const int64_t vid_frame = cfg_.image_channels * cfg_.height * cfg_.width;
+    const int64_t per = (T + world - 1) / world;
+    auto shard = [&](int r, int64_t* f0, int64_t* cnt) {
+        *f0 = std::min<int64_t>(T, per * r);
+        *cnt = std::min<int64_t>(T, *f0 + per) - *f0;
+    };
+    int64_t f0, cnt;
+    shard(rank, &f0, &cnt);
+    DevBuf lat = dev_alloc(nullptr, std::max<int64_t>(1, cnt) * lat_frame * 4, false);
+    DevBuf vid = dev_alloc(nullptr, T * vid_frame * 4, false);
+    if (cnt > 0)
+        LC_CUDA(cudaMemcpy(lat.p, lat_host + f0 * lat_frame, static_cast<size_t>(cnt * lat_frame) * 4,
+                           cudaMemcpyHostToDevice));
+    const int64_t keep = decode_slice;
+    const bool keep_sliced = cfg_.slice_decode;
+    decode_slice = slice;
+    cfg_.slice_decode = true;
+    dec_alloc_ = -1;
+    cudaEvent_t e0, e1;
+    LC_CUDA(cudaEventCreate(&e0));
+    LC_CUDA(cudaEventCreate(&e1));
+    LC_CUDA(cudaEventRecord(e0, s_compute_));
+    if (cnt > 0) decode_dev(lat.as<float>(), cnt, vid.as<float>() + f0 * vid_frame);
+    if (world > 1) {
+        // gather to rank 0: grouped point-to-point (ncclGather equivalent
+        // for uneven shards such as 25 frames over 8 GPUs = 4 + 7x3)
+        if (ncclGroupStart() != ncclSuccess) throw LcError(kCudaError, "ncclGroupStart");
+        if (rank == 0) {
+            for (int r = 1; r < world; ++r) {
+                int64_t g0, gc;
+                shard(r, &g0, &gc);
+                if (gc > 0 &&
+                    ncclRecv(vid.as<float>() + g0 * vid_frame, static_cast<size_t>(gc * vid_frame), ncclFloat,
+                             r, comm, s_compute_) != ncclSuccess)
+                    throw LcError(kCudaError, "ncclRecv");
+            }
+        } else if (cnt > 0) {
+            if (ncclSend(vid.as<float>() + f0 * vid_frame, static_cast<size_t>(cnt * vid_frame), ncclFloat, 0,
+                         comm, s_compute_) != ncclSuccess)
+                throw LcError(kCudaError, "ncclSend");
+        }
+        if (ncclGroupEnd() != ncclSuccess) throw LcError(kCudaError, "ncclGroupEnd");
+    }
+    LC_CUDA(cudaEventRecord(e1, s_compute_));
+    LC_CUDA(cudaStreamSynchronize(s_compute_));
+    float ms = 0;
+    LC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (ms_out) *ms_out = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    decode_slice = keep;
+    cfg_.slice_decode = keep_sliced;
+    dec_alloc_ = -1;
+    if (rank == 0 && video_host)
+        LC_CUDA(cudaMemcpy(video_host, vid.p, static_cast<size_t>(T * vid_frame) * 4, cudaMemcpyDeviceToHost));
+}
+
+}  // namespace lc

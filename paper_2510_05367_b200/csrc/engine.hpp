@@ -1,0 +1,219 @@
+// GPU execution engine for the LightCache path: packed weights, device
+// buffers, streams, the denoise loop with the feature cache and its
+// asynchronous host swap, chunked execution and sliced decode.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <array>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "conv_tc.cuh"
+#include "host.hpp"
+#include "kernels.cuh"
+
+namespace lc {
+
+void cuda_check(cudaError_t e, const char* what);
+#define LC_CUDA(x) ::lc::cuda_check((x), #x)
+
+// ---------------------------------------------------------------- ledger
+// Physical memory accounting per (stage, tier): Fast = HBM bytes allocated
+// by the engine, Slow = pinned host bytes (cf. MemLedger,
+// proj/include/stagecache/ledger.hpp:69-146; peaks per stage, fast budget).
+enum Stage { kSetup = 0, kEncode = 1, kDenoise = 2, kDecode = 3 };
+struct Ledger {
+    int stage = kSetup;
+    int64_t occ[2] = {0, 0};
+    int64_t peak[4][2] = {};
+    int64_t budget_fast = 0;
+    void enter(int s);
+    void alloc(int tier, int64_t bytes);
+    void free(int tier, int64_t bytes);
+};
+
+struct DevBuf {
+    void* p = nullptr;
+    int64_t bytes = 0;
+    Ledger* ledger = nullptr;
+    int tier = 0;  // 0 device, 1 pinned host
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept { *this = std::move(o); }
+    DevBuf& operator=(DevBuf&& o) noexcept;
+    ~DevBuf() { reset(); }
+    void reset();
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+DevBuf dev_alloc(Ledger* l, int64_t bytes, bool zero = true);
+DevBuf host_alloc(Ledger* l, int64_t bytes);
+
+// fp16 NHWC activation view.
+struct Act {
+    __half* p = nullptr;
+    int n = 0, h = 0, w = 0, cs = 0, c = 0;
+    int64_t elems() const { return static_cast<int64_t>(n) * h * w * cs; }
+};
+
+// ------------------------------------------------------- tensor-core layer
+// One conv bank packed for conv_tc: fp16 weights [P][n_pad][K], bias, and
+// the conditioning-shift border tables.  mode 0: regular taps (segments =
+// channel split of c_in); mode 1: sub-pixel nearest-upsample fusion (k=3):
+// seg0 = full-res skip read with stride 2 (absent when c_skip == 0), seg1 =
+// low-res operand with merged 2x2 taps; P = 4 parity classes.
+struct TcLayer {
+    int mode = 0;
+    int k = 3, r = 1;
+    int c_out = 0, n_pad = 0, BN = 0, P = 1, k_total = 0;
+    int nseg = 0;
+    int seg_c[2] = {0, 0};      // real channels per segment
+    int seg_cpad[2] = {0, 0};   // channels read per segment (multiple of 64)
+    int seg_ntaps[2] = {0, 0};
+    int seg_kbase[2] = {0, 0};
+    int seg_m[2] = {1, 1};      // lattice->source multiplier
+    int8_t ox[2][4][kMaxTaps] = {}, oy[2][4][kMaxTaps] = {};
+    int rc = 1;                 // class radius in lattice units
+    float wscale = 1.0f;        // weights stored as fp16(w * wscale)
+    DevBuf w, bias, corr;
+};
+// c_split: channels of segment 0 (the skip operand for up blocks; c_in for
+// a single-source conv).
+std::unique_ptr<TcLayer> pack_tc_layer(Ledger* l, const Bank& b, int c_split, int mode);
+
+// Thin (CUDA-core) layer: fp32 weights on device.
+struct ThinLayer {
+    int c_in = 0, c_out = 0, k = 3;
+    DevBuf w, bias;
+};
+std::unique_ptr<ThinLayer> pack_thin_layer(Ledger* l, const Bank& b);
+
+// Launch one tensor-core conv (all tiles of one region).  `srcs` are the
+// segment operands in source coordinates; `win` the valid window of the
+// operand of segment 0 in ITS coordinates ({0,h,0,w} = whole image) and the
+// output region in output-pixel coordinates.
+void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window& win, float s,
+                 float o, bool silu, cudaStream_t st);
+
+// ---------------------------------------------------------------- engine
+struct RunStats {
+    double ms_denoise = 0, ms_decode = 0, ms_total = 0;  // device-timed
+    double stall_ms = 0, makespan_ms = 0;
+    int64_t full_steps = 0, cached_steps = 0;
+    int64_t macs_full = 0, macs_cached = 0, denoiser_macs = 0;
+    int64_t swap_bytes = 0, swap_calls = 0;
+    int64_t cache_bytes_planned = 0, cache_bytes_physical = 0;
+    int64_t peak[4][2] = {};
+    int64_t hbm_peak = 0;
+    std::vector<std::array<double, 4>> timeline;  // kind, step, bytes, t_ms
+    int64_t kernel_launches = 0;
+};
+
+class Engine {
+public:
+    explicit Engine(int device);
+    ~Engine();
+
+    // Prepare weights/buffers for a config (no-op when unchanged).
+    void configure(const RunConfig& cfg);
+    const RunConfig& config() const { return cfg_; }
+
+    // Whole pipeline.  x0_host: initial latent (1,T,C,h,w) fp32 or nullptr
+    // to generate it (text mode: randn(derive_seed(seed,1)),
+    // pipeline.cpp:115).  video_host may be nullptr (video stays on device
+    // in video_dev()).  latent_host receives the final latent if non-null.
+    RunStats run(const float* x0_host, float* video_host, float* latent_host, bool resident_input);
+
+    // Operator-level entry points (for unit parity).
+    // forward_full / forward_cached on x (2,T,C,h,w) host fp32.
+    void forward(const float* x_host, int64_t T, int64_t timestep, const float* deep_in_ref,
+                 float* deep_out_ref, float* eps_host);
+    // decode n latents (n,C,h,w) -> (n,3,H,W)
+    void decode(const float* lat_host, int64_t n, float* video_host, int64_t slice);
+    // Sliced decode sharded over `world` ranks (contiguous frame blocks of
+    // ceil(T/world)), decoded frames gathered to rank 0 over NCCL.
+    void decode_sharded(const float* lat_host, int64_t T, int64_t slice, float* video_host,
+                        ncclComm_t comm, int world, int rank, float* ms_out);
+    // Allocate run buffers for the configured frame count.
+    void run_prepare() { alloc_activations(cfg_.frames); }
+
+    // Device-resident helpers for the bench.
+    float* latent_dev() { return x_.as<float>(); }
+    float* video_dev() { return video_.as<float>(); }
+    int64_t latent_elems() const;
+    int64_t video_elems() const;
+    cudaStream_t stream() const { return s_compute_; }
+    Ledger& ledger() { return ledger_; }
+
+    int64_t decode_slice = 4;  // frames per decode launch group (tool flag)
+    int64_t launches = 0;
+
+private:
+    struct Level {
+        Act D;     // skip output of d_i
+        Act P;     // pooled input of d_i (i >= 1) / mid
+        Act U;     // output of u_i
+        Act UP;    // materialised upsample (fallback path only)
+    };
+    void alloc_activations(int64_t T);
+    // seam: 0 no swap, 1 await the prefetch at the seam, 2 await + evict
+    // (last consumer).  stacked: x_dev holds the explicit (2,T,...) CFG
+    // stack instead of the b=1 latent.
+    void forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t timestep, bool full,
+                     float* eps2_dev, int step, int seam);
+    void conv_block(int j, const Act& in, const Act& out, float s, float o, bool silu);
+    void up_block(int i, const Act& skip, const Act& u, const Act& out, float s, float o);
+    void decode_dev(const float* lat_dev, int64_t n, float* video_dev);
+    void issue_evict(int step);
+    void issue_prefetch(int issued, int needed);
+    void seam_await(int step);
+    void record(int kind, int step, int64_t bytes, cudaStream_t st);
+
+    int device_;
+    RunConfig cfg_;
+    bool configured_ = false;
+    std::string cfg_key_;
+    Ledger ledger_;
+    UNetWeights uw_;
+    CodecWeights cw_;
+    std::vector<std::unique_ptr<TcLayer>> tc_;     // per block (nullptr for thin)
+    std::vector<std::unique_ptr<TcLayer>> tc_fb_;  // up blocks: materialised-upsample fallback
+    std::unique_ptr<ThinLayer> stem_, head_;
+    std::vector<std::unique_ptr<TcLayer>> dec_tc_;  // decoder stages 1..S-1
+    std::unique_ptr<ThinLayer> dec0_, dec_last_;
+    std::vector<Level> lv_;
+    Act stem_out_, mid_;
+    Act cache_;        // U_{m+1} (b=2 stacked: images [0,T) uncond, [T,2T) cond)
+    DevBuf cache_buf_, cache_host_;
+    std::vector<DevBuf> act_bufs_;
+    DevBuf x_, xn_, eps2_, video_, z_, bad_;
+    std::vector<DevBuf> dec_bufs_;
+    int64_t T_alloc_ = -1;
+    int64_t dec_alloc_ = -1;
+    Act dec_act_[8];
+
+    cudaStream_t s_compute_ = nullptr, s_d2h_ = nullptr, s_h2d_ = nullptr;
+    cudaEvent_t ev_base_ = nullptr;
+    std::vector<cudaEvent_t> ev_pool_;
+    size_t ev_next_ = 0;
+    struct Mark {
+        int kind;
+        int step;
+        int64_t bytes;
+        cudaEvent_t ev;
+    };
+    std::vector<Mark> marks_;
+    cudaEvent_t ev_evict_[2] = {nullptr, nullptr}, ev_prefetch_[2] = {nullptr, nullptr},
+                ev_cache_ready_ = nullptr;
+    bool evict_pending_ = false, prefetch_pending_ = false;
+    RunStats* stats_ = nullptr;
+    cudaEvent_t next_event();
+};
+
+}  // namespace lc

@@ -1,0 +1,86 @@
+// HBM-bound and thin-channel kernels of the path (everything that is not a
+// dense tensor-core contraction).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace lc {
+
+// Valid (readable) window + output region of one tiled launch, in pixel
+// coordinates of the operand.  Reads outside [vy0,vy1)x[vx0,vx1) are zero
+// (the reference's crop-then-conv, proj/src/chunk.cpp:182-188).
+struct Window {
+    int vy0, vy1, vx0, vx1;  // valid input window
+    int oy0, oy1, ox0, ox1;  // output region
+};
+
+// Thin-input conv (c_in <= 8): fp32 NCHW input -> fp16 NHWC output.
+//  * stem of the denoiser (cfg_pair=1: writes both CFG branches; branch 1
+//    reads x + 0.15f, proj/src/pipeline.cpp:127-131), conditioning affine
+//    applied exactly as the reference (affine before zero padding);
+//  * first decoder conv (cfg_pair=0, s=1, o=0 skips the affine).
+// Arithmetic mirrors conv2d_window (tensor.cpp:170-193) in fp32.
+struct ThinInArgs {
+    const float* x;   // (nsrc, c_in, H, W)
+    int nsrc, c_in, H, W;
+    int cfg_pair;     // 1: output images = 2*nsrc
+    float cond_bias;  // added to x for branch 1
+    float s, o;
+    int apply_affine;
+    const float* w;   // [c_out][c_in][k][k]
+    const float* bias;
+    int c_out, k;
+    int silu;
+    __half* out;      // (nimg, H, W, cs_out)
+    int cs_out;
+    Window win;
+};
+cudaError_t launch_thin_in(const ThinInArgs& a, cudaStream_t st);
+
+// Thin-output conv (c_out <= 8): fp16 NHWC input -> fp32 NCHW output.
+//  * denoiser head: affine (s,o) then conv, no SiLU;
+//  * last decoder conv with the nearest upsample fused (up2=1: the input is
+//    the low-res tensor, output extents are 2x).
+struct ThinOutArgs {
+    const __half* x;  // (nimg, Hin, Win, cs_in)
+    int nimg, Hin, Win, cs_in, c_in;
+    int up2;
+    float s, o;
+    int apply_affine;
+    const float* w;   // [c_out][c_in][k][k]
+    const float* bias;
+    int c_out, k;
+    float* out;       // (nimg, c_out, H, W), H = Hin*(up2?2:1)
+    Window win;       // in output coordinates
+};
+cudaError_t launch_thin_out(const ThinOutArgs& a, cudaStream_t st);
+
+// 2x2 mean pool 0.25f*(a+b+c+d) (tensor.cpp:206-225), fp16 NHWC.
+cudaError_t launch_down2(const __half* in, __half* out, int nimg, int H, int W, int cs,
+                         cudaStream_t st);
+// Nearest 2x upsample (tensor.cpp:232-248), fp16 NHWC.
+cudaError_t launch_up2(const __half* in, __half* out, int nimg, int H, int W, int cs,
+                       cudaStream_t st);
+
+// CFG combine + sampler update (sampler.cpp:95-133, pipeline.cpp:170-185):
+//   eps = (1-g)*e_u + g*e_c ; x' = a*x + b*eps [; x' = 1*x' + c*z]
+// with the reference's two-rounding order; raises *bad if x' is non-finite
+// (the next step's check_input, unet.cpp:134).
+struct StepArgs {
+    const float* eps2;  // (2, n)
+    const float* x;
+    float* x_out;
+    const float* z;     // nullable
+    int64_t n;
+    float g, a, b, c;
+    int* bad;
+};
+cudaError_t launch_step(const StepArgs& a, cudaStream_t st);
+
+// Non-finite scan of a fp32 buffer (all_finite, tensor.cpp:376).
+cudaError_t launch_isfinite(const float* x, int64_t n, int* bad, cudaStream_t st);
+
+}  // namespace lc
