@@ -67,6 +67,21 @@ int lc_download_video(lc_ctx* ctx, float* video);
  * key; the output is identical for every value). */
 int lc_set_decode_slice(lc_ctx* ctx, int64_t frames);
 
+/* Measurement helpers (bench.py) ------------------------------------------ */
+/* CUDA events on the context's compute stream bracketing any number of
+ * calls; lc_timer_stop synchronises and returns the elapsed device ms. */
+int lc_timer_start(lc_ctx* ctx);
+int lc_timer_stop(lc_ctx* ctx, float* ms);
+/* Per-launch CUDA-event timing of the tensor-core conv kernel (on/off);
+ * lc_conv_profile returns launches, device ms, algorithmic FLOPs (the
+ * reference's conv MAC count x2) and executed MMA FLOPs since the last reset. */
+int lc_set_conv_profile(lc_ctx* ctx, int on);
+int lc_conv_profile(lc_ctx* ctx, int64_t* launches, double* ms, double* alg_flops,
+                    double* exec_flops);
+/* Pinned host buffers for end-to-end copies. */
+void* lc_alloc_pinned(int64_t bytes);
+int lc_free_pinned(void* p);
+
 /* Operators -------------------------------------------------------------- */
 /* forward_full (deep_in == NULL; proj/src/unet.cpp:188-230) or
  * forward_cached (proj/src/unet.cpp:232-276) on x (2,T,C,h,w).  deep_in /

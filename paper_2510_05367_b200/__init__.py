@@ -95,7 +95,8 @@ EXPORTS = [
     "lc_upload_latent", "lc_run_resident", "lc_download_video", "lc_set_decode_slice",
     "lc_forward", "lc_decode", "lc_conv2d", "lc_up_conv2d", "lc_plan_steps", "lc_split",
     "lc_model_numbers", "lc_derive_seed", "lc_randn", "lc_shard_frames", "lc_nccl_unique_id",
-    "lc_nccl_init", "lc_decode_sharded",
+    "lc_nccl_init", "lc_decode_sharded", "lc_timer_start", "lc_timer_stop", "lc_set_conv_profile",
+    "lc_conv_profile", "lc_alloc_pinned", "lc_free_pinned",
 ]
 
 # ----------------------------------------------------------------- config
@@ -265,6 +266,30 @@ class Context:
         _check(lib().lc_download_video(self._h, _p(out)))
         return out
 
+    # -- measurement
+    def timer_start(self):
+        _check(lib().lc_timer_start(self._h))
+
+    def timer_stop(self) -> float:
+        ms = ctypes.c_float()
+        _check(lib().lc_timer_stop(self._h, ctypes.byref(ms)))
+        return ms.value
+
+    def set_conv_profile(self, on: bool):
+        _check(lib().lc_set_conv_profile(self._h, ctypes.c_int(int(on))))
+
+    def conv_profile(self) -> dict:
+        n, ms, alg, exe = I64(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        _check(lib().lc_conv_profile(self._h, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(alg),
+                                     ctypes.byref(exe)))
+        return {"launches": n.value, "ms": ms.value, "alg_flops": alg.value, "exec_flops": exe.value}
+
+    def run_e2e(self, x0_pinned: "PinnedArray", video_pinned: "PinnedArray") -> dict:
+        """run_pipeline with pinned host input/output buffers (H2D + D2H inside)."""
+        rep = ctypes.create_string_buffer(1 << 22)
+        _check(lib().lc_run_pipeline(self._h, x0_pinned.ptr, video_pinned.ptr, None, rep, I64(1 << 22)))
+        return json.loads(rep.value.decode())
+
     # -- operators
     def forward(self, x: np.ndarray, timestep: int, deep_in: Optional[np.ndarray] = None,
                 want_deep: bool = False, deep_shape=None):
@@ -320,6 +345,24 @@ class Context:
         ms = ctypes.c_float()
         _check(lib().lc_decode_sharded(self._h, _p(lat), I64(T), I64(slice_frames), _p(out), ctypes.byref(ms)))
         return out, ms.value
+
+
+class PinnedArray:
+    """fp32 array in page-locked host memory (lc_alloc_pinned)."""
+
+    def __init__(self, n: int):
+        L = lib()
+        L.lc_alloc_pinned.restype = ctypes.c_void_p
+        self.ptr = ctypes.c_void_p(L.lc_alloc_pinned(I64(max(1, n) * 4)))
+        if not self.ptr:
+            raise DeviceError(L.lc_last_error().decode())
+        self.n = n
+        self.array = np.ctypeslib.as_array(ctypes.cast(self.ptr, ctypes.POINTER(ctypes.c_float)), shape=(n,))
+
+    def free(self):
+        if self.ptr:
+            lib().lc_free_pinned(self.ptr)
+            self.ptr = None
 
 
 def nccl_unique_id() -> bytes:

@@ -16,6 +16,8 @@ struct lc_ctx {
     lc::Engine engine;
     ncclComm_t comm = nullptr;
     int world = 1, rank = 0;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    lc::ConvProfiler prof;
 };
 
 namespace {
@@ -174,6 +176,43 @@ int lc_set_decode_slice(lc_ctx* ctx, int64_t frames) {
         if (frames < 1) lc::throw_config("decode slice must be >= 1");
         ctx->engine.decode_slice = frames;
     });
+}
+
+int lc_timer_start(lc_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx->t0) {
+            LC_CUDA(cudaEventCreate(&ctx->t0));
+            LC_CUDA(cudaEventCreate(&ctx->t1));
+        }
+        LC_CUDA(cudaEventRecord(ctx->t0, ctx->engine.stream()));
+    });
+}
+int lc_timer_stop(lc_ctx* ctx, float* ms) {
+    return guarded([&] {
+        LC_CUDA(cudaEventRecord(ctx->t1, ctx->engine.stream()));
+        LC_CUDA(cudaEventSynchronize(ctx->t1));
+        LC_CUDA(cudaEventElapsedTime(ms, ctx->t0, ctx->t1));
+    });
+}
+int lc_set_conv_profile(lc_ctx* ctx, int on) {
+    return guarded([&] {
+        ctx->prof.clear();
+        lc::set_conv_profiler(on ? &ctx->prof : nullptr);
+    });
+}
+int lc_conv_profile(lc_ctx* ctx, int64_t* launches, double* ms, double* alg, double* exec) {
+    return guarded([&] { ctx->prof.summarize(launches, ms, alg, exec); });
+}
+void* lc_alloc_pinned(int64_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, static_cast<size_t>(bytes), cudaHostAllocDefault) != cudaSuccess) {
+        g_err = "cudaHostAlloc failed";
+        return nullptr;
+    }
+    return p;
+}
+int lc_free_pinned(void* p) {
+    return guarded([&] { LC_CUDA(cudaFreeHost(p)); });
 }
 
 int lc_forward(lc_ctx* ctx, const float* x, int64_t T, int64_t timestep, const float* deep_in,

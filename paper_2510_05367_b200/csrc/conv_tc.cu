@@ -41,8 +41,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     mt /= p.tiles_x;
     const int ty = mt % p.tiles_y;
     const int ti = mt / p.tiles_y;
-    const int X0 = p.lx0 + tx * p.TW;
-    const int Y0 = p.ly0 + ty * p.TH;
+    const int X0 = p.lx0[parity] + tx * p.TW;
+    const int Y0 = p.ly0[parity] + ty * p.TH;
     const int I0 = ti * p.TI;
 
     int total_kb = 0;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int lx = m % p.TW;
         const int img = I0 + li;
         const int Y = Y0 + ly, X = X0 + lx;
-        const bool valid = (m < p.TI * tile_px) && img < p.n_img && Y < p.ly1 && X < p.lx1;
+        const bool valid = (m < p.TI * tile_px) && img < p.n_img && Y < p.ly1[parity] && X < p.lx1[parity];
         // conditioning-shift border class (distance to the class window)
         const int rr = p.rc + 1;
         int dt = Y - p.cy0, db = p.cy1 - 1 - Y, dl = X - p.cx0, dr = p.cx1 - 1 - X;

@@ -45,7 +45,7 @@ struct alignas(64) ConvParams {
     ConvSegDev seg[2];
     int nseg;
     int n_img;                    // images = b*t
-    int ly0, ly1, lx0, lx1;       // output region in lattice coordinates
+    int ly0[4], ly1[4], lx0[4], lx1[4];  // output region in lattice coords, per parity class
     int TI, TH, TW;               // pixel tile
     int tiles_x, tiles_y, tiles_i;
     int BN;                       // N tile

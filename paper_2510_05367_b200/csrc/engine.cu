@@ -289,15 +289,21 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
     ConvParams p;
     std::memset(&p, 0, sizeof(p));
     const int sub = L.mode == 1 ? 2 : 1;
-    p.ly0 = win.oy0 / sub;
-    p.ly1 = win.oy1 / sub;
-    p.lx0 = win.ox0 / sub;
-    p.lx1 = win.ox1 / sub;
+    // per parity class q = (py, px): output pixels 2Y+py in [oy0, oy1)
+    int Lh = 0, Lw = 0;
+    for (int q = 0; q < 4; ++q) {
+        const int py = sub == 2 ? q / 2 : 0, px = sub == 2 ? q % 2 : 0;
+        p.ly0[q] = (win.oy0 - py + sub - 1) / sub;
+        p.ly1[q] = (win.oy1 - py + sub - 1) / sub;
+        p.lx0[q] = (win.ox0 - px + sub - 1) / sub;
+        p.lx1[q] = (win.ox1 - px + sub - 1) / sub;
+        Lh = std::max(Lh, p.ly1[q] - p.ly0[q]);
+        Lw = std::max(Lw, p.lx1[q] - p.lx0[q]);
+    }
     p.cy0 = win.vy0 / sub;
     p.cy1 = win.vy1 / sub;
     p.cx0 = win.vx0 / sub;
     p.cx1 = win.vx1 / sub;
-    const int Lh = p.ly1 - p.ly0, Lw = p.lx1 - p.lx0;
     p.n_img = out.n;
     p.TW = std::min(Lw, 128);
     p.TH = std::max(1, std::min(Lh, 128 / p.TW));
@@ -362,6 +368,27 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
     p.scale = s / L.wscale;
     p.shift = o;
     p.silu = silu ? 1 : 0;
+    ConvProfiler* prof = conv_profiler();
+    if (prof) {
+        // algorithmic work of the reference op (conv2d over the concat,
+        // tensor.cpp:194-195 count_macs) vs the MMA work actually issued
+        int64_t pix = 0;
+        for (int q = 0; q < L.P; ++q)
+            pix += static_cast<int64_t>(std::max(0, p.ly1[q] - p.ly0[q])) * std::max(0, p.lx1[q] - p.lx0[q]);
+        int64_t cin = 0;
+        for (int sgi = 0; sgi < L.nseg; ++sgi) cin += L.seg_c[sgi];
+        ConvProfiler::Rec r;
+        r.alg_flops = 2.0 * static_cast<double>(pix) * out.n * L.c_out * L.k * L.k * cin;
+        r.exec_flops = 2.0 * static_cast<double>(p.tiles_x) * p.tiles_y * p.tiles_i * L.P * 128.0 *
+                       L.n_pad * L.k_total;
+        LC_CUDA(cudaEventCreate(&r.e0));
+        LC_CUDA(cudaEventCreate(&r.e1));
+        LC_CUDA(cudaEventRecord(r.e0, st));
+        LC_CUDA(launch_conv_tc(p, L.P, st));
+        LC_CUDA(cudaEventRecord(r.e1, st));
+        prof->recs.push_back(r);
+        return;
+    }
     LC_CUDA(launch_conv_tc(p, L.P, st));
 }
 
@@ -455,7 +482,10 @@ void Engine::configure(const RunConfig& cfg) {
         T_alloc_ = -1;
         dec_alloc_ = -1;
     }
-    if (!same_geom) T_alloc_ = -1;
+    if (!same_geom) {
+        T_alloc_ = -1;
+        dec_alloc_ = -1;
+    }
     configured_ = true;
 }
 
@@ -513,6 +543,7 @@ void Engine::alloc_activations(int64_t T) {
         if (cfg_.swap_mode != SwapMode::Off) cache_host_ = host_alloc(&ledger_, a.elems() * 2);
     }
     const int64_t nl = T * cfg_.latent_channels * lh * lw;
+    x0_ = dev_alloc(&ledger_, nl * 4, true);
     x_ = dev_alloc(&ledger_, nl * 4, true);
     xn_ = dev_alloc(&ledger_, nl * 4, true);
     z_ = dev_alloc(&ledger_, nl * 4, true);
@@ -563,8 +594,10 @@ void Engine::up_block(int i, const Act& skip, const Act& u, const Act& out, floa
     const int j = static_cast<int>(block_index(cfg_, "u" + std::to_string(i)));
     const auto wins = block_windows(cfg_, "u" + std::to_string(i), skip.h, skip.w);
     bool subpixel = tc_[j] != nullptr;
+    // merged sub-pixel taps need a parity-aligned readable window; odd
+    // output cores are fine (per-parity lattice regions)
     for (const Window& wd : wins)
-        if ((wd.vy0 | wd.vy1 | wd.vx0 | wd.vx1 | wd.oy0 | wd.oy1 | wd.ox0 | wd.ox1) & 1) subpixel = false;
+        if ((wd.vy0 | wd.vy1 | wd.vx0 | wd.vx1) & 1) subpixel = false;
     if (subpixel) {
         const Act srcs[2] = {skip, u};
         for (const Window& wd : wins) {
@@ -573,9 +606,14 @@ void Engine::up_block(int i, const Act& skip, const Act& u, const Act& out, floa
         }
         return;
     }
-    // Fallback: materialise the nearest upsample, then a two-segment conv.
-    const Act& up = lv_[i].UP;
-    if (!up.p) throw_invariant("upsample buffer missing for fallback path");
+    // Fallback (k != 3, or odd tile windows): materialise the nearest
+    // upsample, then a two-segment conv.
+    Act& up = lv_[i].UP;
+    if (!up.p) {
+        up = Act{nullptr, u.n, skip.h, skip.w, u.cs, u.c};
+        act_bufs_.push_back(dev_alloc(&ledger_, up.elems() * 2, true));
+        up.p = act_bufs_.back().as<__half>();
+    }
     LC_CUDA(launch_up2(u.p, up.p, u.n, u.h, u.w, u.cs, s_compute_));
     ++launches;
     const Act srcs[2] = {skip, up};
@@ -723,15 +761,19 @@ void Engine::issue_prefetch(int issued, int needed) {
     }
     if (stats_) stats_->swap_calls += 1;
     prefetch_pending_ = true;
+    prefetch_tag_ = needed;
 }
 
 void Engine::seam_await(int step) {
     // CacheStore::assemble -> fetch -> await_ready (cache.cpp:65-90): the
     // compute stream waits for the prefetch only here, after the shallow path.
+    // Await events carry the ticket's step, i.e. the prefetch's
+    // needed_at_step (swap.cpp:306-324, ticket step set at submit).
+    (void)step;
     for (int b = 0; b < 2; ++b) {
-        record(4, step, 0, s_compute_);
+        record(4, prefetch_tag_, 0, s_compute_);
         if (prefetch_pending_) LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_prefetch_[b], 0));
-        record(5, step, 0, s_compute_);
+        record(5, prefetch_tag_, 0, s_compute_);
     }
     prefetch_pending_ = false;
 }
@@ -848,6 +890,8 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
         }
         LC_CUDA(cudaMemcpyAsync(x_.p, src, static_cast<size_t>(nl) * 4, cudaMemcpyHostToDevice, s_compute_));
         if (!x0_host) LC_CUDA(cudaStreamSynchronize(s_compute_));
+    } else {
+        LC_CUDA(cudaMemcpyAsync(x_.p, x0_.p, static_cast<size_t>(nl) * 4, cudaMemcpyDeviceToDevice, s_compute_));
     }
     LC_CUDA(cudaMemsetAsync(bad_.p, 0, 16, s_compute_));
     LC_CUDA(launch_isfinite(x_.as<float>(), nl, bad_.as<int>(), s_compute_));
@@ -1082,6 +1126,38 @@ void Engine::decode_sharded(const float* lat_host, int64_t T, int64_t slice, flo
     dec_alloc_ = -1;
     if (rank == 0 && video_host)
         LC_CUDA(cudaMemcpy(video_host, vid.p, static_cast<size_t>(T * vid_frame) * 4, cudaMemcpyDeviceToHost));
+}
+
+}  // namespace lc
+
+namespace lc {
+
+namespace {
+ConvProfiler* g_conv_prof = nullptr;
+}
+
+ConvProfiler* conv_profiler() { return g_conv_prof; }
+void set_conv_profiler(ConvProfiler* p) { g_conv_prof = p; }
+
+void ConvProfiler::clear() {
+    for (auto& r : recs) {
+        cudaEventDestroy(r.e0);
+        cudaEventDestroy(r.e1);
+    }
+    recs.clear();
+}
+
+void ConvProfiler::summarize(int64_t* n, double* ms, double* alg, double* exec) const {
+    *n = static_cast<int64_t>(recs.size());
+    *ms = *alg = *exec = 0;
+    for (const auto& r : recs) {
+        float t = 0;
+        LC_CUDA(cudaEventSynchronize(r.e1));
+        LC_CUDA(cudaEventElapsedTime(&t, r.e0, r.e1));
+        *ms += t;
+        *alg += r.alg_flops;
+        *exec += r.exec_flops;
+    }
 }
 
 }  // namespace lc

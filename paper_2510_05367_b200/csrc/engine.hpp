@@ -94,6 +94,21 @@ struct ThinLayer {
 };
 std::unique_ptr<ThinLayer> pack_thin_layer(Ledger* l, const Bank& b);
 
+// Optional per-launch timing of the tensor-core conv (bench roofline):
+// CUDA events on the launching stream around each launch.
+struct ConvProfiler {
+    struct Rec {
+        double alg_flops = 0, exec_flops = 0;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+    };
+    std::vector<Rec> recs;
+    void clear();
+    // totals: launches, ms, algorithmic FLOPs, executed MMA FLOPs
+    void summarize(int64_t* n, double* ms, double* alg, double* exec) const;
+};
+ConvProfiler* conv_profiler();
+void set_conv_profiler(ConvProfiler* p);
+
 // Launch one tensor-core conv (all tiles of one region).  `srcs` are the
 // segment operands in source coordinates; `win` the valid window of the
 // operand of segment 0 in ITS coordinates ({0,h,0,w} = whole image) and the
@@ -144,7 +159,9 @@ public:
     void run_prepare() { alloc_activations(cfg_.frames); }
 
     // Device-resident helpers for the bench.
-    float* latent_dev() { return x_.as<float>(); }
+    // Staged initial latent for resident runs (copied into the trajectory
+    // buffer at the start of every run).
+    float* latent_dev() { return x0_.as<float>(); }
     float* video_dev() { return video_.as<float>(); }
     int64_t latent_elems() const;
     int64_t video_elems() const;
@@ -192,7 +209,7 @@ private:
     Act cache_;        // U_{m+1} (b=2 stacked: images [0,T) uncond, [T,2T) cond)
     DevBuf cache_buf_, cache_host_;
     std::vector<DevBuf> act_bufs_;
-    DevBuf x_, xn_, eps2_, video_, z_, bad_;
+    DevBuf x0_, x_, xn_, eps2_, video_, z_, bad_;
     std::vector<DevBuf> dec_bufs_;
     int64_t T_alloc_ = -1;
     int64_t dec_alloc_ = -1;
@@ -212,6 +229,7 @@ private:
     cudaEvent_t ev_evict_[2] = {nullptr, nullptr}, ev_prefetch_[2] = {nullptr, nullptr},
                 ev_cache_ready_ = nullptr;
     bool evict_pending_ = false, prefetch_pending_ = false;
+    int prefetch_tag_ = -1;
     RunStats* stats_ = nullptr;
     cudaEvent_t next_event();
 };

@@ -1,0 +1,106 @@
+"""Generate the committed golden fixtures from the reference itself.
+
+Runs the UNMODIFIED reference (oracle/_ref, compiled in place from
+/root/reference/proj/src by oracle/Makefile) and stores its outputs as
+compressed .npz under tests/golden/.  The B/C frame-0 slices (SURVEY.md
+section 8c: frame 0 of a T-frame run is bit-identical to the T=1 run) are
+too slow for the single-threaded reference and are produced by the
+restatement oracle/lc_oracle.c, which tests/test_oracle.py pins bit-exactly
+to the reference on every smaller case.
+
+Usage:  python tests/golden/make_golden.py [small|b0|c0]...
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+import lco  # noqa: E402
+
+DEFAULT = open(os.path.join(HERE, "default.cfg")).read()
+
+SMALL = {
+    "default": {},
+    "tiny": {"run.frames": 2, "run.height": 32, "run.width": 32, "sampler.steps": 6},
+    "tiny_ancestral": {"run.frames": 2, "run.height": 32, "run.width": 32, "sampler.steps": 6,
+                       "sampler.kind": "ancestral"},
+    "tiny_ddim_m1": {"run.frames": 2, "run.height": 32, "run.width": 32, "sampler.steps": 6,
+                     "sampler.kind": "ddim", "unet.cache_depth": 1},
+    "tiny_halo_none": {"run.frames": 2, "run.height": 32, "run.width": 32, "sampler.steps": 6,
+                       "chunk.halo": "none", "chunk.targets": "stem,d0,u0,head"},
+    "tiny_k5": {"run.frames": 2, "run.height": 32, "run.width": 32, "sampler.steps": 6, "unet.kernel": 5},
+    "config_a": {"run.height": 128, "run.width": 128, "cache.n": 3, "chunk.eta": 2, "chunk.omega": 1},
+}
+B0 = {"run.frames": 1, "run.height": 512, "run.width": 512, "codec.stages": 3, "codec.width": 128,
+      "unet.base_channels": 320, "unet.depth": 3, "sampler.steps": 4, "cache.n": 2}
+C0 = {"run.frames": 1, "run.height": 576, "run.width": 1024, "codec.stages": 3, "codec.width": 128,
+      "unet.base_channels": 320, "unet.depth": 3, "sampler.steps": 25, "cache.n": 2, "swap.mode": "async"}
+
+
+def kv_of(over):
+    kv = lco.parse_text(DEFAULT)
+    kv.update({k: str(v) for k, v in over.items()})
+    return kv
+
+
+def small():
+    ref = lco.Reference()
+    for name, over in SMALL.items():
+        kv = kv_of(over)
+        t = time.time()
+        video, report, macs = ref.run_pipeline(kv)
+        # final latent via the restatement (the reference API returns only
+        # the video); the restatement's video must equal the reference's
+        v2, lat = lco.Restatement().run_pipeline(kv)
+        assert np.array_equal(video, v2), name
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), video=video, latent=lat,
+                            macs=np.array(macs, np.int64),
+                            config=np.array(lco.to_text(kv)), report=np.array(json.dumps(report)))
+        print(name, f"{time.time() - t:.1f}s", flush=True)
+    # integer contracts
+    plans = {}
+    for total in range(1, 13):
+        for n in range(1, 6):
+            k, f = ref.plan_steps(total, n)
+            plans[f"{total}_{n}"] = np.stack([k, f])
+    np.savez_compressed(os.path.join(HERE, "plans.npz"), **plans)
+    splits = {}
+    for (h, w) in [(8, 8), (16, 16), (32, 32), (72, 128), (9, 16), (36, 64)]:
+        for eta in (1, 2, 3, 4):
+            for omega in (1, 2, 4):
+                if h % eta or w % omega:
+                    continue
+                for hk, hp in ((0, 0), (1, 1), (1, 3), (2, 0)):
+                    for k in (1, 3, 5):
+                        regions, halo = ref.split(h, w, eta, omega, hk, hp, k)
+                        splits[f"{h}_{w}_{eta}_{omega}_{hk}_{hp}_{k}"] = np.concatenate(
+                            [regions.reshape(-1), [halo]])
+    np.savez_compressed(os.path.join(HERE, "splits.npz"), **splits)
+    nums = {}
+    for name, over in dict(SMALL, b=dict(B0, **{"run.frames": 16}), c=dict(C0, **{"run.frames": 25})).items():
+        nums[name] = np.array(ref.model_numbers(kv_of(over)), np.int64)
+    np.savez_compressed(os.path.join(HERE, "model_numbers.npz"), **nums)
+
+
+def slice0(name, over):
+    kv = kv_of(over)
+    t = time.time()
+    video, lat = lco.Restatement().run_pipeline(kv)
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), video=video, latent=lat,
+                        config=np.array(lco.to_text(kv)), seconds=np.array(time.time() - t))
+    print(name, f"{time.time() - t:.1f}s", flush=True)
+
+
+if __name__ == "__main__":
+    what = sys.argv[1:] or ["small"]
+    if "small" in what:
+        small()
+    if "b0" in what:
+        slice0("b_frame0", B0)
+    if "c0" in what:
+        slice0("c_frame0", C0)

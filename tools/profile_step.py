@@ -1,0 +1,17 @@
+"""One warm resident pipeline step of a bench workload (for ncu)."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench
+import paper_2510_05367_b200 as lc
+wl = sys.argv[1] if len(sys.argv) > 1 else "B"
+over = bench.WORKLOADS[wl]
+text = lc.config_text(over, base=lc.DEFAULT_CONFIG)
+ctx = lc.Context(0)
+ctx.configure(text)
+ctx.set_decode_slice(4)
+kv = lc.parse_config(text)
+n = ctx.latent_elems()
+ctx.upload_latent(lc.randn(lc.derive_seed(int(kv["run.seed"]), 1), n))
+for _ in range(int(sys.argv[2]) if len(sys.argv) > 2 else 2):
+    rep = ctx.run_resident()
+print("launches/step", rep["kernel_launches"], "device ms", rep["device_ms"])
