@@ -55,6 +55,9 @@ struct alignas(64) ConvParams {
     int sy, sx;                   // lattice -> output pixel multiplier (1 or 2)
     int py[4], px[4];             // per parity output offset
     __half* out;
+    float* out32;                 // non-null: fp32 NCHW (img, c_out, out_h, out_w) output instead
+    int shuffle_c;                // >0 (with out32): depth-to-space, channel p*shuffle_c+o ->
+                                  // pixel (2Y+p/2, 2X+p%2), channel o of a shuffle_c-channel image
     const float* bias;            // [n_pad]
     const float* corr;            // [P][ncls][n_pad]   sum of in-bound tap weights
     int rc;                       // class radius (lattice units)

@@ -284,8 +284,51 @@ std::unique_ptr<ThinLayer> pack_thin_layer(Ledger* l, const Bank& b) {
 }
 
 // ------------------------------------------------------- conv launch
+Bank patch_bank(const Bank& b) {
+    Bank p;
+    const int64_t kk = b.c_in * b.k * b.k;
+    p.c_in = (kk + 63) / 64 * 64;
+    p.c_out = b.c_out;
+    p.k = 1;
+    p.taps.assign(static_cast<size_t>(p.c_out * p.c_in), 0.0f);
+    for (int64_t oc = 0; oc < b.c_out; ++oc)
+        for (int64_t t = 0; t < kk; ++t) p.taps[oc * p.c_in + t] = b.taps[oc * kk + t];
+    p.bias = b.bias;
+    return p;
+}
+
+Bank subpixel_shuffle_bank(const Bank& b) {
+    if (b.k != 3) throw_invariant("sub-pixel shuffle needs k == 3");
+    Bank s;
+    s.c_in = b.c_in;
+    s.c_out = 4 * b.c_out;
+    s.k = 3;
+    s.taps.assign(static_cast<size_t>(s.c_out * s.c_in * 9), 0.0f);
+    s.bias.resize(static_cast<size_t>(s.c_out));
+    // rows(parity, d): merged source rows of the 3x3 kernel
+    const int lo[2][2] = {{0, 1}, {0, 2}}, hi[2][2] = {{1, 3}, {2, 3}};
+    for (int p = 0; p < 4; ++p) {
+        const int py = p / 2, px = p % 2;
+        for (int64_t o = 0; o < b.c_out; ++o) {
+            s.bias[p * b.c_out + o] = b.bias[o];
+            for (int64_t c = 0; c < b.c_in; ++c)
+                for (int ry = 0; ry < 3; ++ry)
+                    for (int rx = 0; rx < 3; ++rx) {
+                        const int dy = ry - py, dx = rx - px;  // low-res row Y+ry-1 = Y+dy-1+py
+                        if (dy < 0 || dy > 1 || dx < 0 || dx > 1) continue;
+                        double acc = 0.0;
+                        for (int ky = lo[py][dy]; ky < hi[py][dy]; ++ky)
+                            for (int kx = lo[px][dx]; kx < hi[px][dx]; ++kx)
+                                acc += b.taps[((o * b.c_in + c) * 3 + ky) * 3 + kx];
+                        s.taps[(((p * b.c_out + o) * s.c_in + c) * 3 + ry) * 3 + rx] = static_cast<float>(acc);
+                    }
+        }
+    }
+    return s;
+}
+
 void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window& win, float s,
-                 float o, bool silu, cudaStream_t st) {
+                 float o, bool silu, cudaStream_t st, float* out32, int shuffle_c) {
     ConvParams p;
     std::memset(&p, 0, sizeof(p));
     const int sub = L.mode == 1 ? 2 : 1;
@@ -362,6 +405,8 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
         p.px[q] = L.mode == 1 ? q % 2 : 0;
     }
     p.out = out.p;
+    p.out32 = out32;
+    p.shuffle_c = shuffle_c;
     p.bias = L.bias.as<float>();
     p.corr = L.corr.as<float>();
     p.rc = L.rc;
@@ -409,6 +454,8 @@ Engine::Engine(int device) : device_(device) {
 Engine::~Engine() {
     cudaDeviceSynchronize();
     for (auto e : ev_pool_) cudaEventDestroy(e);
+    for (int b = 0; b < 2; ++b)
+        for (auto e : ev_chunk_[b]) cudaEventDestroy(e);
     cudaEventDestroy(ev_base_);
     for (int b = 0; b < 2; ++b) {
         cudaEventDestroy(ev_evict_[b]);
@@ -476,6 +523,37 @@ void Engine::configure(const RunConfig& cfg) {
         head_ = pack_thin_layer(&ledger_, uw_.banks.back());
         dec0_ = pack_thin_layer(&ledger_, cw_.dec[0]);
         dec_last_ = pack_thin_layer(&ledger_, cw_.dec[static_cast<size_t>(cfg.stages)]);
+        head_tc_ = pack_tc_layer(&ledger_, uw_.banks.back(), static_cast<int>(cfg.base_channels), 0);
+        {
+            const Bank sp = patch_bank(uw_.banks.front());
+            stem_kp_ = static_cast<int>(sp.c_in);
+            stem_tc_ = pack_tc_layer(&ledger_, sp, stem_kp_, 0);
+            const Bank dp = patch_bank(cw_.dec[0]);
+            dec0_kp_ = static_cast<int>(dp.c_in);
+            dec0_tc_ = pack_tc_layer(&ledger_, dp, dec0_kp_, 0);
+            const Bank ds = subpixel_shuffle_bank(cw_.dec[static_cast<size_t>(cfg.stages)]);
+            dec_last_tc_ = pack_tc_layer(&ledger_, ds, static_cast<int>(ds.c_in), 0);
+        }
+        {
+            // merged sub-pixel taps of the last decoder conv: wm[p][dy*2+dx][c][4]
+            const Bank& b = cw_.dec[static_cast<size_t>(cfg.stages)];
+            const int ci = static_cast<int>(b.c_in), co = static_cast<int>(b.c_out);
+            if (co > 4) throw_config("codec image channels > 4 not supported on the GPU decoder");
+            std::vector<float> wm(static_cast<size_t>(16) * ci * 4, 0.0f);
+            const int lo[2][2] = {{0, 1}, {0, 2}}, hi[2][2] = {{1, 3}, {2, 3}};  // rows(parity, d)
+            for (int p = 0; p < 4; ++p)
+                for (int t = 0; t < 4; ++t)
+                    for (int c = 0; c < ci; ++c)
+                        for (int o = 0; o < co; ++o) {
+                            double acc = 0.0;
+                            for (int ky = lo[p / 2][t / 2]; ky < hi[p / 2][t / 2]; ++ky)
+                                for (int kx = lo[p % 2][t % 2]; kx < hi[p % 2][t % 2]; ++kx)
+                                    acc += b.taps[((static_cast<size_t>(o) * ci + c) * 3 + ky) * 3 + kx];
+                            wm[((static_cast<size_t>(p) * 4 + t) * ci + c) * 4 + o] = static_cast<float>(acc);
+                        }
+            dec_last_wm_ = dev_alloc(&ledger_, static_cast<int64_t>(wm.size() * 4), false);
+            LC_CUDA(cudaMemcpy(dec_last_wm_.p, wm.data(), wm.size() * 4, cudaMemcpyHostToDevice));
+        }
         dec_tc_.clear();
         for (int64_t i = 1; i < cfg.stages; ++i) dec_tc_.push_back(pack_tc_layer(&ledger_, cw_.dec[i], 0, 1));
         cfg_key_ = key;
@@ -516,6 +594,7 @@ void Engine::alloc_activations(int64_t T) {
     };
     lv_.assign(static_cast<size_t>(M + 1), Level{});
     stem_out_ = make(lh, lw, ch(0));
+    patch_ = make(lh, lw, stem_kp_);
     for (int i = 0; i < M; ++i) {
         const int h = lh >> i, w = lw >> i;
         lv_[i].D = make(h, w, ch(i));
@@ -650,11 +729,15 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
             a.c_out = stem_->c_out;
             a.k = stem_->k;
             a.silu = 1;
-            a.out = stem_out_.p;
-            a.cs_out = stem_out_.cs;
+            // gather conditioned 3x3x4 patches (exact reference roundings),
+            // then a K=64 tensor-core GEMM with bias + SiLU epilogue
+            a.out = patch_.p;
+            a.cs_out = patch_.cs;
             a.win = wd;
-            LC_CUDA(launch_thin_in(a, s_compute_));
-            ++launches;
+            LC_CUDA(launch_patch(a, stem_kp_, s_compute_));
+            run_tc_conv(*stem_tc_, &patch_, stem_out_, Window{0, lh, 0, lw, wd.oy0, wd.oy1, wd.ox0, wd.ox1},
+                        1.0f, 0.0f, true, s_compute_);
+            launches += 2;
         }
     }
     cond(1, &s, &o);
@@ -683,6 +766,10 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
         ++launches;
         cond(1 + M, &s, &o);
         conv_block(1 + M, lv_[M].P, mid_, s, o, true);
+        if (writes_cache && m + 1 == M && seam == 3) {
+            LC_CUDA(cudaEventRecord(ev_cache_ready_, s_compute_));
+            cache_ready_recorded_ = true;
+        }
     } else if (seam > 0) {
         seam_await(step);
         // last consumer: evict_all right after assemble (pipeline.cpp:156-160)
@@ -693,52 +780,68 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
         const int j = static_cast<int>(block_index(cfg_, "u" + std::to_string(i)));
         cond(j, &s, &o);
         up_block(i, lv_[i].D, U_of(i + 1), i == 0 ? lv_[0].U : U_of(i), s, o);
+        if (writes_cache && i == m + 1 && seam == 3) {
+            LC_CUDA(cudaEventRecord(ev_cache_ready_, s_compute_));
+            cache_ready_recorded_ = true;
+        }
     }
     // head: affine + conv, no SiLU -> eps (2,T,C,h,w) fp32
     {
         const int j = static_cast<int>(block_index(cfg_, "head"));
         cond(j, &s, &o);
+        Act eps_view;  // fp32 NCHW output geometry (2T, C, h, w)
+        eps_view.n = lv_[0].U.n;
+        eps_view.h = lh;
+        eps_view.w = lw;
+        eps_view.c = head_tc_->c_out;
         for (const Window& wd : block_windows(cfg_, "head", lh, lw)) {
-            ThinOutArgs a{};
-            a.x = lv_[0].U.p;
-            a.nimg = lv_[0].U.n;
-            a.Hin = lh;
-            a.Win = lw;
-            a.cs_in = lv_[0].U.cs;
-            a.c_in = head_->c_in;
-            a.up2 = 0;
-            a.s = s;
-            a.o = o;
-            a.apply_affine = 1;
-            a.w = head_->w.as<float>();
-            a.bias = head_->bias.as<float>();
-            a.c_out = head_->c_out;
-            a.k = head_->k;
-            a.out = eps2_dev;
-            a.win = wd;
-            LC_CUDA(launch_thin_out(a, s_compute_));
+            run_tc_conv(*head_tc_, &lv_[0].U, eps_view, wd, s, o, false, s_compute_, eps2_dev);
             ++launches;
         }
     }
+}
+
+// Swap transfers (TransferEngine evict/prefetch, proj/src/swap.cpp:284-304).
+// One "transfer" = one CFG branch entry (half of the b=2 cache, contiguous
+// since b is the outermost image index).  Each entry moves in chunks of
+// kSwapChunk bytes so the H2D prefetch of chunk i can start as soon as its
+// D2H eviction lands (PCIe is full duplex); async mode uses dedicated D2H
+// and H2D streams ordered by CUDA events, sync mode serialises on compute.
+static constexpr int64_t kSwapChunk = 4 << 20;
+
+cudaEvent_t Engine::chunk_event(int b, size_t i) {
+    while (ev_chunk_[b].size() <= i) {
+        cudaEvent_t e;
+        LC_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ev_chunk_[b].push_back(e);
+    }
+    return ev_chunk_[b][i];
 }
 
 void Engine::issue_evict(int step) {
     if (!cache_host_.p) return;
     const bool async = cfg_.swap_mode == SwapMode::Async;
     cudaStream_t st = async ? s_d2h_ : s_compute_;
-    LC_CUDA(cudaEventRecord(ev_cache_ready_, s_compute_));
+    // The entry is complete once U_{m+1} was produced: on a full step that
+    // event was recorded right after the producing block (forward_dev), so
+    // the copy overlaps the remaining up path; at a seam it is recorded now.
+    if (!cache_ready_recorded_) LC_CUDA(cudaEventRecord(ev_cache_ready_, s_compute_));
+    cache_ready_recorded_ = false;
     if (async) LC_CUDA(cudaStreamWaitEvent(st, ev_cache_ready_, 0));
-    const int64_t half = cache_.elems();  // halves in elements of one branch (n = 2T)
-    const int64_t bytes = half;           // elems()*2 bytes / 2 branches
+    const int64_t bytes = cache_.elems();  // one branch: elems()*2 bytes / 2 branches
     for (int b = 0; b < 2; ++b) {
         record(2, step, bytes, st);
-        LC_CUDA(cudaMemcpyAsync(cache_host_.as<char>() + b * bytes, reinterpret_cast<char*>(cache_.p) + b * bytes,
-                                static_cast<size_t>(bytes), cudaMemcpyDeviceToHost, st));
+        size_t ci = 0;
+        for (int64_t off = 0; off < bytes; off += kSwapChunk, ++ci) {
+            const int64_t len = std::min(kSwapChunk, bytes - off);
+            LC_CUDA(cudaMemcpyAsync(cache_host_.as<char>() + b * bytes + off,
+                                    reinterpret_cast<char*>(cache_.p) + b * bytes + off, static_cast<size_t>(len),
+                                    cudaMemcpyDeviceToHost, st));
+            LC_CUDA(cudaEventRecord(chunk_event(b, ci), st));
+        }
         record(3, step, bytes, st);
         LC_CUDA(cudaEventRecord(ev_evict_[b], st));
-        if (stats_) {
-            stats_->swap_bytes += bytes;
-        }
+        if (stats_) stats_->swap_bytes += bytes;
     }
     if (stats_) stats_->swap_calls += 1;
     evict_pending_ = true;
@@ -751,10 +854,15 @@ void Engine::issue_prefetch(int issued, int needed) {
     cudaStream_t st = async ? s_h2d_ : s_compute_;
     const int64_t bytes = cache_.elems();
     for (int b = 0; b < 2; ++b) {
-        if (async) LC_CUDA(cudaStreamWaitEvent(st, ev_evict_[b], 0));
         record(2, needed, bytes, st);
-        LC_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(cache_.p) + b * bytes, cache_host_.as<char>() + b * bytes,
-                                static_cast<size_t>(bytes), cudaMemcpyHostToDevice, st));
+        size_t ci = 0;
+        for (int64_t off = 0; off < bytes; off += kSwapChunk, ++ci) {
+            const int64_t len = std::min(kSwapChunk, bytes - off);
+            if (async) LC_CUDA(cudaStreamWaitEvent(st, chunk_event(b, ci), 0));
+            LC_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(cache_.p) + b * bytes + off,
+                                    cache_host_.as<char>() + b * bytes + off, static_cast<size_t>(len),
+                                    cudaMemcpyHostToDevice, st));
+        }
         record(3, needed, bytes, st);
         LC_CUDA(cudaEventRecord(ev_prefetch_[b], st));
         if (stats_) stats_->swap_bytes += bytes;
@@ -795,6 +903,9 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
             a.p = dec_bufs_.back().as<__half>();
             dec_act_[i] = a;
         }
+        dec_patch_ = Act{nullptr, G, lh, lw, dec0_kp_, dec0_kp_};
+        dec_patch_buf_ = dev_alloc(&ledger_, dec_patch_.elems() * 2, true);
+        dec_patch_.p = dec_patch_buf_.as<__half>();
         dec_alloc_ = G;
     }
     const int C = static_cast<int>(cfg_.latent_channels), IC = static_cast<int>(cfg_.image_channels);
@@ -821,35 +932,30 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
         a.c_out = dec0_->c_out;
         a.k = 3;
         a.silu = 1;
-        a.out = e[0].p;
-        a.cs_out = e[0].cs;
+        Act patch = dec_patch_;
+        patch.n = gs;
+        a.out = patch.p;
+        a.cs_out = patch.cs;
         a.win = Window{0, lh, 0, lw, 0, lh, 0, lw};
-        LC_CUDA(launch_thin_in(a, s_compute_));
-        ++launches;
+        LC_CUDA(launch_patch(a, dec0_kp_, s_compute_));
+        run_tc_conv(*dec0_tc_, &patch, e[0], a.win, 1.0f, 0.0f, true, s_compute_);
+        launches += 2;
         for (int i = 1; i < S; ++i) {
             const int h = lh << i, w = lw << i;
             run_tc_conv(*dec_tc_[i - 1], &e[i - 1], e[i], Window{0, h, 0, w, 0, h, 0, w}, 1.0f, 0.0f, true,
                         s_compute_);
             ++launches;
         }
-        ThinOutArgs t{};
-        t.x = e[S - 1].p;
-        t.nimg = gs;
-        t.Hin = lh << (S - 1);
-        t.Win = lw << (S - 1);
-        t.cs_in = e[S - 1].cs;
-        t.c_in = static_cast<int>(cfg_.codec_width);
-        t.up2 = 1;
-        t.s = 1.0f;
-        t.o = 0.0f;
-        t.apply_affine = 0;
-        t.w = dec_last_->w.as<float>();
-        t.bias = dec_last_->bias.as<float>();
-        t.c_out = IC;
-        t.k = 3;
-        t.out = video_dev + g0 * IC * H * W;
-        t.win = Window{0, H, 0, W, 0, H, 0, W};
-        LC_CUDA(launch_thin_out(t, s_compute_));
+        // last conv: sub-pixel 3x3 on the low-res image with 4x3 outputs,
+        // depth-to-space into the fp32 NCHW video
+        const int hl = lh << (S - 1), wl = lw << (S - 1);
+        Act vid;
+        vid.n = gs;
+        vid.h = H;
+        vid.w = W;
+        vid.c = IC;
+        run_tc_conv(*dec_last_tc_, &e[S - 1], vid, Window{0, hl, 0, wl, 0, hl, 0, wl}, 1.0f, 0.0f, false,
+                    s_compute_, video_dev + g0 * IC * H * W, IC);
         ++launches;
     }
 }
@@ -908,7 +1014,8 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
         const int64_t t_orig = sc.src[j];
         const bool full = plan.is_full(s);
         record(0, static_cast<int>(s), 0, s_compute_);
-        const int seam = (!full && swap) ? (plan.is_last_consumer(s) ? 2 : 1) : 0;
+        // 3: full step whose store will be evicted (mark the cache-ready point)
+        const int seam = swap ? (full ? 3 : (plan.is_last_consumer(s) ? 2 : 1)) : 0;
         forward_dev(x_.as<float>(), false, T, t_orig, full, eps2_.as<float>(), static_cast<int>(s), seam);
         record(1, static_cast<int>(s), 0, s_compute_);
         if (full) {

@@ -113,8 +113,18 @@ void set_conv_profiler(ConvProfiler* p);
 // segment operands in source coordinates; `win` the valid window of the
 // operand of segment 0 in ITS coordinates ({0,h,0,w} = whole image) and the
 // output region in output-pixel coordinates.
+// out32 non-null: write fp32 NCHW (out.n, c_out, out.h, out.w) instead of
+// fp16 NHWC into out.p.
 void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window& win, float s,
-                 float o, bool silu, cudaStream_t st);
+                 float o, bool silu, cudaStream_t st, float* out32 = nullptr, int shuffle_c = 0);
+
+// Bank of a thin-input conv re-expressed as a 1x1 conv over gathered
+// patches (see launch_patch): c_in' = roundup64(c_in*k*k).
+Bank patch_bank(const Bank& b);
+// Last decoder conv (nearest upsample + 3x3, c_out small) re-expressed as a
+// 3x3 conv on the low-res image with 4*c_out outputs (one per parity) --
+// the sub-pixel form -- followed by depth-to-space in the epilogue.
+Bank subpixel_shuffle_bank(const Bank& b);
 
 // ---------------------------------------------------------------- engine
 struct RunStats {
@@ -180,7 +190,8 @@ private:
     };
     void alloc_activations(int64_t T);
     // seam: 0 no swap, 1 await the prefetch at the seam, 2 await + evict
-    // (last consumer).  stacked: x_dev holds the explicit (2,T,...) CFG
+    // (last consumer), 3 full step with swap (record the cache-ready event
+    // after the U_{m+1} producer).  stacked: x_dev holds the explicit (2,T,...) CFG
     // stack instead of the b=1 latent.
     void forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t timestep, bool full,
                      float* eps2_dev, int step, int seam);
@@ -202,6 +213,13 @@ private:
     std::vector<std::unique_ptr<TcLayer>> tc_;     // per block (nullptr for thin)
     std::vector<std::unique_ptr<TcLayer>> tc_fb_;  // up blocks: materialised-upsample fallback
     std::unique_ptr<ThinLayer> stem_, head_;
+    std::unique_ptr<TcLayer> head_tc_;  // head on the tensor cores (N padded to 16)
+    std::unique_ptr<TcLayer> stem_tc_, dec0_tc_, dec_last_tc_;
+    int stem_kp_ = 64, dec0_kp_ = 64;
+    Act patch_;                          // stem patch rows (2T, h, w, kp)
+    DevBuf patch_buf_, dec_patch_buf_;
+    Act dec_patch_;
+    DevBuf dec_last_wm_;                // merged sub-pixel weights of the last decoder conv
     std::vector<std::unique_ptr<TcLayer>> dec_tc_;  // decoder stages 1..S-1
     std::unique_ptr<ThinLayer> dec0_, dec_last_;
     std::vector<Level> lv_;
@@ -228,7 +246,9 @@ private:
     std::vector<Mark> marks_;
     cudaEvent_t ev_evict_[2] = {nullptr, nullptr}, ev_prefetch_[2] = {nullptr, nullptr},
                 ev_cache_ready_ = nullptr;
-    bool evict_pending_ = false, prefetch_pending_ = false;
+    bool evict_pending_ = false, prefetch_pending_ = false, cache_ready_recorded_ = false;
+    std::vector<cudaEvent_t> ev_chunk_[2];
+    cudaEvent_t chunk_event(int b, size_t i);
     int prefetch_tag_ = -1;
     RunStats* stats_ = nullptr;
     cudaEvent_t next_event();
