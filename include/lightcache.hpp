@@ -1,0 +1,107 @@
+// lightcache.hpp -- header-only C++ mirror of the reference's operator and
+// config API (namespace stagecache, /root/reference/proj/include/stagecache)
+// over the C-ABI of liblightcache.so.  Same names, argument meaning and
+// error behaviour: every failure rethrows the reference exception type for
+// the status code (proj/include/stagecache/common.hpp:33-57).
+//
+// A reference user switches by replacing
+//     #include "stagecache/pipeline.hpp"      stagecache::run_pipeline(cfg)
+// with
+//     #include "lightcache.hpp"               stagecache_b200::run_pipeline(text)
+// where `text` is the reference's own config grammar (config_to_text output
+// or a config file's contents), so existing configs and --set overrides
+// carry over unchanged.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lightcache.h"
+
+namespace stagecache_b200 {
+
+struct Error : std::runtime_error {
+    explicit Error(const std::string& m) : std::runtime_error(m) {}
+};
+struct ShapeError : Error {
+    using Error::Error;
+};
+struct ConfigError : Error {
+    using Error::Error;
+};
+struct BudgetError : Error {
+    using Error::Error;
+};
+struct InvariantError : Error {
+    using Error::Error;
+};
+struct DeviceError : Error {
+    using Error::Error;
+};
+
+inline void check(int rc) {
+    if (rc == 0) return;
+    const std::string m = lc_last_error();
+    switch (rc) {
+        case 1: throw ShapeError(m);
+        case 2: throw ConfigError(m);
+        case 3: throw BudgetError(m);
+        case 4: throw InvariantError(m);
+        default: throw DeviceError(m);
+    }
+}
+
+// StepPlan / plan_steps (proj/include/stagecache/cache.hpp:27-40).
+struct StepPlan {
+    std::vector<int8_t> kinds, flags;
+    bool is_full(int64_t s) const { return kinds[static_cast<size_t>(s)] != 0; }
+    bool has_consumers(int64_t s) const { return (flags[static_cast<size_t>(s)] & 1) != 0; }
+    bool is_last_consumer(int64_t s) const { return (flags[static_cast<size_t>(s)] & 2) != 0; }
+};
+inline StepPlan plan_steps(int64_t total, int64_t interval_n) {
+    StepPlan p;
+    p.kinds.resize(static_cast<size_t>(total > 0 ? total : 0));
+    p.flags.resize(p.kinds.size());
+    check(lc_plan_steps(total, interval_n, p.kinds.data(), p.flags.data()));
+    return p;
+}
+
+// RunResult subset (proj/include/stagecache/pipeline.hpp:18-39): the
+// decoded video {t,c,h,w} fp32 plus the JSON report (device ms per stage,
+// MAC counters, cache bytes, swap timeline, per-stage peaks).
+struct RunResult {
+    std::vector<float> video;
+    std::string report_json;
+};
+
+// One GPU context (weights, buffers, streams).
+class Context {
+public:
+    explicit Context(int device = 0) { check(lc_ctx_create(device, &ctx_)); }
+    ~Context() { lc_ctx_destroy(ctx_); }
+    Context(const Context&) = delete;
+    Context& operator=(const Context&) = delete;
+
+    // run_pipeline (proj/src/pipeline.cpp:64) for a config in the reference grammar.
+    RunResult run_pipeline(const std::string& config_text) {
+        check(lc_configure(ctx_, config_text.c_str()));
+        RunResult r;
+        r.video.resize(static_cast<size_t>(lc_video_elems(ctx_)));
+        std::vector<char> rep(1 << 22);
+        check(lc_run_pipeline(ctx_, nullptr, r.video.data(), nullptr, rep.data(),
+                              static_cast<int64_t>(rep.size())));
+        r.report_json = rep.data();
+        return r;
+    }
+    lc_ctx* raw() { return ctx_; }
+
+private:
+    lc_ctx* ctx_ = nullptr;
+};
+
+inline void validate_config(const std::string& config_text) { check(lc_config_check(config_text.c_str())); }
+
+}  // namespace stagecache_b200

@@ -21,6 +21,23 @@ def test_library_exports_every_declared_symbol():
         assert isinstance(getattr(L, name), ctypes._CFuncPtr), name
 
 
+def test_cpp_mirror_compiles_and_runs(tmp_path):
+    """include/lightcache.hpp (stagecache-style C++ API over the C-ABI) links
+    against liblightcache.so and maps status codes to the reference's
+    exception types."""
+    import os
+    import subprocess
+    root = lc.REPO_ROOT
+    exe = str(tmp_path / "demo")
+    libdir = os.path.dirname(lc.LIB_PATH)
+    subprocess.run(["g++", "-std=c++20", "-I" + os.path.join(root, "include"),
+                    os.path.join(root, "tools", "cpp", "host_api_demo.cpp"), "-L" + libdir, "-llightcache",
+                    "-Wl,-rpath," + libdir, "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, check=True).stdout
+    assert out.splitlines()[0].split() == ["F+", "c", "c!", "F+", "c", "c!", "F"]
+    assert "ConfigError: unknown config key" in out
+
+
 def test_library_is_sm100a():
     import subprocess
     out = subprocess.run(["cuobjdump", "--list-elf", lc.LIB_PATH], capture_output=True, text=True).stdout
