@@ -65,7 +65,12 @@ struct alignas(64) ConvParams {
     float scale;                  // s / weight_scale
     float shift;                  // o
     int silu;
+    int cg;                       // 1: one CTA per M=128 tile; 2: CTA pair, M=256 (cta_group::2)
 };
+
+// CTA-group choice for a launch (the weight tensor map's box depends on it:
+// each CTA of a pair stages BN/2 weight rows).
+int conv_tc_cta_group(int BN, int m_tiles, int n_tiles, int parities, int k_blocks);
 
 struct ConvTcConfig {
     int stages;

@@ -121,7 +121,14 @@ void class_geom(int d_lo, int d_hi, int rc, int* L, int* Y) {
 }  // namespace
 
 // ------------------------------------------------------- layer packing
-std::unique_ptr<TcLayer> pack_tc_layer(Ledger* l, const Bank& b, int c_split, int mode) {
+int est_m_tiles(int n, int h, int w) {
+    const int TW = std::min(w, 128);
+    const int TH = std::max(1, std::min(h, 128 / TW));
+    const int TI = std::max(1, std::min(n, 128 / (TW * TH)));
+    return ((n + TI - 1) / TI) * ((h + TH - 1) / TH) * ((w + TW - 1) / TW);
+}
+
+std::unique_ptr<TcLayer> pack_tc_layer(Ledger* l, const Bank& b, int c_split, int mode, int m_tiles_hint) {
     auto L = std::make_unique<TcLayer>();
     L->mode = mode;
     L->k = static_cast<int>(b.k);
@@ -183,10 +190,24 @@ std::unique_ptr<TcLayer> pack_tc_layer(Ledger* l, const Bank& b, int c_split, in
         L->seg_kbase[s] = L->k_total;
         L->k_total += L->seg_ntaps[s] * L->seg_cpad[s];
     }
-    // N tiling
+    // N tiling: fewest N tiles of <= 256 columns (largest BN: least A
+    // re-reading, best MMA/smem ratio).  Only when that leaves the machine
+    // under-filled (fewer tiles than SMs, e.g. the mid block at 8x8) the
+    // largest BN that yields >= ~80% of the SMs is used instead.
     int nt = 1;
     while (round_up((L->c_out + nt - 1) / nt, 16) > 256) ++nt;
     L->BN = round_up((L->c_out + nt - 1) / nt, 16);
+    if (m_tiles_hint > 0 && L->c_out > 64 &&
+        static_cast<int64_t>(m_tiles_hint) * nt * L->P < 148) {
+        for (int bn = L->BN; bn >= 64; bn -= 16) {
+            const int n_t = (L->c_out + bn - 1) / bn;
+            if (static_cast<int64_t>(m_tiles_hint) * n_t * L->P >= 120) {
+                L->BN = bn;
+                break;
+            }
+        }
+        nt = (L->c_out + L->BN - 1) / L->BN;
+    }
     L->n_pad = nt * L->BN;
     // power-of-two weight scale ~ sqrt(fan_in): exact to undo in fp32
     const double fan_in = static_cast<double>(k) * k * c_in;
@@ -389,7 +410,8 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
                                   static_cast<uint64_t>(L.P)};
         const uint64_t strides[2] = {static_cast<uint64_t>(L.k_total) * 2,
                                      static_cast<uint64_t>(L.n_pad) * L.k_total * 2};
-        const uint32_t box[3] = {64, static_cast<uint32_t>(L.BN), 1};
+        p.cg = conv_tc_cta_group(L.BN, p.tiles_x * p.tiles_y * p.tiles_i, L.n_pad / L.BN, L.P, L.k_total / 64);
+        const uint32_t box[3] = {64, static_cast<uint32_t>(L.BN / p.cg), 1};
         const uint32_t estr[3] = {1, 1, 1};
         encode_map(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, L.w.p, dims, strides, box, estr);
     }
@@ -449,6 +471,9 @@ Engine::Engine(int device) : device_(device) {
         LC_CUDA(cudaEventCreateWithFlags(&ev_prefetch_[b], cudaEventDisableTiming));
     }
     LC_CUDA(cudaEventCreateWithFlags(&ev_cache_ready_, cudaEventDisableTiming));
+    LC_CUDA(cudaEventCreate(&ev_start_));
+    for (int b = 0; b < 2; ++b) LC_CUDA(cudaEventCreateWithFlags(&ev_join_[b], cudaEventDisableTiming));
+    if (const char* e = std::getenv("LC_NO_GRAPH")) use_graphs = (e[0] == '0');
 }
 
 Engine::~Engine() {
@@ -462,6 +487,9 @@ Engine::~Engine() {
         cudaEventDestroy(ev_prefetch_[b]);
     }
     cudaEventDestroy(ev_cache_ready_);
+    cudaEventDestroy(ev_start_);
+    for (int b = 0; b < 2; ++b) cudaEventDestroy(ev_join_[b]);
+    if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     cudaStreamDestroy(s_compute_);
     cudaStreamDestroy(s_d2h_);
     cudaStreamDestroy(s_h2d_);
@@ -476,9 +504,19 @@ cudaEvent_t Engine::next_event() {
     return ev_pool_[ev_next_++];
 }
 
+// Timing event record: inside a stream capture it must become an event
+// record NODE (cudaEventRecordExternal) so graph replays re-record it; a
+// plain record would only express a capture dependency.
+void record_timing(cudaEvent_t e, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    LC_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs == cudaStreamCaptureStatusActive) LC_CUDA(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+    else LC_CUDA(cudaEventRecord(e, st));
+}
+
 void Engine::record(int kind, int step, int64_t bytes, cudaStream_t st) {
     cudaEvent_t e = next_event();
-    LC_CUDA(cudaEventRecord(e, st));
+    record_timing(e, st);
     marks_.push_back({kind, step, bytes, e});
 }
 
@@ -486,7 +524,9 @@ static std::string weights_key(const RunConfig& c) {
     return std::to_string(c.depth) + "/" + std::to_string(c.base_channels) + "/" + std::to_string(c.kernel) +
            "/" + std::to_string(c.cache_depth) + "/" + std::to_string(c.in_channels) + "/" +
            std::to_string(c.unet_seed) + "/" + std::to_string(c.stages) + "/" + std::to_string(c.codec_width) +
-           "/" + std::to_string(c.codec_seed);
+           "/" + std::to_string(c.codec_seed) +
+           // geometry steers the N tiling of the packed layers
+           "/" + std::to_string(c.frames) + "x" + std::to_string(c.height) + "x" + std::to_string(c.width);
 }
 
 void Engine::configure(const RunConfig& cfg) {
@@ -510,13 +550,18 @@ void Engine::configure(const RunConfig& cfg) {
         for (size_t j = 0; j < plan.size(); ++j) {
             const auto& bp = plan[j];
             if (bp.name == "stem" || bp.name == "head") continue;
+            // M-tile hints from the run geometry (2T images at the block's level)
+            const int n2 = static_cast<int>(2 * cfg.frames);
+            const int hl = static_cast<int>(cfg.latent_h() >> bp.level), wl = static_cast<int>(cfg.latent_w() >> bp.level);
             if (bp.name[0] == 'u') {
                 const int i = std::stoi(bp.name.substr(1));
                 const int c_skip = static_cast<int>(cfg.base_channels << i);
-                if (cfg.kernel == 3) tc_[j] = pack_tc_layer(&ledger_, uw_.banks[j], c_skip, 1);
-                tc_fb_[j] = pack_tc_layer(&ledger_, uw_.banks[j], c_skip, 0);
+                if (cfg.kernel == 3)
+                    tc_[j] = pack_tc_layer(&ledger_, uw_.banks[j], c_skip, 1,
+                                           est_m_tiles(n2, std::max(1, hl / 2), std::max(1, wl / 2)));
+                tc_fb_[j] = pack_tc_layer(&ledger_, uw_.banks[j], c_skip, 0, est_m_tiles(n2, hl, wl));
             } else {
-                tc_[j] = pack_tc_layer(&ledger_, uw_.banks[j], static_cast<int>(bp.c_in), 0);
+                tc_[j] = pack_tc_layer(&ledger_, uw_.banks[j], static_cast<int>(bp.c_in), 0, est_m_tiles(n2, hl, wl));
             }
         }
         stem_ = pack_thin_layer(&ledger_, uw_.banks.front());
@@ -564,6 +609,7 @@ void Engine::configure(const RunConfig& cfg) {
         T_alloc_ = -1;
         dec_alloc_ = -1;
     }
+    invalidate_graph();  // any config change re-records the body
     configured_ = true;
 }
 
@@ -574,6 +620,8 @@ int64_t Engine::video_elems() const { return cfg_.frames * cfg_.image_channels *
 
 void Engine::alloc_activations(int64_t T) {
     if (T_alloc_ == T) return;
+    invalidate_graph();
+    z_key_.clear();
     act_bufs_.clear();
     cache_buf_.reset();
     cache_host_.reset();
@@ -625,7 +673,7 @@ void Engine::alloc_activations(int64_t T) {
     x0_ = dev_alloc(&ledger_, nl * 4, true);
     x_ = dev_alloc(&ledger_, nl * 4, true);
     xn_ = dev_alloc(&ledger_, nl * 4, true);
-    z_ = dev_alloc(&ledger_, nl * 4, true);
+    z_.reset();  // ancestral noise, allocated by prepare_noise()
     eps2_ = dev_alloc(&ledger_, 2 * nl * 4, true);
     bad_ = dev_alloc(&ledger_, 16, true);
     video_ = dev_alloc(&ledger_, T * cfg_.image_channels * cfg_.height * cfg_.width * 4, false);
@@ -641,6 +689,13 @@ static std::vector<Window> block_windows(const RunConfig& c, const std::string& 
     int64_t halo = 0;
     const auto tiles = split(h, w, c.eta, c.omega, c.halo, c.halo_px, c.kernel, &halo);
     const int64_t r = (c.kernel - 1) / 2;
+    // A halo >= the receptive radius makes every tile read the whole image
+    // window its core needs, i.e. tiled == untiled (the reference's lossless
+    // case, proj/tests/test_chunk.cpp:118-160).  The fused kernels never
+    // materialise a tile, so the tiles of that case run as ONE launch over
+    // the union of the cores (the full image): identical bytes, no per-tile
+    // tails.  Halos below the radius (seams) keep one launch per tile.
+    if (halo >= r) return {Window{0, h, 0, w, 0, h, 0, w}};
     std::vector<Window> out;
     for (const Tile& t : tiles) {
         Window wd;
@@ -830,6 +885,7 @@ void Engine::issue_evict(int step) {
     if (async) LC_CUDA(cudaStreamWaitEvent(st, ev_cache_ready_, 0));
     const int64_t bytes = cache_.elems();  // one branch: elems()*2 bytes / 2 branches
     for (int b = 0; b < 2; ++b) {
+        if (async) side_used_ = true;
         record(2, step, bytes, st);
         size_t ci = 0;
         for (int64_t off = 0; off < bytes; off += kSwapChunk, ++ci) {
@@ -854,6 +910,7 @@ void Engine::issue_prefetch(int issued, int needed) {
     cudaStream_t st = async ? s_h2d_ : s_compute_;
     const int64_t bytes = cache_.elems();
     for (int b = 0; b < 2; ++b) {
+        if (async) side_used_ = true;
         record(2, needed, bytes, st);
         size_t ci = 0;
         for (int64_t off = 0; off < bytes; off += kSwapChunk, ++ci) {
@@ -891,6 +948,7 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
     const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
     const int G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cfg_.slice_decode ? decode_slice : n, n)));
     if (dec_alloc_ != G) {
+        invalidate_graph();
         dec_bufs_.clear();
         for (int i = 0; i < S; ++i) {
             Act a;
@@ -960,20 +1018,42 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
     }
 }
 
-RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host, bool resident_input) {
-    if (cfg_.mode != "text") throw_config("run.mode=image: the encode stage is not built on the GPU path yet");
-    RunStats st;
-    stats_ = &st;
-    marks_.clear();
-    ev_next_ = 0;
-    launches = 0;
+void Engine::invalidate_graph() {
+    if (graph_exec_) {
+        cudaGraphExecDestroy(graph_exec_);
+        graph_exec_ = nullptr;
+    }
+    eager_runs_ = 0;
+}
+
+// Ancestral per-step noise randn(derive_seed(seed, 0x1000 + s))
+// (pipeline.cpp:181-182), drawn on the host with the reference's
+// SplitMix64/Box-Muller stream (libm double log/sqrt/cos/sin, bit-exact with
+// the reference) once per config and kept resident: S x n floats.
+void Engine::prepare_noise() {
+    if (cfg_.sampler != Sampler::Ancestral) return;
+    const int64_t nl = latent_elems(), S = cfg_.steps;
+    const std::string key = std::to_string(cfg_.seed) + "/" + std::to_string(S) + "/" + std::to_string(nl) +
+                            "/" + std::to_string(cfg_.train_steps);
+    if (key == z_key_) return;
+    invalidate_graph();
+    z_ = dev_alloc(&ledger_, S * nl * 4, true);
+    const Schedule sc = make_schedule(cfg_);
+    std::vector<float> z(static_cast<size_t>(nl));
+    for (int64_t s = 0; s < S; ++s) {
+        const StepCoeffs k = step_coeffs(cfg_, sc, s);
+        if (!k.has_noise) continue;
+        randn(k.noise_seed, nl, z.data());
+        LC_CUDA(cudaMemcpy(z_.as<float>() + s * nl, z.data(), static_cast<size_t>(nl) * 4, cudaMemcpyHostToDevice));
+    }
+    z_key_ = key;
+}
+
+// Denoise loop + decode for the current config, enqueued on the compute
+// stream (and the two copy streams).  Fully asynchronous, so it can be
+// captured into a CUDA graph and replayed (Engine::run).
+void Engine::enqueue_body(RunStats& st) {
     const int64_t T = cfg_.frames;
-    alloc_activations(T);
-    ledger_.budget_fast = cfg_.budget_fast_bytes;
-    if (cfg_.budget_fast_bytes > 0 && ledger_.occ[0] > cfg_.budget_fast_bytes)
-        throw LcError(kBudgetError, "fast-tier budget exceeded in stage denoise: " +
-                                        std::to_string(ledger_.occ[0]) + " > " +
-                                        std::to_string(cfg_.budget_fast_bytes) + " bytes");
     const Schedule sc = make_schedule(cfg_);
     const StepPlan plan = cfg_.cache_enabled ? plan_steps(cfg_.steps, cfg_.cache_n)
                                              : StepPlan{std::vector<bool>(static_cast<size_t>(cfg_.steps), true)};
@@ -981,9 +1061,93 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
     const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
     const bool swap = cfg_.cache_enabled && cfg_.swap_mode != SwapMode::Off;
     evict_pending_ = prefetch_pending_ = false;
+    side_used_ = false;
+    marks_.clear();
+    ev_next_ = 0;
+    launches = 0;
+    ev_den0_ = next_event();
+    ev_den1_ = next_event();
+    ev_end_ = next_event();
+    record(6, -1, 0, s_compute_);  // timeline origin inside the body
 
-    LC_CUDA(cudaEventRecord(ev_base_, s_compute_));
-    cudaEvent_t t_start = next_event(), t_den0 = next_event(), t_den1 = next_event(), t_end = next_event();
+    LC_CUDA(cudaMemsetAsync(bad_.p, 0, 16, s_compute_));
+    LC_CUDA(launch_isfinite(x_.as<float>(), nl, bad_.as<int>(), s_compute_));
+    ++launches;
+    record_timing(ev_den0_, s_compute_);
+    st.macs_full = flops_estimate(cfg_, 2, T, lh, lw, false);
+    st.macs_cached = flops_estimate(cfg_, 2, T, lh, lw, true);
+    const int64_t S = cfg_.steps;
+    float* xa = x_.as<float>();
+    float* xb = xn_.as<float>();
+    for (int64_t s = 0; s < S; ++s) {
+        const int64_t j = S - 1 - s;
+        const int64_t t_orig = sc.src[j];
+        const bool full = plan.is_full(s);
+        record(0, static_cast<int>(s), 0, s_compute_);
+        // 3: full step whose store will be evicted (mark the cache-ready point)
+        const int seam = swap ? (full ? 3 : (plan.is_last_consumer(s) ? 2 : 1)) : 0;
+        forward_dev(xa, false, T, t_orig, full, eps2_.as<float>(), static_cast<int>(s), seam);
+        record(1, static_cast<int>(s), 0, s_compute_);
+        if (full) {
+            st.full_steps++;
+            st.denoiser_macs += st.macs_full;
+            if (swap) {
+                issue_evict(static_cast<int>(s));
+                if (plan.has_consumers(s)) issue_prefetch(static_cast<int>(s), static_cast<int>(s + 1));
+            }
+        } else {
+            st.cached_steps++;
+            st.denoiser_macs += st.macs_cached;
+        }
+        const StepCoeffs k = step_coeffs(cfg_, sc, s);
+        StepArgs a{};
+        a.eps2 = eps2_.as<float>();
+        a.x = xa;
+        a.x_out = xb;
+        // ancestral noise randn(derive_seed(seed, 0x1000+s)) (pipeline.cpp:181),
+        // drawn on the host once per config (rng.hpp, bit-exact) and resident
+        a.z = k.has_noise ? z_.as<float>() + s * nl : nullptr;
+        a.n = nl;
+        a.g = static_cast<float>(cfg_.guidance);
+        a.a = k.a;
+        a.b = k.b;
+        a.c = k.noise;
+        a.bad = bad_.as<int>();
+        LC_CUDA(launch_step(a, s_compute_));
+        ++launches;
+        std::swap(xa, xb);
+    }
+    x_final_ = xa;
+    record_timing(ev_den1_, s_compute_);
+    ledger_.enter(kDecode);
+    decode_dev(xa, T, video_.as<float>());
+    if (side_used_) {
+        // join the copy streams (required to close a graph capture; the last
+        // eviction stays in flight through decode as in the reference)
+        LC_CUDA(cudaEventRecord(ev_join_[0], s_d2h_));
+        LC_CUDA(cudaEventRecord(ev_join_[1], s_h2d_));
+        LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_join_[0], 0));
+        LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_join_[1], 0));
+    }
+    record_timing(ev_end_, s_compute_);
+}
+
+RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host, bool resident_input) {
+    if (cfg_.mode != "text") throw_config("run.mode=image: the encode stage is not built on the GPU path yet");
+    RunStats st;
+    stats_ = &st;
+    const int64_t T = cfg_.frames;
+    alloc_activations(T);
+    ledger_.budget_fast = cfg_.budget_fast_bytes;
+    if (cfg_.budget_fast_bytes > 0 && ledger_.occ[0] > cfg_.budget_fast_bytes)
+        throw LcError(kBudgetError, "fast-tier budget exceeded in stage denoise: " +
+                                        std::to_string(ledger_.occ[0]) + " > " +
+                                        std::to_string(cfg_.budget_fast_bytes) + " bytes");
+    const int64_t nl = latent_elems();
+    const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
+    prepare_noise();
+
+    cudaEvent_t t_start = ev_start_;
     LC_CUDA(cudaEventRecord(t_start, s_compute_));
     ledger_.enter(kEncode);
     if (!resident_input) {
@@ -999,68 +1163,44 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
     } else {
         LC_CUDA(cudaMemcpyAsync(x_.p, x0_.p, static_cast<size_t>(nl) * 4, cudaMemcpyDeviceToDevice, s_compute_));
     }
-    LC_CUDA(cudaMemsetAsync(bad_.p, 0, 16, s_compute_));
-    LC_CUDA(launch_isfinite(x_.as<float>(), nl, bad_.as<int>(), s_compute_));
-    ++launches;
 
     ledger_.enter(kDenoise);
-    LC_CUDA(cudaEventRecord(t_den0, s_compute_));
-    st.macs_full = flops_estimate(cfg_, 2, T, lh, lw, false);
-    st.macs_cached = flops_estimate(cfg_, 2, T, lh, lw, true);
-    const int64_t S = cfg_.steps;
-    std::vector<float> znoise;
-    for (int64_t s = 0; s < S; ++s) {
-        const int64_t j = S - 1 - s;
-        const int64_t t_orig = sc.src[j];
-        const bool full = plan.is_full(s);
-        record(0, static_cast<int>(s), 0, s_compute_);
-        // 3: full step whose store will be evicted (mark the cache-ready point)
-        const int seam = swap ? (full ? 3 : (plan.is_last_consumer(s) ? 2 : 1)) : 0;
-        forward_dev(x_.as<float>(), false, T, t_orig, full, eps2_.as<float>(), static_cast<int>(s), seam);
-        record(1, static_cast<int>(s), 0, s_compute_);
-        if (full) {
-            st.full_steps++;
-            st.denoiser_macs += st.macs_full;
-            if (swap) {
-                issue_evict(static_cast<int>(s));
-                if (plan.has_consumers(s)) issue_prefetch(static_cast<int>(s), static_cast<int>(s + 1));
-            }
-        } else {
-            st.cached_steps++;
-            st.denoiser_macs += st.macs_cached;
+    // The body is enqueued eagerly on the first run after (re)configuration
+    // (allocations, kernel attributes), captured into a CUDA graph on the
+    // second, and replayed from then on: the host no longer paces ~70
+    // launches per video (tensor-map encoding, parameter setup).
+    const bool can_graph = use_graphs && conv_profiler() == nullptr;
+    if (graph_exec_ && graph_slice_ != decode_slice) invalidate_graph();
+    graph_slice_ = decode_slice;
+    if (can_graph && graph_exec_) {
+        LC_CUDA(cudaGraphLaunch(graph_exec_, s_compute_));
+        st = graph_stats_;
+        stats_ = &st;
+    } else if (can_graph && eager_runs_ > 0) {
+        cudaGraph_t g = nullptr;
+        LC_CUDA(cudaStreamBeginCapture(s_compute_, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue_body(st);
+        } catch (...) {
+            cudaStreamEndCapture(s_compute_, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
         }
-        const StepCoeffs k = step_coeffs(cfg_, sc, s);
-        if (k.has_noise) {
-            znoise.resize(static_cast<size_t>(nl));
-            randn(k.noise_seed, nl, znoise.data());
-            LC_CUDA(cudaMemcpyAsync(z_.p, znoise.data(), static_cast<size_t>(nl) * 4, cudaMemcpyHostToDevice,
-                                    s_compute_));
-            LC_CUDA(cudaStreamSynchronize(s_compute_));
-        }
-        StepArgs a{};
-        a.eps2 = eps2_.as<float>();
-        a.x = x_.as<float>();
-        a.x_out = xn_.as<float>();
-        a.z = k.has_noise ? z_.as<float>() : nullptr;
-        a.n = nl;
-        a.g = static_cast<float>(cfg_.guidance);
-        a.a = k.a;
-        a.b = k.b;
-        a.c = k.noise;
-        a.bad = bad_.as<int>();
-        LC_CUDA(launch_step(a, s_compute_));
-        ++launches;
-        std::swap(x_, xn_);
+        LC_CUDA(cudaStreamEndCapture(s_compute_, &g));
+        LC_CUDA(cudaGraphInstantiate(&graph_exec_, g, 0));
+        LC_CUDA(cudaGraphDestroy(g));
+        graph_stats_ = st;
+        LC_CUDA(cudaGraphLaunch(graph_exec_, s_compute_));
+    } else {
+        enqueue_body(st);
+        ++eager_runs_;
     }
-    LC_CUDA(cudaEventRecord(t_den1, s_compute_));
     ledger_.enter(kDecode);
-    decode_dev(x_.as<float>(), T, video_.as<float>());
-    LC_CUDA(cudaEventRecord(t_end, s_compute_));
     if (video_host)
         LC_CUDA(cudaMemcpyAsync(video_host, video_.p, static_cast<size_t>(video_elems()) * 4,
                                 cudaMemcpyDeviceToHost, s_compute_));
     if (latent_host)
-        LC_CUDA(cudaMemcpyAsync(latent_host, x_.p, static_cast<size_t>(nl) * 4, cudaMemcpyDeviceToHost,
+        LC_CUDA(cudaMemcpyAsync(latent_host, x_final_, static_cast<size_t>(nl) * 4, cudaMemcpyDeviceToHost,
                                 s_compute_));
     int bad = 0;
     LC_CUDA(cudaMemcpyAsync(&bad, bad_.p, 4, cudaMemcpyDeviceToHost, s_compute_));
@@ -1071,16 +1211,20 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
     if (bad) throw_shape("denoiser input contains non-finite values");
 
     float ms = 0;
-    LC_CUDA(cudaEventElapsedTime(&ms, t_den0, t_den1));
+    LC_CUDA(cudaEventElapsedTime(&ms, ev_den0_, ev_den1_));
     st.ms_denoise = ms;
-    LC_CUDA(cudaEventElapsedTime(&ms, t_den1, t_end));
+    LC_CUDA(cudaEventElapsedTime(&ms, ev_den1_, ev_end_));
     st.ms_decode = ms;
-    LC_CUDA(cudaEventElapsedTime(&ms, t_start, t_end));
+    LC_CUDA(cudaEventElapsedTime(&ms, t_start, ev_end_));
     st.ms_total = ms;
+    st.timeline.clear();
+    st.stall_ms = 0;
     double open = 0, lo = 1e30, hi = -1e30;
+    const cudaEvent_t origin = marks_.empty() ? t_start : marks_.front().ev;
     for (const Mark& mk : marks_) {
+        if (mk.kind == 6) continue;
         float t = 0;
-        LC_CUDA(cudaEventElapsedTime(&t, ev_base_, mk.ev));
+        LC_CUDA(cudaEventElapsedTime(&t, origin, mk.ev));
         st.timeline.push_back({static_cast<double>(mk.kind), static_cast<double>(mk.step),
                                static_cast<double>(mk.bytes), static_cast<double>(t)});
         lo = std::min(lo, static_cast<double>(t));
@@ -1114,6 +1258,7 @@ void Engine::forward(const float* x_host, int64_t T, int64_t timestep, const flo
     const int C = static_cast<int>(cfg_.latent_channels);
     const int64_t n1 = T * C * lh * lw;
     // explicit (2,T,...) input: the stem reads both halves as given.
+    invalidate_graph();
     DevBuf xin = dev_alloc(nullptr, 2 * n1 * 4, false);
     LC_CUDA(cudaMemcpy(xin.p, x_host, static_cast<size_t>(2 * n1) * 4, cudaMemcpyHostToDevice));
     const bool full = deep_in_ref == nullptr;
@@ -1154,6 +1299,7 @@ void Engine::decode(const float* lat_host, int64_t n, float* video_host, int64_t
     const int C = static_cast<int>(cfg_.latent_channels);
     const int64_t nl = n * C * cfg_.latent_h() * cfg_.latent_w();
     const int64_t nv = n * cfg_.image_channels * cfg_.height * cfg_.width;
+    invalidate_graph();
     DevBuf lat = dev_alloc(nullptr, nl * 4, false);
     DevBuf vid = dev_alloc(nullptr, nv * 4, false);
     LC_CUDA(cudaMemcpy(lat.p, lat_host, static_cast<size_t>(nl) * 4, cudaMemcpyHostToDevice));
@@ -1186,6 +1332,7 @@ void Engine::decode_sharded(const float* lat_host, int64_t T, int64_t slice, flo
     };
     int64_t f0, cnt;
     shard(rank, &f0, &cnt);
+    invalidate_graph();
     DevBuf lat = dev_alloc(nullptr, std::max<int64_t>(1, cnt) * lat_frame * 4, false);
     DevBuf vid = dev_alloc(nullptr, T * vid_frame * 4, false);
     if (cnt > 0)

@@ -85,7 +85,10 @@ struct TcLayer {
 };
 // c_split: channels of segment 0 (the skip operand for up blocks; c_in for
 // a single-source conv).
-std::unique_ptr<TcLayer> pack_tc_layer(Ledger* l, const Bank& b, int c_split, int mode);
+// m_tiles_hint: M tiles per parity class of the launches this layer will
+// serve (0 = unknown) -- steers the choice of BN (see pack_tc_layer).
+std::unique_ptr<TcLayer> pack_tc_layer(Ledger* l, const Bank& b, int c_split, int mode, int m_tiles_hint = 0);
+int est_m_tiles(int n, int h, int w);
 
 // Thin (CUDA-core) layer: fp32 weights on device.
 struct ThinLayer {
@@ -180,6 +183,7 @@ public:
 
     int64_t decode_slice = 4;  // frames per decode launch group (tool flag)
     int64_t launches = 0;
+    bool use_graphs = true;    // replay the denoise+decode body as a CUDA graph
 
 private:
     struct Level {
@@ -189,6 +193,9 @@ private:
         Act UP;    // materialised upsample (fallback path only)
     };
     void alloc_activations(int64_t T);
+    void enqueue_body(RunStats& st);
+    void prepare_noise();
+    void invalidate_graph();
     // seam: 0 no swap, 1 await the prefetch at the seam, 2 await + evict
     // (last consumer), 3 full step with swap (record the cache-ready event
     // after the U_{m+1} producer).  stacked: x_dev holds the explicit (2,T,...) CFG
@@ -247,6 +254,15 @@ private:
     cudaEvent_t ev_evict_[2] = {nullptr, nullptr}, ev_prefetch_[2] = {nullptr, nullptr},
                 ev_cache_ready_ = nullptr;
     bool evict_pending_ = false, prefetch_pending_ = false, cache_ready_recorded_ = false;
+    bool side_used_ = false;
+    cudaEvent_t ev_start_ = nullptr, ev_den0_ = nullptr, ev_den1_ = nullptr, ev_end_ = nullptr;
+    cudaEvent_t ev_join_[2] = {nullptr, nullptr};
+    float* x_final_ = nullptr;
+    cudaGraphExec_t graph_exec_ = nullptr;
+    RunStats graph_stats_;
+    int eager_runs_ = 0;
+    int64_t graph_slice_ = -1;
+    std::string z_key_;
     std::vector<cudaEvent_t> ev_chunk_[2];
     cudaEvent_t chunk_event(int b, size_t i);
     int prefetch_tag_ = -1;

@@ -150,6 +150,22 @@ def test_budget_error(ctx):
         _run(ctx, dict(TINY, **{"budget.fast_bytes": 80000}))
 
 
+@pytest.mark.parametrize("kind", ["euler", "ancestral"])
+def test_graph_replay_is_bit_identical(ctx, oracle, kind):
+    """Run 1 is eager, run 2 captures the body into a CUDA graph, run 3+
+    replay it: all must give the same bytes (and match the oracle)."""
+    over = dict(TINY, **{"sampler.kind": kind, "sampler.steps": 5})
+    outs = [_run(ctx, over) for _ in range(4)]
+    for v, l, _ in outs[1:]:
+        assert np.array_equal(v, outs[0][0]) and np.array_equal(l, outs[0][1])
+    want_v, want_l = oracle.run_pipeline(_kv(over))
+    assert lc.rel_l2(outs[-1][1], want_l) < TOL
+    # resident path through the same graph
+    ctx.upload_latent(lc.randn(lc.derive_seed(42, 1), ctx.latent_elems()))
+    ctx.run_resident()
+    assert np.array_equal(ctx.download_video().reshape(outs[0][0].shape), outs[0][0])
+
+
 # ---------------------------------------------------------------- B / C
 def _gold(name):
     import os
