@@ -578,6 +578,15 @@ void Engine::configure(const RunConfig& cfg) {
             dec0_tc_ = pack_tc_layer(&ledger_, dp, dec0_kp_, 0);
             const Bank ds = subpixel_shuffle_bank(cw_.dec[static_cast<size_t>(cfg.stages)]);
             dec_last_tc_ = pack_tc_layer(&ledger_, ds, static_cast<int>(ds.c_in), 0);
+            const Bank ep = patch_bank(cw_.enc[0]);
+            enc0_kp_ = static_cast<int>(ep.c_in);
+            enc0_tc_ = pack_tc_layer(&ledger_, ep, enc0_kp_, 0);
+            enc_tc_.clear();
+            for (int64_t i = 1; i <= cfg.stages; ++i)
+                enc_tc_.push_back(pack_tc_layer(&ledger_, cw_.enc[static_cast<size_t>(i)],
+                                                static_cast<int>(cw_.enc[static_cast<size_t>(i)].c_in), 0));
+            enc_alloc_ = -1;
+            img_key_.clear();
         }
         {
             // merged sub-pixel taps of the last decoder conv: wm[p][dy*2+dx][c][4]
@@ -911,11 +920,11 @@ void Engine::issue_prefetch(int issued, int needed) {
     const int64_t bytes = cache_.elems();
     for (int b = 0; b < 2; ++b) {
         if (async) side_used_ = true;
-        record(2, needed, bytes, st);
         size_t ci = 0;
         for (int64_t off = 0; off < bytes; off += kSwapChunk, ++ci) {
             const int64_t len = std::min(kSwapChunk, bytes - off);
             if (async) LC_CUDA(cudaStreamWaitEvent(st, chunk_event(b, ci), 0));
+            if (ci == 0) record(2, needed, bytes, st);  // start = first byte can move
             LC_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(cache_.p) + b * bytes + off,
                                     cache_host_.as<char>() + b * bytes + off, static_cast<size_t>(len),
                                     cudaMemcpyHostToDevice, st));
@@ -1049,6 +1058,107 @@ void Engine::prepare_noise() {
     z_key_ = key;
 }
 
+// Image mode inputs (pipeline.cpp:22-37, :108-114): the deterministic
+// synthetic frames and the forward-noise draw randn(derive_seed(seed, 2)),
+// generated on the host with the reference's double-precision formulas
+// once per config and kept resident in HBM.
+void Engine::prepare_image() {
+    const int64_t T = cfg_.frames, IC = cfg_.image_channels, H = cfg_.height, W = cfg_.width;
+    const std::string key = std::to_string(cfg_.seed) + "/" + std::to_string(T) + "x" + std::to_string(H) + "x" +
+                            std::to_string(W);
+    if (key == img_key_ && frames_dev_.p) return;
+    invalidate_graph();
+    std::vector<float> fr(static_cast<size_t>(T * IC * H * W));
+    for (int64_t t = 0; t < T; ++t)
+        for (int64_t c = 0; c < IC; ++c)
+            for (int64_t y = 0; y < H; ++y)
+                for (int64_t x = 0; x < W; ++x) {
+                    const double phase = 0.25 * static_cast<double>(t) + 0.5 * static_cast<double>(c);
+                    fr[static_cast<size_t>(((t * IC + c) * H + y) * W + x)] = static_cast<float>(
+                        0.5 + 0.5 * std::sin(phase + 6.0 * static_cast<double>(y) / static_cast<double>(H)) *
+                                  std::cos(phase + 6.0 * static_cast<double>(x) / static_cast<double>(W)));
+                }
+    frames_dev_ = dev_alloc(&ledger_, static_cast<int64_t>(fr.size()) * 4, false);
+    LC_CUDA(cudaMemcpy(frames_dev_.p, fr.data(), fr.size() * 4, cudaMemcpyHostToDevice));
+    const int64_t nl = latent_elems();
+    std::vector<float> e(static_cast<size_t>(nl));
+    randn(derive_seed(cfg_.seed, 2), nl, e.data());
+    eps0_dev_ = dev_alloc(&ledger_, nl * 4, false);
+    LC_CUDA(cudaMemcpy(eps0_dev_.p, e.data(), e.size() * 4, cudaMemcpyHostToDevice));
+    img_key_ = key;
+}
+
+// encode (codec.cpp:64-81), frame slices of decode_slice frames:
+// conv_silu(frames, enc0) -> [downsample2 -> conv(_silu)] x S -> latent
+// (fp32 NCHW into lat_dev).
+void Engine::encode_dev(float* lat_dev) {
+    const int S = static_cast<int>(cfg_.stages);
+    const int T = static_cast<int>(cfg_.frames), IC = static_cast<int>(cfg_.image_channels);
+    const int H = static_cast<int>(cfg_.height), W = static_cast<int>(cfg_.width);
+    const int Wc = static_cast<int>(cfg_.codec_width), C = static_cast<int>(cfg_.latent_channels);
+    const int G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(decode_slice, T)));
+    if (enc_alloc_ != G) {
+        invalidate_graph();
+        enc_bufs_.clear();
+        auto make = [&](int h, int w, int c) {
+            Act a;
+            a.n = G;
+            a.h = h;
+            a.w = w;
+            a.c = c;
+            a.cs = round_up(c, 64);
+            enc_bufs_.push_back(dev_alloc(&ledger_, a.elems() * 2, true));
+            a.p = enc_bufs_.back().as<__half>();
+            return a;
+        };
+        enc_patch_ = make(H, W, enc0_kp_);
+        for (int i = 0; i < S; ++i) enc_e_[i] = make(H >> i, W >> i, Wc);
+        for (int i = 1; i <= S; ++i) enc_p_[i] = make(H >> i, W >> i, Wc);
+        enc_alloc_ = G;
+    }
+    const int lh = H >> S, lw = W >> S;
+    for (int g0 = 0; g0 < T; g0 += G) {
+        const int gs = std::min(G, T - g0);
+        Act patch = enc_patch_, e[8], pl[8];
+        patch.n = gs;
+        for (int i = 0; i < S; ++i) (e[i] = enc_e_[i]).n = gs;
+        for (int i = 1; i <= S; ++i) (pl[i] = enc_p_[i]).n = gs;
+        ThinInArgs a{};
+        a.x = frames_dev_.as<float>() + static_cast<int64_t>(g0) * IC * H * W;
+        a.nsrc = gs;
+        a.c_in = IC;
+        a.H = H;
+        a.W = W;
+        a.cfg_pair = 0;
+        a.apply_affine = 0;
+        a.k = 3;
+        a.out = patch.p;
+        a.cs_out = patch.cs;
+        a.win = Window{0, H, 0, W, 0, H, 0, W};
+        LC_CUDA(launch_patch(a, enc0_kp_, s_compute_));
+        run_tc_conv(*enc0_tc_, &patch, e[0], a.win, 1.0f, 0.0f, true, s_compute_);
+        launches += 2;
+        for (int i = 1; i <= S; ++i) {
+            const Act& prev = e[i - 1];
+            LC_CUDA(launch_down2(prev.p, pl[i].p, gs, prev.h, prev.w, prev.cs, s_compute_));
+            const int h = H >> i, w = W >> i;
+            if (i < S) {
+                run_tc_conv(*enc_tc_[i - 1], &pl[i], e[i], Window{0, h, 0, w, 0, h, 0, w}, 1.0f, 0.0f, true,
+                            s_compute_);
+            } else {
+                Act latv;
+                latv.n = gs;
+                latv.h = lh;
+                latv.w = lw;
+                latv.c = C;
+                run_tc_conv(*enc_tc_[i - 1], &pl[i], latv, Window{0, h, 0, w, 0, h, 0, w}, 1.0f, 0.0f, false,
+                            s_compute_, lat_dev + static_cast<int64_t>(g0) * C * lh * lw);
+            }
+            launches += 2;
+        }
+    }
+}
+
 // Denoise loop + decode for the current config, enqueued on the compute
 // stream (and the two copy streams).  Fully asynchronous, so it can be
 // captured into a CUDA graph and replayed (Engine::run).
@@ -1070,6 +1180,19 @@ void Engine::enqueue_body(RunStats& st) {
     ev_end_ = next_event();
     record(6, -1, 0, s_compute_);  // timeline origin inside the body
 
+    if (cfg_.mode == "image") {
+        // Encode stage: latent = encode(frames); x = forward_noise(latent,
+        // S-1, eps0) = sqrt(abar)*latent + sqrt(1-abar)*eps0 (pipeline.cpp:108-114)
+        ledger_.enter(kEncode);
+        encode_dev(xn_.as<float>());
+        const Schedule sc0 = make_schedule(cfg_);
+        const double ab = sc0.abar[static_cast<size_t>(cfg_.steps - 1)];
+        LC_CUDA(launch_linear(static_cast<float>(std::sqrt(ab)), xn_.as<float>(),
+                              static_cast<float>(std::sqrt(1.0 - ab)), eps0_dev_.as<float>(), x_.as<float>(), nl,
+                              s_compute_));
+        ++launches;
+        ledger_.enter(kDenoise);
+    }
     LC_CUDA(cudaMemsetAsync(bad_.p, 0, 16, s_compute_));
     LC_CUDA(launch_isfinite(x_.as<float>(), nl, bad_.as<int>(), s_compute_));
     ++launches;
@@ -1133,7 +1256,6 @@ void Engine::enqueue_body(RunStats& st) {
 }
 
 RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host, bool resident_input) {
-    if (cfg_.mode != "text") throw_config("run.mode=image: the encode stage is not built on the GPU path yet");
     RunStats st;
     stats_ = &st;
     const int64_t T = cfg_.frames;
@@ -1146,11 +1268,15 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
     const int64_t nl = latent_elems();
     const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
     prepare_noise();
+    const bool image = cfg_.mode == "image";
+    if (image) prepare_image();
 
     cudaEvent_t t_start = ev_start_;
     LC_CUDA(cudaEventRecord(t_start, s_compute_));
     ledger_.enter(kEncode);
-    if (!resident_input) {
+    if (image) {
+        // the latent comes from the encode stage inside the body
+    } else if (!resident_input) {
         std::vector<float> gen;
         const float* src = x0_host;
         if (!src) {

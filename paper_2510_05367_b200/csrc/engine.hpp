@@ -222,6 +222,17 @@ private:
     std::unique_ptr<ThinLayer> stem_, head_;
     std::unique_ptr<TcLayer> head_tc_;  // head on the tensor cores (N padded to 16)
     std::unique_ptr<TcLayer> stem_tc_, dec0_tc_, dec_last_tc_;
+    // encoder (image mode, codec.cpp:64-81): patch GEMM + [down2 + conv]xS
+    std::unique_ptr<TcLayer> enc0_tc_;
+    std::vector<std::unique_ptr<TcLayer>> enc_tc_;
+    int enc0_kp_ = 64;
+    DevBuf frames_dev_, eps0_dev_;
+    std::string img_key_;
+    std::vector<DevBuf> enc_bufs_;
+    Act enc_patch_, enc_e_[8], enc_p_[8];
+    int64_t enc_alloc_ = -1;
+    void prepare_image();
+    void encode_dev(float* lat_dev);
     int stem_kp_ = 64, dec0_kp_ = 64;
     Act patch_;                          // stem patch rows (2T, h, w, kp)
     DevBuf patch_buf_, dec_patch_buf_;

@@ -406,6 +406,12 @@ __global__ void step_kernel(const StepArgs a) {
     }
 }
 
+__global__ void linear_kernel(float a, const float* x, float b, const float* y, float* out, int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = __fadd_rn(__fmul_rn(a, x[i]), __fmul_rn(b, y[i]));
+}
+
 __global__ void isfinite_kernel(const float* x, int64_t n, int* bad) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -530,6 +536,12 @@ cudaError_t launch_up2(const __half* in, __half* out, int nimg, int H, int W, in
 
 cudaError_t launch_step(const StepArgs& a, cudaStream_t st) {
     step_kernel<<<grid_for(a.n, 256), 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_linear(float a, const float* x, float b, const float* y, float* out, int64_t n,
+                          cudaStream_t st) {
+    linear_kernel<<<grid_for(n, 256), 256, 0, st>>>(a, x, b, y, out, n);
     return cudaGetLastError();
 }
 

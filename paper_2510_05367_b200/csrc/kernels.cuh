@@ -100,6 +100,11 @@ struct StepArgs {
 };
 cudaError_t launch_step(const StepArgs& a, cudaStream_t st);
 
+// out = a*x + b*y with two roundings (linear, tensor.cpp:269-274); used for
+// forward_noise (sampler.cpp:87-93).
+cudaError_t launch_linear(float a, const float* x, float b, const float* y, float* out, int64_t n,
+                          cudaStream_t st);
+
 // Non-finite scan of a fp32 buffer (all_finite, tensor.cpp:376).
 cudaError_t launch_isfinite(const float* x, int64_t n, int* bad, cudaStream_t st);
 

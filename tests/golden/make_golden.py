@@ -34,6 +34,7 @@ SMALL = {
     "tiny_halo_none": {"run.frames": 2, "run.height": 32, "run.width": 32, "sampler.steps": 6,
                        "chunk.halo": "none", "chunk.targets": "stem,d0,u0,head"},
     "tiny_k5": {"run.frames": 2, "run.height": 32, "run.width": 32, "sampler.steps": 6, "unet.kernel": 5},
+    "tiny_image": {"run.frames": 2, "run.height": 32, "run.width": 32, "sampler.steps": 6, "run.mode": "image"},
     "config_a": {"run.height": 128, "run.width": 128, "cache.n": 3, "chunk.eta": 2, "chunk.omega": 1},
 }
 B0 = {"run.frames": 1, "run.height": 512, "run.width": 512, "codec.stages": 3, "codec.width": 128,

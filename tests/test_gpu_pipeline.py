@@ -50,6 +50,10 @@ def _run(ctx, over, **kw):
     dict(TINY, **{"unet.kernel": 5}),
     dict(TINY, **{"unet.kernel": 1}),
     dict(TINY, **{"cache.enabled": "false", "swap.mode": "off"}),
+    # image mode: encode stage + forward_noise (pipeline.cpp:108-114)
+    dict(TINY, **{"run.mode": "image"}),
+    dict(TINY, **{"run.mode": "image", "sampler.kind": "ancestral", "codec.stages": 3, "run.height": 64,
+                  "run.width": 64}),
 ])
 def test_pipeline_matches_oracle(ctx, oracle, over):
     video, lat, rep = _run(ctx, over)
