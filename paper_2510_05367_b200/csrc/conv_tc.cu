@@ -54,11 +54,26 @@ struct TileCoord {
 template <int CG>
 __device__ __forceinline__ TileCoord tile_coord(const ConvParams& p, int u, int m_units, int n_tiles, int m_tiles,
                                                 int rank) {
+    // Operand-stationary order.  Activation-heavy layers: N tile fastest,
+    // then parity, then M -- concurrently running CTAs share one input
+    // neighbourhood (all N tiles and all four parity classes read the same
+    // pixels), fetched from DRAM once while the small weights stay in L2.
+    // Weight-heavy layers (deep up blocks: up to 170 MB of per-parity
+    // weights): M fastest, so one weight slab is streamed by all CTAs.
     TileCoord c;
-    const int mu = u % m_units;
-    const int rest = u / m_units;
-    c.n_tile = rest % n_tiles;
-    c.parity = rest / n_tiles;
+    const int P = p.nparity;
+    int mu;
+    if (p.m_fastest) {
+        mu = u % m_units;
+        const int rest = u / m_units;
+        c.n_tile = rest % n_tiles;
+        c.parity = rest / n_tiles;
+    } else {
+        c.n_tile = u % n_tiles;
+        const int rest = u / n_tiles;
+        c.parity = rest % P;
+        mu = rest / P;
+    }
     int mt = mu * CG + rank;
     c.live = mt < m_tiles;
     if (!c.live) mt = m_tiles - 1;  // keep coordinates sane; results are discarded

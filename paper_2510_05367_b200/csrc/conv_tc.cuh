@@ -66,6 +66,8 @@ struct alignas(64) ConvParams {
     float shift;                  // o
     int silu;
     int cg;                       // 1: one CTA per M=128 tile; 2: CTA pair, M=256 (cta_group::2)
+    int nparity;                  // parity classes (grid z of the schedule): 1 or 4
+    int m_fastest;                // tile order: 1 weight-stationary (M fastest), 0 activation-stationary
 };
 
 // CTA-group choice for a launch (the weight tensor map's box depends on it:

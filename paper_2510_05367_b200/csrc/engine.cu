@@ -411,6 +411,13 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
         const uint64_t strides[2] = {static_cast<uint64_t>(L.k_total) * 2,
                                      static_cast<uint64_t>(L.n_pad) * L.k_total * 2};
         p.cg = conv_tc_cta_group(L.BN, p.tiles_x * p.tiles_y * p.tiles_i, L.n_pad / L.BN, L.P, L.k_total / 64);
+        p.nparity = L.P;
+        {
+            const double wbytes = 2.0 * L.n_pad * L.k_total * L.P;
+            double abytes = 0;
+            for (int sgi = 0; sgi < L.nseg; ++sgi) abytes += 2.0 * srcs[sgi].elems();
+            p.m_fastest = wbytes > abytes ? 1 : 0;
+        }
         const uint32_t box[3] = {64, static_cast<uint32_t>(L.BN / p.cg), 1};
         const uint32_t estr[3] = {1, 1, 1};
         encode_map(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, L.w.p, dims, strides, box, estr);
@@ -894,7 +901,7 @@ void Engine::issue_evict(int step) {
     if (async) LC_CUDA(cudaStreamWaitEvent(st, ev_cache_ready_, 0));
     const int64_t bytes = cache_.elems();  // one branch: elems()*2 bytes / 2 branches
     for (int b = 0; b < 2; ++b) {
-        if (async) side_used_ = true;
+        if (async) d2h_used_ = true;
         record(2, step, bytes, st);
         size_t ci = 0;
         for (int64_t off = 0; off < bytes; off += kSwapChunk, ++ci) {
@@ -919,7 +926,7 @@ void Engine::issue_prefetch(int issued, int needed) {
     cudaStream_t st = async ? s_h2d_ : s_compute_;
     const int64_t bytes = cache_.elems();
     for (int b = 0; b < 2; ++b) {
-        if (async) side_used_ = true;
+        if (async) h2d_used_ = true;
         size_t ci = 0;
         for (int64_t off = 0; off < bytes; off += kSwapChunk, ++ci) {
             const int64_t len = std::min(kSwapChunk, bytes - off);
@@ -1171,7 +1178,7 @@ void Engine::enqueue_body(RunStats& st) {
     const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
     const bool swap = cfg_.cache_enabled && cfg_.swap_mode != SwapMode::Off;
     evict_pending_ = prefetch_pending_ = false;
-    side_used_ = false;
+    d2h_used_ = h2d_used_ = false;
     marks_.clear();
     ev_next_ = 0;
     launches = 0;
@@ -1244,12 +1251,15 @@ void Engine::enqueue_body(RunStats& st) {
     record_timing(ev_den1_, s_compute_);
     ledger_.enter(kDecode);
     decode_dev(xa, T, video_.as<float>());
-    if (side_used_) {
-        // join the copy streams (required to close a graph capture; the last
-        // eviction stays in flight through decode as in the reference)
+    // join the copy streams that were used (required to close a graph
+    // capture; the last eviction stays in flight through decode as in the
+    // reference, proj/README.md "Swap schedule")
+    if (d2h_used_) {
         LC_CUDA(cudaEventRecord(ev_join_[0], s_d2h_));
-        LC_CUDA(cudaEventRecord(ev_join_[1], s_h2d_));
         LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_join_[0], 0));
+    }
+    if (h2d_used_) {
+        LC_CUDA(cudaEventRecord(ev_join_[1], s_h2d_));
         LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_join_[1], 0));
     }
     record_timing(ev_end_, s_compute_);

@@ -265,7 +265,7 @@ private:
     cudaEvent_t ev_evict_[2] = {nullptr, nullptr}, ev_prefetch_[2] = {nullptr, nullptr},
                 ev_cache_ready_ = nullptr;
     bool evict_pending_ = false, prefetch_pending_ = false, cache_ready_recorded_ = false;
-    bool side_used_ = false;
+    bool d2h_used_ = false, h2d_used_ = false;
     cudaEvent_t ev_start_ = nullptr, ev_den0_ = nullptr, ev_den1_ = nullptr, ev_end_ = nullptr;
     cudaEvent_t ev_join_[2] = {nullptr, nullptr};
     float* x_final_ = nullptr;

@@ -154,11 +154,12 @@ def test_budget_error(ctx):
         _run(ctx, dict(TINY, **{"budget.fast_bytes": 80000}))
 
 
-@pytest.mark.parametrize("kind", ["euler", "ancestral"])
-def test_graph_replay_is_bit_identical(ctx, oracle, kind):
+@pytest.mark.parametrize("kind,extra", [("euler", {}), ("ancestral", {}), ("euler", {"cache.n": 1}),
+                                        ("euler", {"swap.mode": "sync"}), ("ddim", {"cache.n": 4})])
+def test_graph_replay_is_bit_identical(ctx, oracle, kind, extra):
     """Run 1 is eager, run 2 captures the body into a CUDA graph, run 3+
     replay it: all must give the same bytes (and match the oracle)."""
-    over = dict(TINY, **{"sampler.kind": kind, "sampler.steps": 5})
+    over = dict(TINY, **{"sampler.kind": kind, "sampler.steps": 5}, **extra)
     outs = [_run(ctx, over) for _ in range(4)]
     for v, l, _ in outs[1:]:
         assert np.array_equal(v, outs[0][0]) and np.array_equal(l, outs[0][1])
