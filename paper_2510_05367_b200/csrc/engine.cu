@@ -841,16 +841,41 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
             LC_CUDA(cudaEventRecord(ev_cache_ready_, s_compute_));
             cache_ready_recorded_ = true;
         }
-    } else if (seam > 0) {
+    }
+    // Branch-wise seam (async swap with a prefetch in flight): the two CFG
+    // entries are separate transfers (CacheStore entries, cache.cpp:43-90),
+    // so the seam block starts on the uncond half as soon as that entry has
+    // landed and overlaps the cond entry's transfer.  Same bytes, same order
+    // of awaits and issue points as assemble() + evict_all().
+    const bool branch_seam = !full && seam > 0 && prefetch_pending_ && cfg_.swap_mode == SwapMode::Async;
+    if (!full && seam > 0 && !branch_seam) {
         seam_await(step);
         // last consumer: evict_all right after assemble (pipeline.cpp:156-160)
         if (seam == 2) issue_evict(step);
     }
+    auto half = [&](const Act& a, int b) {
+        Act h = a;
+        h.n = a.n / 2;
+        h.p = a.p + static_cast<int64_t>(b) * h.n * a.h * a.w * a.cs;
+        return h;
+    };
     const int top = full ? M - 1 : m;
     for (int i = top; i >= 0; --i) {
         const int j = static_cast<int>(block_index(cfg_, "u" + std::to_string(i)));
         cond(j, &s, &o);
-        up_block(i, lv_[i].D, U_of(i + 1), i == 0 ? lv_[0].U : U_of(i), s, o);
+        const Act& out_i = i == 0 ? lv_[0].U : U_of(i);
+        if (branch_seam && i == m) {
+            for (int b = 0; b < 2; ++b) {
+                record(4, prefetch_tag_, 0, s_compute_);
+                LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_prefetch_[b], 0));
+                record(5, prefetch_tag_, 0, s_compute_);
+                if (b == 1 && seam == 2) issue_evict(step);
+                up_block(i, half(lv_[i].D, b), half(U_of(i + 1), b), half(out_i, b), s, o);
+            }
+            prefetch_pending_ = false;
+        } else {
+            up_block(i, lv_[i].D, U_of(i + 1), out_i, s, o);
+        }
         if (writes_cache && i == m + 1 && seam == 3) {
             LC_CUDA(cudaEventRecord(ev_cache_ready_, s_compute_));
             cache_ready_recorded_ = true;
