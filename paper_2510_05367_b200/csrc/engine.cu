@@ -486,7 +486,7 @@ Engine::Engine(int device) : device_(device) {
 Engine::~Engine() {
     cudaDeviceSynchronize();
     for (auto e : ev_pool_) cudaEventDestroy(e);
-    for (int b = 0; b < 2; ++b)
+    for (int b = 0; b < 3; ++b)
         for (auto e : ev_chunk_[b]) cudaEventDestroy(e);
     cudaEventDestroy(ev_base_);
     for (int b = 0; b < 2; ++b) {
@@ -1056,6 +1056,17 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
         run_tc_conv(*dec_last_tc_, &e[S - 1], vid, Window{0, hl, 0, wl, 0, hl, 0, wl}, 1.0f, 0.0f, false,
                     s_compute_, video_dev + g0 * IC * H * W, IC);
         ++launches;
+        if (video_host_pinned_) {
+            // stream this slice's frames to the caller's pinned buffer while
+            // the next slice decodes (D2H copy stream, event-ordered)
+            cudaEvent_t ev = chunk_event(2, static_cast<size_t>(g0 / G));
+            LC_CUDA(cudaEventRecord(ev, s_compute_));
+            LC_CUDA(cudaStreamWaitEvent(s_d2h_, ev, 0));
+            const int64_t frame = static_cast<int64_t>(IC) * H * W;
+            LC_CUDA(cudaMemcpyAsync(video_host_pinned_ + g0 * frame, video_dev + g0 * frame,
+                                    static_cast<size_t>(gs * frame) * 4, cudaMemcpyDeviceToHost, s_d2h_));
+            d2h_used_ = true;
+        }
     }
 }
 
@@ -1331,7 +1342,17 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
     // second, and replayed from then on: the host no longer paces ~70
     // launches per video (tensor-map encoding, parameter setup).
     const bool can_graph = use_graphs && conv_profiler() == nullptr;
-    if (graph_exec_ && graph_slice_ != decode_slice) invalidate_graph();
+    // Pinned destination: the decoded slices stream out inside the body.
+    float* pinned = nullptr;
+    if (video_host) {
+        cudaPointerAttributes pa{};
+        if (cudaPointerGetAttributes(&pa, video_host) == cudaSuccess && pa.type == cudaMemoryTypeHost)
+            pinned = video_host;
+        cudaGetLastError();  // clear a "not a CUDA pointer" status for pageable memory
+    }
+    if (graph_exec_ && (graph_slice_ != decode_slice || graph_video_ != pinned)) invalidate_graph();
+    graph_video_ = pinned;
+    video_host_pinned_ = pinned;
     graph_slice_ = decode_slice;
     if (can_graph && graph_exec_) {
         LC_CUDA(cudaGraphLaunch(graph_exec_, s_compute_));
@@ -1357,7 +1378,7 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
         ++eager_runs_;
     }
     ledger_.enter(kDecode);
-    if (video_host)
+    if (video_host && !video_host_pinned_)
         LC_CUDA(cudaMemcpyAsync(video_host, video_.p, static_cast<size_t>(video_elems()) * 4,
                                 cudaMemcpyDeviceToHost, s_compute_));
     if (latent_host)
@@ -1369,6 +1390,7 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
     LC_CUDA(cudaStreamSynchronize(s_d2h_));
     LC_CUDA(cudaStreamSynchronize(s_h2d_));
     stats_ = nullptr;
+    video_host_pinned_ = nullptr;  // operator-level decode() must not stream to it
     if (bad) throw_shape("denoiser input contains non-finite values");
 
     float ms = 0;

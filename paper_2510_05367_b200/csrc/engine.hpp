@@ -273,8 +273,10 @@ private:
     RunStats graph_stats_;
     int eager_runs_ = 0;
     int64_t graph_slice_ = -1;
+    float* graph_video_ = nullptr;        // pinned video destination baked into the graph
+    float* video_host_pinned_ = nullptr;  // current run's pinned destination (or null)
     std::string z_key_;
-    std::vector<cudaEvent_t> ev_chunk_[2];
+    std::vector<cudaEvent_t> ev_chunk_[3];  // [0,1] swap chunks per branch, [2] decoded slices
     cudaEvent_t chunk_event(int b, size_t i);
     int prefetch_tag_ = -1;
     RunStats* stats_ = nullptr;

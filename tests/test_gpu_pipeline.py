@@ -169,6 +169,16 @@ def test_graph_replay_is_bit_identical(ctx, oracle, kind, extra):
     ctx.upload_latent(lc.randn(lc.derive_seed(42, 1), ctx.latent_elems()))
     ctx.run_resident()
     assert np.array_equal(ctx.download_video().reshape(outs[0][0].shape), outs[0][0])
+    # pinned host buffers: decoded slices stream out inside the body
+    x0 = lc.PinnedArray(ctx.latent_elems())
+    x0.array[:] = lc.randn(lc.derive_seed(42, 1), ctx.latent_elems())
+    vid = lc.PinnedArray(ctx.video_elems())
+    for _ in range(3):
+        vid.array[:] = -1.0
+        ctx.run_e2e(x0, vid)
+        assert np.array_equal(vid.array.reshape(outs[0][0].shape), outs[0][0])
+    x0.free()
+    vid.free()
 
 
 # ---------------------------------------------------------------- B / C

@@ -5,8 +5,9 @@ rows = list(csv.reader(open(path)))
 hdr_i = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 hdr = rows[hdr_i]; data = rows[hdr_i + 1:]
 ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+mn = hdr.index("Metric Name") if "Metric Name" in hdr else None
 gi = hdr.index("Grid Size") if "Grid Size" in hdr else None
-recs = [(r[ki].split("(")[0].split("::")[-1], float(r[vi].replace(",", "")), r[gi] if gi else "") for r in data if len(r) > vi]
+recs = [(r[ki].split("(")[0].split("::")[-1], float(r[vi].replace(",", "")), r[gi] if gi else "") for r in data if len(r) > vi and (mn is None or r[mn] == "gpu__time_duration.sum")]
 last = recs[len(recs) - len(recs) // steps:]
 agg = collections.defaultdict(lambda: [0, 0.0])
 for k, v, _ in last:
