@@ -44,6 +44,16 @@ __host__ __device__ inline uint32_t tmem_cols_for(int bn) {
     return need <= 32 ? 32u : need <= 64 ? 64u : need <= 128 ? 128u : need <= 256 ? 256u : 512u;
 }
 
+// SiLU x*sigmoid(x) = h*(1+tanh(h)), h = x/2: one MUFU.TANH + 2 FP ops.
+// tanh.approx has ~2^-11 relative error, below the fp16 rounding of the
+// stored activation.
+__device__ __forceinline__ float silu_fast(float x) {
+    const float h = 0.5f * x;
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
+    return fmaf(h, t, h);
+}
+
 struct TileCoord {
     int X0, Y0, I0, parity, n_tile;
     bool live;  // M tile exists (the second tile of a pair may not)
@@ -284,6 +294,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             // this warp owns the 16-column chunks eh, eh+2, eh+4, ...; two
             // TMEM loads in flight per wait
             for (int c00 = 16 * eh; c00 < p.BN; c00 += 64) {
+                // per-channel offsets bias + o * (sum of in-bound tap weights),
+                // loaded before the TMEM wait so the two latencies overlap
+                float offv[32];
+                if (!p.out32) {
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int nb = tc.n_tile * p.BN + c00 + 32 * hh;
+                        if (hh == 1 && c00 + 32 >= p.BN) break;
+#pragma unroll
+                        for (int j = 0; j < 16; j += 4) {
+                            const float4 cb = *reinterpret_cast<const float4*>(corr + nb + j);
+                            const float4 bb = *reinterpret_cast<const float4*>(p.bias + nb + j);
+                            offv[16 * hh + j] = fmaf(p.shift, cb.x, bb.x);
+                            offv[16 * hh + j + 1] = fmaf(p.shift, cb.y, bb.y);
+                            offv[16 * hh + j + 2] = fmaf(p.shift, cb.z, bb.z);
+                            offv[16 * hh + j + 3] = fmaf(p.shift, cb.w, bb.w);
+                        }
+                    }
+                }
                 uint32_t vv[32];
                 tmem_ld16(t_row + c00, *reinterpret_cast<uint32_t(*)[16]>(&vv[0]));
                 const bool two = c00 + 32 < p.BN;
@@ -326,25 +355,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                         }
                     } else if (valid && nb < p.cs_out) {
-                        // per-channel offset: bias + o * (sum of in-bound tap weights)
-                        float off[16];
-#pragma unroll
-                        for (int j = 0; j < 16; j += 4) {
-                            const float4 cb = *reinterpret_cast<const float4*>(corr + nb + j);
-                            const float4 bb = *reinterpret_cast<const float4*>(p.bias + nb + j);
-                            off[j] = fmaf(p.shift, cb.x, bb.x);
-                            off[j + 1] = fmaf(p.shift, cb.y, bb.y);
-                            off[j + 2] = fmaf(p.shift, cb.z, bb.z);
-                            off[j + 3] = fmaf(p.shift, cb.w, bb.w);
-                        }
+                        const float* off = offv + 16 * hh;
                         __align__(16) __half2 h[8];
 #pragma unroll
                         for (int j = 0; j < 16; j += 2) {
                             float a = fmaf(__uint_as_float(v[j]), p.scale, off[j]);
                             float b = fmaf(__uint_as_float(v[j + 1]), p.scale, off[j + 1]);
                             if (p.silu) {
-                                a = __fdividef(a, 1.0f + __expf(-a));
-                                b = __fdividef(b, 1.0f + __expf(-b));
+                                a = silu_fast(a);
+                                b = silu_fast(b);
                             }
                             h[j / 2] = __floats2half2_rn(a, b);
                         }
