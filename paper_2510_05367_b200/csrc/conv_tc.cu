@@ -30,6 +30,7 @@ constexpr int kThreads = 320;      // w0 TMA, w1 MMA+TMEM, w2..w9 epilogue
 constexpr int kEpiWarps = 8;
 constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
 constexpr size_t kSmemBudget = 200 * 1024;   // stage ring budget
+constexpr int kOffFloats = 5120;             // interior-class offset table (20 KB)
 
 template <int CG>
 __host__ __device__ inline int num_stages(int bn) {
@@ -114,6 +115,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull = empty_bar + stages;  // [2] accumulator ready
     uint64_t* tempty = tfull + 2;          // [2] accumulator drained (leader counts both CTAs)
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    // per-channel epilogue offsets of the interior border class, bias + o *
+    // (sum of all tap weights), per parity: read from shared memory instead of
+    // two dependent global loads per 16-channel chunk
+    float* off_tab = reinterpret_cast<float*>(smB + stages * b_bytes + 256);
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -156,6 +161,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                              smem_u32(tmem_holder)),
                          "r"(ncols));
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
+    }
+    const int rc_rr = p.rc + 1;
+    const int n_cls = rc_rr * rc_rr * rc_rr * rc_rr;
+    const int cls_int = (p.rc * rc_rr + p.rc) * (rc_rr * rc_rr) + (p.rc * rc_rr + p.rc);
+    const bool use_tab = p.shuffle_c == 0 && p.nparity * p.n_pad <= kOffFloats;
+    if (use_tab) {
+        for (int i = threadIdx.x; i < p.nparity * p.n_pad; i += kThreads) {
+            const int par = i / p.n_pad, n = i % p.n_pad;
+            off_tab[i] = fmaf(p.shift, p.corr[(static_cast<size_t>(par) * n_cls + cls_int) * p.n_pad + n], p.bias[n]);
         }
     }
     tc_fence_before();
@@ -282,8 +297,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             dl = dl < p.rc ? dl : p.rc;
             dr = dr < p.rc ? dr : p.rc;
             const int cls = (dt * rr + db) * (rr * rr) + (dl * rr + dr);
+            const bool tab = use_tab && (cls == cls_int || !valid);
             const float* corr =
                 p.corr + (static_cast<size_t>(tc.parity) * ncls + (valid ? cls : 0)) * p.n_pad;
+            const float* tab_row = off_tab + tc.parity * p.n_pad;
             const int oy = Y * p.sy + p.py[tc.parity];
             const int ox = X * p.sx + p.px[tc.parity];
             __half* dst = p.out + ((static_cast<size_t>(img) * p.out_h + oy) * p.out_w + ox) * p.cs_out;
@@ -297,7 +314,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // per-channel offsets bias + o * (sum of in-bound tap weights),
                 // loaded before the TMEM wait so the two latencies overlap
                 float offv[32];
-                if (!p.out32) {
+                if (tab) {
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int nb = tc.n_tile * p.BN + c00 + 32 * hh;
+                        if (hh == 1 && c00 + 32 >= p.BN) break;
+#pragma unroll
+                        for (int j = 0; j < 16; j += 4)
+                            *reinterpret_cast<float4*>(&offv[16 * hh + j]) =
+                                *reinterpret_cast<const float4*>(tab_row + nb + j);
+                    }
+                } else if (p.shuffle_c == 0) {
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
                         const int nb = tc.n_tile * p.BN + c00 + 32 * hh;
@@ -348,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (int j = 0; j < 16; ++j) {
                                 if (nb + j < p.c_out) {
-                                    float a = __uint_as_float(v[j]) * p.scale + p.shift * corr[nb + j] + p.bias[nb + j];
+                                    float a = fmaf(__uint_as_float(v[j]), p.scale, offv[16 * hh + j]);
                                     if (p.silu) a = __fdividef(a, 1.0f + __expf(-a));
                                     o32[static_cast<size_t>(nb + j) * plane] = a;
                                 }
@@ -412,7 +439,8 @@ int sm_count() {
 template <int CG>
 size_t smem_bytes_for(int BN) {
     const int st = num_stages<CG>(BN);
-    return 1024 + static_cast<size_t>(st) * (kABytes + static_cast<size_t>(BN / CG) * kBK * 2) + 256;
+    return 1024 + static_cast<size_t>(st) * (kABytes + static_cast<size_t>(BN / CG) * kBK * 2) + 256 +
+           kOffFloats * sizeof(float);
 }
 
 int g_cta_group_override = -1;  // LC_CTA_GROUP env: 1 or 2 forces the variant
@@ -442,10 +470,10 @@ cudaError_t launch_conv_tc(const ConvParams& p, int parities, cudaStream_t strea
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(kSmemBudget + 2048));
+                                             static_cast<int>(kSmemBudget + 2048 + kOffFloats * sizeof(float)));
         if (e != cudaSuccess) return e;
         e = cudaFuncSetAttribute(conv_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(kSmemBudget + 2048));
+                                 static_cast<int>(kSmemBudget + 2048 + kOffFloats * sizeof(float)));
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
