@@ -1,15 +1,24 @@
 // tcgen05 implicit-GEMM convolution kernel.  See conv_tc.cuh for the design.
 //
 // Persistent, warp-specialised: one CTA (or CTA pair) per SM walks the tile
-// list (M tiles fastest so co-resident CTAs share the weight tile in L2).
+// list (operand-stationary order, see tile_coord).
 //   warp 0      TMA producer: A (activation box per tap) + B (weights) into a
 //               smem ring (mbarrier full/empty pairs);
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer, fp32
 //               accumulators in TMEM, two accumulator buffers so the
 //               epilogue of tile i overlaps the main loop of tile i+1;
 //   warps 2..9  epilogue (two warps per TMEM lane quarter, alternating
-//               16-column chunks): tcgen05.ld -> scale/shift/bias/SiLU ->
+//               16-column chunks): tcgen05.ld -> scale/offset/SiLU ->
 //               fp16 NHWC (or fp32 NCHW) stores, then release the accumulator.
+//
+// Epilogue offsets.  The folded conditioning needs, per output channel and
+// per pixel border class, off = bias + o * (sum of in-bound tap weights).  The
+// epilogue warps stage the (parity, N tile) slice of that table for the NEXT
+// tile in shared memory with cp.async while they drain the current one, so the
+// inner loop reads offsets with broadcast ld.shared instead of two dependent
+// global loads per 16-column chunk (the stem GEMM went from 66 to ~46 us on
+// that alone).  The SiLU half-argument (x*sigmoid(x) = h + h*tanh(h), h = x/2)
+// is folded into the staged offsets and the scale.
 //
 // CG = 2 (cta_group::2): a cluster of two CTAs on one TPC computes an M=256
 // tile; each CTA stages its own 128 pixel rows of A and HALF of the N rows of
@@ -20,6 +29,8 @@
 #include "conv_tc.cuh"
 #include "ptx.cuh"
 
+#include <cstdlib>
+
 namespace lc {
 
 namespace {
@@ -28,14 +39,31 @@ constexpr int kBM = 128;           // UMMA M per CTA (pixels per tile, padded)
 constexpr int kBK = 64;            // K elements per stage (one 128 B row per pixel)
 constexpr int kThreads = 320;      // w0 TMA, w1 MMA+TMEM, w2..w9 epilogue
 constexpr int kEpiWarps = 8;
+constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
-constexpr size_t kSmemBudget = 200 * 1024;   // stage ring budget
-constexpr int kOffFloats = 5120;             // interior-class offset table (20 KB)
+constexpr int kSmemMax = 232448;             // 227 KB opt-in dynamic shared memory
+constexpr int kSmemFixed = 1024 + 256;       // alignment slack + barriers
+constexpr int kMaxTabClasses = 16;           // border classes staged in smem (3x3 kernels)
+
+// Epilogue flavours (compile-time, so the inner loop carries no mode tests).
+enum Epi : int {
+    kEpiF16 = 0,      // fp16 NHWC
+    kEpiF16Silu = 1,  // fp16 NHWC, SiLU
+    kEpiF32 = 2,      // fp32 NCHW (denoiser head)
+    kEpiShuffle = 3,  // fp32 NCHW depth-to-space (last decoder conv)
+};
+
+// floats of one staged offset table: ncls class rows + the bias row, BN wide
+__host__ __device__ inline int tab_floats(int rc, int bn) {
+    const int rr = rc + 1;
+    const int ncls = rr * rr * rr * rr;
+    return ncls <= kMaxTabClasses ? (ncls + 1) * bn : 0;
+}
 
 template <int CG>
-__host__ __device__ inline int num_stages(int bn) {
+__host__ __device__ inline int num_stages(int bn, int tabf) {
     const int per = static_cast<int>(kABytes) + (bn / CG) * kBK * 2;
-    int s = static_cast<int>(kSmemBudget / per);
+    int s = (kSmemMax - kSmemFixed - 2 * tabf * 4) / per;
     return s > 8 ? 8 : (s < 2 ? 2 : s);
 }
 
@@ -45,14 +73,18 @@ __host__ __device__ inline uint32_t tmem_cols_for(int bn) {
     return need <= 32 ? 32u : need <= 64 ? 64u : need <= 128 ? 128u : need <= 256 ? 256u : 512u;
 }
 
+__device__ __forceinline__ float tanh_approx(float x) {
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(x));
+    return t;
+}
+
 // SiLU x*sigmoid(x) = h*(1+tanh(h)), h = x/2: one MUFU.TANH + 2 FP ops.
 // tanh.approx has ~2^-11 relative error, below the fp16 rounding of the
 // stored activation.
 __device__ __forceinline__ float silu_fast(float x) {
     const float h = 0.5f * x;
-    float t;
-    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
-    return fmaf(h, t, h);
+    return fmaf(h, tanh_approx(h), h);
 }
 
 struct TileCoord {
@@ -98,14 +130,15 @@ __device__ __forceinline__ TileCoord tile_coord(const ConvParams& p, int u, int 
     return c;
 }
 
-template <int CG>
+template <int CG, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_tc_kernel(const __grid_constant__ ConvParams p, int n_tiles, int parities) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for SW128 atoms.
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    const int stages = num_stages<CG>(p.BN);
+    const int tabf = tab_floats(p.rc, p.BN);
+    const int stages = num_stages<CG>(p.BN, tabf);
     const int bn_cta = p.BN / CG;  // B rows staged by this CTA
     const uint32_t b_bytes = static_cast<uint32_t>(bn_cta) * kBK * 2;
     uint8_t* smA = smem;
@@ -115,10 +148,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull = empty_bar + stages;  // [2] accumulator ready
     uint64_t* tempty = tfull + 2;          // [2] accumulator drained (leader counts both CTAs)
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-    // per-channel epilogue offsets of the interior border class, bias + o *
-    // (sum of all tap weights), per parity: read from shared memory instead of
-    // two dependent global loads per 16-channel chunk
-    float* off_tab = reinterpret_cast<float*>(smB + stages * b_bytes + 256);
+    // two epilogue offset tables [ncls + 1][BN] fp32 (see the header comment)
+    const uint32_t tab_s = smem_u32(smB + stages * b_bytes + 256);
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -161,16 +192,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                              smem_u32(tmem_holder)),
                          "r"(ncols));
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-        }
-    }
-    const int rc_rr = p.rc + 1;
-    const int n_cls = rc_rr * rc_rr * rc_rr * rc_rr;
-    const int cls_int = (p.rc * rc_rr + p.rc) * (rc_rr * rc_rr) + (p.rc * rc_rr + p.rc);
-    const bool use_tab = p.shuffle_c == 0 && p.nparity * p.n_pad <= kOffFloats;
-    if (use_tab) {
-        for (int i = threadIdx.x; i < p.nparity * p.n_pad; i += kThreads) {
-            const int par = i / p.n_pad, n = i % p.n_pad;
-            off_tab[i] = fmaf(p.shift, p.corr[(static_cast<size_t>(par) * n_cls + cls_int) * p.n_pad + n], p.bias[n]);
         }
     }
     tc_fence_before();
@@ -271,8 +292,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ------------------------------------------------ epilogue warps
-        const int q = warp & 3;          // TMEM lane quarter this warp may access
-        const int eh = (warp - 2) >> 2;  // column half: two warps per lane quarter
+        const int et = threadIdx.x - 64;  // 0..255
+        const int q = warp & 3;           // TMEM lane quarter this warp may access
+        const int eh = (warp - 2) >> 2;   // column half: two warps per lane quarter
         const int m = q * 32 + lane;
         const int tile_px = p.TH * p.TW;
         const int li = m / tile_px;
@@ -280,12 +302,66 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int lx = m % p.TW;
         const int rr = p.rc + 1;
         const int ncls = rr * rr * rr * rr;
-        const uint32_t tempty_leader[2] = {CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u,
-                                           CG == 2 ? mapa_shared(smem_u32(&tempty[1]), 0) : 0u};
+        // SiLU runs on h = x/2: fold the 1/2 into scale and offsets
+        constexpr float hs = EPI == kEpiF16Silu ? 0.5f : 1.0f;
+        const float hscale = p.scale * hs;
+        const uint32_t tempty_leader0 = CG == 2 ? mapa_shared(smem_u32(&tempty[0]), 0) : 0u;
+        const uint32_t tempty_leader1 = CG == 2 ? mapa_shared(smem_u32(&tempty[1]), 0) : 0u;
+        const int q4 = p.BN / 4;
+        // stage the raw corr rows + bias row of (parity, n_tile) into table buf
+        auto issue_tab = [&](int buf, int parity, int n_tile) {
+            const uint32_t base = tab_s + static_cast<uint32_t>(buf * tabf) * 4u;
+            const int nq = (ncls + 1) * q4;
+            for (int e = et; e < nq; e += kEpiThreads) {
+                const int row = e / q4, c4 = e - row * q4;
+                const float* src = row < ncls ? p.corr + (static_cast<size_t>(parity) * ncls + row) * p.n_pad
+                                              : p.bias;
+                cp_async16(base + static_cast<uint32_t>(e) * 16u, src + n_tile * p.BN + 4 * c4);
+            }
+            cp_async_commit();
+        };
+        int cur = 0, cur_key = -1;
+        bool pending = false;
+        if (tabf && unit0 < total_units) {
+            const TileCoord t0 = tile_coord<CG>(p, unit0, m_units, n_tiles, m_tiles, static_cast<int>(rank));
+            issue_tab(0, t0.parity, t0.n_tile);
+            cur_key = t0.parity * n_tiles + t0.n_tile;
+            pending = true;
+        }
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int u = unit0; u < total_units; u += unit_step) {
             const TileCoord tc = tile_coord<CG>(p, u, m_units, n_tiles, m_tiles, static_cast<int>(rank));
+            bool next_switch = false;
+            int next_key = cur_key;
+            if (tabf) {
+                if (pending) {
+                    // this tile's slice landed (issued one tile ago): make it
+                    // visible, then turn it into hs * (bias + o * corr)
+                    cp_async_wait_all();
+                    named_bar_sync(1, kEpiThreads);
+                    const uint32_t base = tab_s + static_cast<uint32_t>(cur * tabf) * 4u;
+                    for (int e = et; e < ncls * q4; e += kEpiThreads) {
+                        const int c4 = e % q4;
+                        const float4 c = lds128(base + static_cast<uint32_t>(e) * 16u);
+                        const float4 b = lds128(base + static_cast<uint32_t>(ncls * q4 + c4) * 16u);
+                        sts128(base + static_cast<uint32_t>(e) * 16u,
+                               make_float4(hs * fmaf(p.shift, c.x, b.x), hs * fmaf(p.shift, c.y, b.y),
+                                           hs * fmaf(p.shift, c.z, b.z), hs * fmaf(p.shift, c.w, b.w)));
+                    }
+                    named_bar_sync(1, kEpiThreads);
+                    pending = false;
+                }
+                const int un = u + unit_step;
+                if (un < total_units) {
+                    const TileCoord tn = tile_coord<CG>(p, un, m_units, n_tiles, m_tiles, static_cast<int>(rank));
+                    next_key = tn.parity * n_tiles + tn.n_tile;
+                    if (next_key != cur_key) {
+                        issue_tab(cur ^ 1, tn.parity, tn.n_tile);
+                        next_switch = true;
+                    }
+                }
+            }
             const int img = tc.I0 + li;
             const int Y = tc.Y0 + ly, X = tc.X0 + lx;
             const bool valid = tc.live && (m < p.TI * tile_px) && img < p.n_img && Y < p.ly1[tc.parity] &&
@@ -296,14 +372,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             db = db < p.rc ? db : p.rc;
             dl = dl < p.rc ? dl : p.rc;
             dr = dr < p.rc ? dr : p.rc;
-            const int cls = (dt * rr + db) * (rr * rr) + (dl * rr + dr);
-            const bool tab = use_tab && (cls == cls_int || !valid);
-            const float* corr =
-                p.corr + (static_cast<size_t>(tc.parity) * ncls + (valid ? cls : 0)) * p.n_pad;
-            const float* tab_row = off_tab + tc.parity * p.n_pad;
+            const int cls = valid ? (dt * rr + db) * (rr * rr) + (dl * rr + dr) : 0;
+            const uint32_t off_row = tab_s + static_cast<uint32_t>(cur * tabf + cls * p.BN) * 4u;
+            const float* corr = p.corr + (static_cast<size_t>(tc.parity) * ncls + cls) * p.n_pad;
             const int oy = Y * p.sy + p.py[tc.parity];
             const int ox = X * p.sx + p.px[tc.parity];
-            __half* dst = p.out + ((static_cast<size_t>(img) * p.out_h + oy) * p.out_w + ox) * p.cs_out;
 
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
@@ -311,47 +384,35 @@ __global__ void __launch_bounds__(kThreads, 1)
             // this warp owns the 16-column chunks eh, eh+2, eh+4, ...; two
             // TMEM loads in flight per wait
             for (int c00 = 16 * eh; c00 < p.BN; c00 += 64) {
-                // per-channel offsets bias + o * (sum of in-bound tap weights),
-                // loaded before the TMEM wait so the two latencies overlap
+                const bool two = c00 + 32 < p.BN;
+                uint32_t vv[32];
+                tmem_ld16(t_row + c00, *reinterpret_cast<uint32_t(*)[16]>(&vv[0]));
+                if (two) tmem_ld16(t_row + c00 + 32, *reinterpret_cast<uint32_t(*)[16]>(&vv[16]));
+                // offsets hs * (bias + o * corr[class]) for the two chunks
                 float offv[32];
-                if (tab) {
 #pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
-                        const int nb = tc.n_tile * p.BN + c00 + 32 * hh;
-                        if (hh == 1 && c00 + 32 >= p.BN) break;
+                for (int hh = 0; hh < 2; ++hh) {
+                    if (hh == 1 && !two) break;
+                    const int c0 = c00 + 32 * hh;
+                    if (tabf) {
 #pragma unroll
                         for (int j = 0; j < 16; j += 4)
                             *reinterpret_cast<float4*>(&offv[16 * hh + j]) =
-                                *reinterpret_cast<const float4*>(tab_row + nb + j);
-                    }
-                } else if (p.shuffle_c == 0) {
+                                lds128(off_row + static_cast<uint32_t>(c0 + j) * 4u);
+                    } else {
+                        const int nb = tc.n_tile * p.BN + c0;
 #pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
-                        const int nb = tc.n_tile * p.BN + c00 + 32 * hh;
-                        if (hh == 1 && c00 + 32 >= p.BN) break;
-#pragma unroll
-                        for (int j = 0; j < 16; j += 4) {
-                            const float4 cb = *reinterpret_cast<const float4*>(corr + nb + j);
-                            const float4 bb = *reinterpret_cast<const float4*>(p.bias + nb + j);
-                            offv[16 * hh + j] = fmaf(p.shift, cb.x, bb.x);
-                            offv[16 * hh + j + 1] = fmaf(p.shift, cb.y, bb.y);
-                            offv[16 * hh + j + 2] = fmaf(p.shift, cb.z, bb.z);
-                            offv[16 * hh + j + 3] = fmaf(p.shift, cb.w, bb.w);
-                        }
+                        for (int j = 0; j < 16; ++j) offv[16 * hh + j] = hs * fmaf(p.shift, corr[nb + j], p.bias[nb + j]);
                     }
                 }
-                uint32_t vv[32];
-                tmem_ld16(t_row + c00, *reinterpret_cast<uint32_t(*)[16]>(&vv[0]));
-                const bool two = c00 + 32 < p.BN;
-                if (two) tmem_ld16(t_row + c00 + 32, *reinterpret_cast<uint32_t(*)[16]>(&vv[16]));
                 tmem_ld_wait();
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
                     if (hh == 1 && !two) break;
                     const uint32_t* v = vv + 16 * hh;
-                    const int c0 = c00 + 32 * hh;
-                    const int nb = tc.n_tile * p.BN + c0;
-                    if (p.out32 && p.shuffle_c > 0) {
+                    const float* off = offv + 16 * hh;
+                    const int nb = tc.n_tile * p.BN + c00 + 32 * hh;
+                    if (EPI == kEpiShuffle) {
                         // depth-to-space fp32 NCHW (last decoder conv, sub-pixel form)
                         if (valid) {
                             const size_t plane = static_cast<size_t>(p.out_h) * p.out_w;
@@ -360,13 +421,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 const int ch = nb + j;
                                 if (ch < p.c_out) {
                                     const int par = ch / p.shuffle_c, o = ch % p.shuffle_c;
-                                    const float a = __uint_as_float(v[j]) * p.scale + p.bias[ch];
                                     p.out32[(static_cast<size_t>(img) * p.shuffle_c + o) * plane +
-                                            static_cast<size_t>(2 * Y + par / 2) * p.out_w + 2 * X + par % 2] = a;
+                                            static_cast<size_t>(2 * Y + par / 2) * p.out_w + 2 * X + par % 2] =
+                                        fmaf(__uint_as_float(v[j]), hscale, off[j]);
                                 }
                             }
                         }
-                    } else if (p.out32) {
+                    } else if (EPI == kEpiF32) {
                         // fp32 NCHW output (denoiser head: eps feeds the fp32 sampler)
                         if (valid) {
                             const size_t plane = static_cast<size_t>(p.out_h) * p.out_w;
@@ -375,26 +436,27 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (int j = 0; j < 16; ++j) {
                                 if (nb + j < p.c_out) {
-                                    float a = fmaf(__uint_as_float(v[j]), p.scale, offv[16 * hh + j]);
-                                    if (p.silu) a = __fdividef(a, 1.0f + __expf(-a));
+                                    float a = fmaf(__uint_as_float(v[j]), hscale, off[j]);
+                                    if (p.silu) a = silu_fast(a);
                                     o32[static_cast<size_t>(nb + j) * plane] = a;
                                 }
                             }
                         }
                     } else if (valid && nb < p.cs_out) {
-                        const float* off = offv + 16 * hh;
                         __align__(16) __half2 h[8];
 #pragma unroll
                         for (int j = 0; j < 16; j += 2) {
-                            float a = fmaf(__uint_as_float(v[j]), p.scale, off[j]);
-                            float b = fmaf(__uint_as_float(v[j + 1]), p.scale, off[j + 1]);
-                            if (p.silu) {
-                                a = silu_fast(a);
-                                b = silu_fast(b);
+                            float a = fmaf(__uint_as_float(v[j]), hscale, off[j]);
+                            float b = fmaf(__uint_as_float(v[j + 1]), hscale, off[j + 1]);
+                            if (EPI == kEpiF16Silu) {
+                                a = fmaf(a, tanh_approx(a), a);
+                                b = fmaf(b, tanh_approx(b), b);
                             }
                             h[j / 2] = __floats2half2_rn(a, b);
                         }
-                        uint4* d4 = reinterpret_cast<uint4*>(dst + nb);
+                        __half* dst =
+                            p.out + ((static_cast<size_t>(img) * p.out_h + oy) * p.out_w + ox) * p.cs_out + nb;
+                        uint4* d4 = reinterpret_cast<uint4*>(dst);
                         d4[0] = *reinterpret_cast<uint4*>(&h[0]);
                         d4[1] = *reinterpret_cast<uint4*>(&h[4]);
                     }
@@ -405,11 +467,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) {
                 if (CG == 1) mbar_arrive(&tempty[acc]);
-                else mbar_arrive_cluster(tempty_leader[acc]);
+                else mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
             }
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
+            }
+            if (next_switch) {
+                cur ^= 1;
+                cur_key = next_key;
+                pending = true;
             }
         }
     }
@@ -437,17 +504,64 @@ int sm_count() {
 }
 
 template <int CG>
-size_t smem_bytes_for(int BN) {
-    const int st = num_stages<CG>(BN);
-    return 1024 + static_cast<size_t>(st) * (kABytes + static_cast<size_t>(BN / CG) * kBK * 2) + 256 +
-           kOffFloats * sizeof(float);
+size_t smem_bytes_for(const ConvParams& p) {
+    const int tabf = tab_floats(p.rc, p.BN);
+    const int st = num_stages<CG>(p.BN, tabf);
+    return kSmemFixed + static_cast<size_t>(st) * (kABytes + static_cast<size_t>(p.BN / CG) * kBK * 2) +
+           2 * static_cast<size_t>(tabf) * 4;
 }
 
 int g_cta_group_override = -1;  // LC_CTA_GROUP env: 1 or 2 forces the variant
 
+template <int CG, int EPI>
+cudaError_t launch_variant(const ConvParams& p, int parities, cudaStream_t stream) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e =
+            cudaFuncSetAttribute(conv_tc_kernel<CG, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const int n_tiles = p.n_pad / p.BN;
+    const int m_tiles = p.tiles_x * p.tiles_y * p.tiles_i;
+    if (CG == 1) {
+        const int total = m_tiles * n_tiles * parities;
+        const int grid = total < sm_count() ? total : sm_count();
+        conv_tc_kernel<1, EPI><<<grid, kThreads, smem_bytes_for<1>(p), stream>>>(p, n_tiles, parities);
+        return cudaGetLastError();
+    }
+    const int units = ((m_tiles + 1) / 2) * n_tiles * parities;
+    const int pairs = units < sm_count() / 2 ? units : sm_count() / 2;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem_bytes_for<2>(p);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, conv_tc_kernel<CG, EPI>, p, n_tiles, parities);
+}
+
+template <int CG>
+cudaError_t launch_cg(const ConvParams& p, int parities, cudaStream_t stream) {
+    if (p.out32) {
+        if (p.shuffle_c > 0) return launch_variant<CG, kEpiShuffle>(p, parities, stream);
+        return launch_variant<CG, kEpiF32>(p, parities, stream);
+    }
+    if (p.silu) return launch_variant<CG, kEpiF16Silu>(p, parities, stream);
+    return launch_variant<CG, kEpiF16>(p, parities, stream);
+}
+
 }  // namespace
 
-size_t conv_tc_smem_bytes(int BN) { return smem_bytes_for<1>(BN); }
+size_t conv_tc_smem_bytes(const ConvParams& p) {
+    return p.cg == 2 ? smem_bytes_for<2>(p) : smem_bytes_for<1>(p);
+}
 
 int conv_tc_cta_group(int BN, int m_tiles, int n_tiles, int parities, int k_blocks) {
     static bool read_env = false;
@@ -467,40 +581,7 @@ int conv_tc_cta_group(int BN, int m_tiles, int n_tiles, int parities, int k_bloc
 }
 
 cudaError_t launch_conv_tc(const ConvParams& p, int parities, cudaStream_t stream) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(conv_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(kSmemBudget + 2048 + kOffFloats * sizeof(float)));
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(conv_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(kSmemBudget + 2048 + kOffFloats * sizeof(float)));
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
-    const int n_tiles = p.n_pad / p.BN;
-    const int m_tiles = p.tiles_x * p.tiles_y * p.tiles_i;
-    const int cg = p.cg;
-    if (cg == 1) {
-        const int total = m_tiles * n_tiles * parities;
-        const int grid = total < sm_count() ? total : sm_count();
-        conv_tc_kernel<1><<<grid, kThreads, smem_bytes_for<1>(p.BN), stream>>>(p, n_tiles, parities);
-        return cudaGetLastError();
-    }
-    const int units = ((m_tiles + 1) / 2) * n_tiles * parities;
-    const int pairs = units < sm_count() / 2 ? units : sm_count() / 2;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * pairs);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem_bytes_for<2>(p.BN);
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, conv_tc_kernel<2>, p, n_tiles, parities);
+    return p.cg == 2 ? launch_cg<2>(p, parities, stream) : launch_cg<1>(p, parities, stream);
 }
 
 }  // namespace lc

@@ -82,6 +82,6 @@ struct ConvTcConfig {
 
 // Host launcher (conv_tc.cu).
 cudaError_t launch_conv_tc(const ConvParams& p, int parities, cudaStream_t stream);
-size_t conv_tc_smem_bytes(int BN);
+size_t conv_tc_smem_bytes(const ConvParams& p);
 
 }  // namespace lc
