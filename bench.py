@@ -279,8 +279,9 @@ def gpu_arm(args, world, rank, local):
     ctx.timer_start()
     launches = 0
     for _ in range(args.steps):
-        rep = ctx.run_resident()
-        launches += rep["kernel_launches"]
+        ctx.run_resident_async()  # graph replays queued back to back
+    rep = ctx.wait()
+    launches = rep["kernel_launches"] * args.steps
     ms = ctx.timer_stop()
     ms = allmax(world, ms)
     barrier(world)
@@ -317,11 +318,13 @@ def gpu_arm(args, world, rank, local):
                                              "decode.sliced": "false", "swap.mode": "off"}), base=lc.DEFAULT_CONFIG)
     ctx.configure(base_text)
     ctx.upload_latent(x0.array)
-    ctx.run_resident()
+    for _ in range(max(3, args.warmup)):  # eager, graph capture, replay
+        ctx.run_resident()
     ctx.timer_start()
     nb = max(1, args.steps // 2)
     for _ in range(nb):
-        rep_b = ctx.run_resident()
+        ctx.run_resident_async()
+    rep_b = ctx.wait()
     ms_b = allmax(world, ctx.timer_stop())
     uncached = {"value": world * T * nb / (ms_b / 1000.0), "unit": "frames/s",
                 "hbm_peak_gb": rep_b["hbm_peak_bytes"] / 1e9, "denoiser_macs": rep_b["mac"]["denoiser_total"]}

@@ -62,6 +62,12 @@ int lc_run_pipeline(lc_ctx* ctx, const float* x0, float* video, float* latent_ou
  * (fetch with lc_download_video). */
 int lc_upload_latent(lc_ctx* ctx, const float* x0);
 int lc_run_resident(lc_ctx* ctx, char* report, int64_t report_cap);
+/* Throughput loops: enqueue one resident run without a host round trip
+ * (steady state: a CUDA-graph replay; runs queue back to back), then
+ * lc_wait completes everything queued and reports the last run.  The first
+ * runs after lc_configure execute synchronously (graph capture). */
+int lc_run_resident_async(lc_ctx* ctx);
+int lc_wait(lc_ctx* ctx, char* report, int64_t report_cap);
 int lc_download_video(lc_ctx* ctx, float* video);
 /* Frames decoded per launch group in sliced decode (tool flag, not a config
  * key; the output is identical for every value). */

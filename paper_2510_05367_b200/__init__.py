@@ -92,7 +92,8 @@ I64 = ctypes.c_int64
 EXPORTS = [
     "lc_version", "lc_last_error", "lc_ctx_create", "lc_ctx_destroy", "lc_config_check",
     "lc_config_to_text", "lc_configure", "lc_latent_elems", "lc_video_elems", "lc_run_pipeline",
-    "lc_upload_latent", "lc_run_resident", "lc_download_video", "lc_set_decode_slice",
+    "lc_upload_latent", "lc_run_resident", "lc_run_resident_async", "lc_wait", "lc_download_video",
+    "lc_set_decode_slice",
     "lc_forward", "lc_decode", "lc_conv2d", "lc_up_conv2d", "lc_plan_steps", "lc_split",
     "lc_model_numbers", "lc_derive_seed", "lc_randn", "lc_shard_frames", "lc_nccl_unique_id",
     "lc_nccl_init", "lc_decode_sharded", "lc_timer_start", "lc_timer_stop", "lc_set_conv_profile",
@@ -245,7 +246,7 @@ class Context:
         video = np.empty((1, T, 3, H, W), np.float32) if want_video else None
         lat = np.empty(self.latent_elems(), np.float32) if want_latent else None
         x = None if x0 is None else _f32(x0)
-        rep = ctypes.create_string_buffer(1 << 22)
+        rep = self._report_buf()
         _check(lib().lc_run_pipeline(self._h, _p(x), _p(video), _p(lat), rep, I64(1 << 22)))
         report = json.loads(rep.value.decode())
         if lat is not None:
@@ -256,9 +257,24 @@ class Context:
     def upload_latent(self, x0: np.ndarray):
         _check(lib().lc_upload_latent(self._h, _p(_f32(x0))))
 
+    def _report_buf(self):
+        if getattr(self, "_rep", None) is None:
+            self._rep = ctypes.create_string_buffer(1 << 22)
+        return self._rep
+
     def run_resident(self) -> dict:
-        rep = ctypes.create_string_buffer(1 << 22)
+        rep = self._report_buf()
         _check(lib().lc_run_resident(self._h, rep, I64(1 << 22)))
+        return json.loads(rep.value.decode())
+
+    def run_resident_async(self) -> None:
+        """Queue one resident run (graph replay) without waiting; see wait()."""
+        _check(lib().lc_run_resident_async(self._h))
+
+    def wait(self) -> dict:
+        """Complete the queued resident runs; report of the last one."""
+        rep = self._report_buf()
+        _check(lib().lc_wait(self._h, rep, I64(1 << 22)))
         return json.loads(rep.value.decode())
 
     def download_video(self) -> np.ndarray:
@@ -286,7 +302,7 @@ class Context:
 
     def run_e2e(self, x0_pinned: "PinnedArray", video_pinned: "PinnedArray") -> dict:
         """run_pipeline with pinned host input/output buffers (H2D + D2H inside)."""
-        rep = ctypes.create_string_buffer(1 << 22)
+        rep = self._report_buf()
         _check(lib().lc_run_pipeline(self._h, x0_pinned.ptr, video_pinned.ptr, None, rep, I64(1 << 22)))
         return json.loads(rep.value.decode())
 

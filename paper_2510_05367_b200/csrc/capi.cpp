@@ -165,6 +165,15 @@ int lc_run_resident(lc_ctx* ctx, char* report, int64_t cap) {
         put(report, cap, report_json(ctx->engine, st));
     });
 }
+int lc_run_resident_async(lc_ctx* ctx) {
+    return guarded([&] { ctx->engine.run_resident_async(); });
+}
+int lc_wait(lc_ctx* ctx, char* report, int64_t cap) {
+    return guarded([&] {
+        const lc::RunStats st = ctx->engine.wait();
+        put(report, cap, report_json(ctx->engine, st));
+    });
+}
 int lc_download_video(lc_ctx* ctx, float* video) {
     return guarded([&] {
         LC_CUDA(cudaMemcpy(video, ctx->engine.video_dev(), static_cast<size_t>(ctx->engine.video_elems()) * 4,

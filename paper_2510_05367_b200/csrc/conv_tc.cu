@@ -44,6 +44,8 @@ constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
 constexpr int kSmemMax = 232448;             // 227 KB opt-in dynamic shared memory
 constexpr int kSmemFixed = 1024 + 256;       // alignment slack + barriers
 constexpr int kMaxTabClasses = 16;           // border classes staged in smem (3x3 kernels)
+constexpr int kStageChunk = 2048;                      // one staged box: 32 px x 16 ch (fp32; fp16 uses half)
+constexpr int kStageOutBytes = kEpiWarps * 2 * kStageChunk;  // TMA-store staging: 2 chunks per warp
 
 // Epilogue flavours (compile-time, so the inner loop carries no mode tests).
 enum Epi : int {
@@ -51,6 +53,7 @@ enum Epi : int {
     kEpiF16Silu = 1,  // fp16 NHWC, SiLU
     kEpiF32 = 2,      // fp32 NCHW (denoiser head)
     kEpiShuffle = 3,  // fp32 NCHW depth-to-space (last decoder conv)
+    kEpiF32Raw = 4,   // fp32 NHWC, scale * acc only (tap-to-N GEMMs)
 };
 
 // floats of one staged offset table: ncls class rows + the bias row, BN wide
@@ -60,10 +63,15 @@ __host__ __device__ inline int tab_floats(int rc, int bn) {
     return ncls <= kMaxTabClasses ? (ncls + 1) * bn : 0;
 }
 
+__host__ __device__ inline int epi_smem_bytes(int tabf, int tma_out) {
+    // offset tables, then (1024-aligned) the TMA-store staging buffers
+    return tma_out ? ((2 * tabf * 4 + 1023) & ~1023) + kStageOutBytes : 2 * tabf * 4;
+}
+
 template <int CG>
-__host__ __device__ inline int num_stages(int bn, int tabf) {
+__host__ __device__ inline int num_stages(int bn, int tabf, int tma_out) {
     const int per = static_cast<int>(kABytes) + (bn / CG) * kBK * 2;
-    int s = (kSmemMax - kSmemFixed - 2 * tabf * 4) / per;
+    int s = (kSmemMax - kSmemFixed - epi_smem_bytes(tabf, tma_out)) / per;
     return s > 8 ? 8 : (s < 2 ? 2 : s);
 }
 
@@ -138,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     const int tabf = tab_floats(p.rc, p.BN);
-    const int stages = num_stages<CG>(p.BN, tabf);
+    const int stages = num_stages<CG>(p.BN, tabf, p.tma_out);
     const int bn_cta = p.BN / CG;  // B rows staged by this CTA
     const uint32_t b_bytes = static_cast<uint32_t>(bn_cta) * kBK * 2;
     uint8_t* smA = smem;
@@ -150,6 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
     // two epilogue offset tables [ncls + 1][BN] fp32 (see the header comment)
     const uint32_t tab_s = smem_u32(smB + stages * b_bytes + 256);
+    const uint32_t stage_out_s = tab_s + ((2 * tabf * 4 + 1023) & ~1023);
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -378,6 +387,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int oy = Y * p.sy + p.py[tc.parity];
             const int ox = X * p.sx + p.px[tc.parity];
 
+            // TMA-store box origin of this warp's 32 pixels (lattice coords
+            // relative to the class window, see ConvParams::tmO)
+            constexpr bool kF16 = EPI == kEpiF16 || EPI == kEpiF16Silu;
+            constexpr bool kTma = kF16 || EPI == kEpiF32Raw;  // epilogues with a TMA-store form
+            const int m0 = q * 32;
+            const bool warp_store = kTma && p.tma_out && tc.live && m0 < p.TI * tile_px && !p.debug_nostore;
+            const int bx = tc.X0 + m0 % p.TW - p.lx0[tc.parity];
+            const int by = tc.Y0 + (m0 / p.TW) % p.TH - p.ly0[tc.parity];
+            const int bi = tc.I0 + m0 / tile_px;
+
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t t_row = tmem_base + acc * acc_stride + (static_cast<uint32_t>(q * 32) << 16);
@@ -393,6 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
                     if (hh == 1 && !two) break;
+                    if (EPI == kEpiF32Raw) break;
                     const int c0 = c00 + 32 * hh;
                     if (tabf) {
 #pragma unroll
@@ -406,13 +426,37 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 tmem_ld_wait();
+                if (kTma && p.tma_out) {
+                    // the previous chunk pair's stores have finished reading the staging buffers
+                    if (lane == 0) bulk_wait_read0();
+                    __syncwarp();
+                }
 #pragma unroll
                 for (int hh = 0; hh < 2; ++hh) {
                     if (hh == 1 && !two) break;
                     const uint32_t* v = vv + 16 * hh;
                     const float* off = offv + 16 * hh;
                     const int nb = tc.n_tile * p.BN + c00 + 32 * hh;
-                    if (EPI == kEpiShuffle) {
+                    if (EPI == kEpiF32Raw) {
+                        if (p.tma_out) {
+                            const uint32_t sb =
+                                stage_out_s + static_cast<uint32_t>(((warp - 2) * 2 + hh) * kStageChunk + lane * 64);
+#pragma unroll
+                            for (int j = 0; j < 16; j += 4)
+                                sts128(sb + 4 * j, make_float4(__uint_as_float(v[j]) * hscale,
+                                                               __uint_as_float(v[j + 1]) * hscale,
+                                                               __uint_as_float(v[j + 2]) * hscale,
+                                                               __uint_as_float(v[j + 3]) * hscale));
+                        } else if (valid && nb < p.cs_out) {
+                            float4* o4 = reinterpret_cast<float4*>(
+                                p.out32 + ((static_cast<size_t>(img) * p.out_h + oy) * p.out_w + ox) * p.cs_out + nb);
+#pragma unroll
+                            for (int j = 0; j < 16; j += 4)
+                                o4[j / 4] = make_float4(__uint_as_float(v[j]) * hscale, __uint_as_float(v[j + 1]) * hscale,
+                                                        __uint_as_float(v[j + 2]) * hscale,
+                                                        __uint_as_float(v[j + 3]) * hscale);
+                        }
+                    } else if (EPI == kEpiShuffle) {
                         // depth-to-space fp32 NCHW (last decoder conv, sub-pixel form)
                         if (valid) {
                             const size_t plane = static_cast<size_t>(p.out_h) * p.out_w;
@@ -442,7 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 }
                             }
                         }
-                    } else if (valid && nb < p.cs_out) {
+                    } else if (p.tma_out || (valid && nb < p.cs_out && !p.debug_nostore)) {
                         __align__(16) __half2 h[8];
 #pragma unroll
                         for (int j = 0; j < 16; j += 2) {
@@ -454,11 +498,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                             }
                             h[j / 2] = __floats2half2_rn(a, b);
                         }
-                        __half* dst =
-                            p.out + ((static_cast<size_t>(img) * p.out_h + oy) * p.out_w + ox) * p.cs_out + nb;
-                        uint4* d4 = reinterpret_cast<uint4*>(dst);
-                        d4[0] = *reinterpret_cast<uint4*>(&h[0]);
-                        d4[1] = *reinterpret_cast<uint4*>(&h[4]);
+                        if (p.tma_out) {
+                            const uint32_t sb = stage_out_s + static_cast<uint32_t>(((warp - 2) * 2 + hh) * kStageChunk + lane * 32);
+                            sts128u(sb, *reinterpret_cast<uint4*>(&h[0]));
+                            sts128u(sb + 16, *reinterpret_cast<uint4*>(&h[4]));
+                        } else {
+                            __half* dst =
+                                p.out + ((static_cast<size_t>(img) * p.out_h + oy) * p.out_w + ox) * p.cs_out + nb;
+                            uint4* d4 = reinterpret_cast<uint4*>(dst);
+                            d4[0] = *reinterpret_cast<uint4*>(&h[0]);
+                            d4[1] = *reinterpret_cast<uint4*>(&h[4]);
+                        }
+                    }
+                }
+                if (kTma && p.tma_out) {
+                    // staged 32 px x 16 ch boxes -> global through the TMA unit
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0 && warp_store) {
+                        const int nb0 = tc.n_tile * p.BN + c00;
+                        const uint32_t sb = stage_out_s + static_cast<uint32_t>((warp - 2) * 2 * kStageChunk);
+                        if (nb0 < p.cs_out) tma_store_4d(&p.tmO[tc.parity], sb, nb0, bx, by, bi);
+                        if (two && nb0 + 32 < p.cs_out) tma_store_4d(&p.tmO[tc.parity], sb + kStageChunk, nb0 + 32, bx, by, bi);
+                        bulk_commit();
                     }
                 }
             }
@@ -479,6 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 pending = true;
             }
         }
+        if ((EPI <= kEpiF16Silu || EPI == kEpiF32Raw) && p.tma_out && lane == 0) bulk_wait0();
     }
     tc_fence_before();
     __syncthreads();
@@ -506,9 +569,9 @@ int sm_count() {
 template <int CG>
 size_t smem_bytes_for(const ConvParams& p) {
     const int tabf = tab_floats(p.rc, p.BN);
-    const int st = num_stages<CG>(p.BN, tabf);
+    const int st = num_stages<CG>(p.BN, tabf, p.tma_out);
     return kSmemFixed + static_cast<size_t>(st) * (kABytes + static_cast<size_t>(p.BN / CG) * kBK * 2) +
-           2 * static_cast<size_t>(tabf) * 4;
+           epi_smem_bytes(tabf, p.tma_out);
 }
 
 int g_cta_group_override = -1;  // LC_CTA_GROUP env: 1 or 2 forces the variant
@@ -550,6 +613,7 @@ cudaError_t launch_variant(const ConvParams& p, int parities, cudaStream_t strea
 template <int CG>
 cudaError_t launch_cg(const ConvParams& p, int parities, cudaStream_t stream) {
     if (p.out32) {
+        if (p.nhwc32) return launch_variant<CG, kEpiF32Raw>(p, parities, stream);
         if (p.shuffle_c > 0) return launch_variant<CG, kEpiShuffle>(p, parities, stream);
         return launch_variant<CG, kEpiF32>(p, parities, stream);
     }

@@ -68,6 +68,16 @@ struct alignas(64) ConvParams {
     int cg;                       // 1: one CTA per M=128 tile; 2: CTA pair, M=256 (cta_group::2)
     int nparity;                  // parity classes (grid z of the schedule): 1 or 4
     int m_fastest;                // tile order: 1 weight-stationary (M fastest), 0 activation-stationary
+    int nhwc32;                   // with out32: raw fp32 NHWC (channel stride cs_out), value
+                                  // = scale * acc, no offsets/activation (tap-to-N GEMMs whose
+                                  // taps are summed by a gather kernel)
+    int debug_nostore;            // timing experiment only: skip the output stores
+    // fp16 outputs through TMA tensor stores: per parity class, the output
+    // lattice {C, X, Y, img} of that class (window-clipped, so the TMA unit
+    // drops out-of-window rows); each epilogue warp stages 32 pixels x 16
+    // channels in shared memory and stores them as one box
+    int tma_out;
+    CUtensorMap tmO[4];
 };
 
 // CTA-group choice for a launch (the weight tensor map's box depends on it:

@@ -93,13 +93,31 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 void encode_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* base,
                 const uint64_t* dims, const uint64_t* strides_bytes, const uint32_t* box,
-                const uint32_t* estr) {
+                const uint32_t* estr, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     const CUresult r = encode_fn()(m, dt, static_cast<cuuint32_t>(rank), const_cast<void*>(base), dims,
                                    strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         throw LcError(kCudaError, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
+
+// LC_SPLIT_STORE=0 runs the cache-producing up path on the whole CFG batch (A/B timing)
+bool split_store_enabled() {
+    static const bool on = !(std::getenv("LC_SPLIT_STORE") && std::atoi(std::getenv("LC_SPLIT_STORE")) == 0);
+    return on;
+}
+
+// LC_TAP_GATHER=0 keeps the thin-output convs as direct k x k GEMMs (A/B timing)
+bool tap_gather_enabled() {
+    static const bool on = !(std::getenv("LC_TAP_GATHER") && std::atoi(std::getenv("LC_TAP_GATHER")) == 0);
+    return on;
+}
+
+// LC_TMA_STORE=0 turns the TMA-store epilogue off (A/B timing)
+bool tma_store_enabled() {
+    static const bool on = !(std::getenv("LC_TMA_STORE") && std::atoi(std::getenv("LC_TMA_STORE")) == 0);
+    return on;
 }
 
 // Border-class geometry: lattice window length L and position Y with the
@@ -318,6 +336,51 @@ Bank patch_bank(const Bank& b) {
     return p;
 }
 
+// Tap-to-N bank of a thin-output k x k conv: a 1x1 conv whose output
+// channel t*C + c carries tap t of channel c (no bias; the gather adds it).
+Bank tap_bank(const Bank& b) {
+    Bank t;
+    const int64_t kk = b.k * b.k;
+    t.c_in = b.c_in;
+    t.c_out = kk * b.c_out;
+    t.k = 1;
+    t.taps.assign(static_cast<size_t>(t.c_out * t.c_in), 0.0f);
+    for (int64_t tp = 0; tp < kk; ++tp)
+        for (int64_t c = 0; c < b.c_out; ++c)
+            for (int64_t ic = 0; ic < b.c_in; ++ic)
+                t.taps[static_cast<size_t>((tp * b.c_out + c) * t.c_in + ic)] = b.taps[(c * b.c_in + ic) * kk + tp];
+    t.bias.assign(static_cast<size_t>(t.c_out), 0.0f);
+    return t;
+}
+
+// Sub-pixel tap-to-N bank of nearest-upsample + 3x3 (the last decoder conv):
+// output channel (p*4 + t)*4 + c = merged weights of parity p = (py, px) and
+// low-res tap t = (dy, dx), channels padded to 4 (see launch_subpix_gather).
+Bank subpix_tap_bank(const Bank& b) {
+    if (b.k != 3) throw_invariant("sub-pixel tap bank needs k == 3");
+    Bank t;
+    t.c_in = b.c_in;
+    if (b.c_out > 4) throw_invariant("sub-pixel tap bank needs c_out <= 4");
+    t.c_out = 64;
+    t.k = 1;
+    t.taps.assign(static_cast<size_t>(t.c_out * t.c_in), 0.0f);
+    t.bias.assign(static_cast<size_t>(t.c_out), 0.0f);
+    const int lo[2][2] = {{0, 1}, {0, 2}}, hi[2][2] = {{1, 3}, {2, 3}};  // rows(parity, d)
+    for (int p = 0; p < 4; ++p)
+        for (int tp = 0; tp < 4; ++tp) {
+            const int py = p / 2, px = p % 2, dy = tp / 2, dx = tp % 2;
+            for (int64_t c = 0; c < b.c_out; ++c)
+                for (int64_t ic = 0; ic < b.c_in; ++ic) {
+                    double acc = 0.0;
+                    for (int ky = lo[py][dy]; ky < hi[py][dy]; ++ky)
+                        for (int kx = lo[px][dx]; kx < hi[px][dx]; ++kx)
+                            acc += b.taps[((c * b.c_in + ic) * 3 + ky) * 3 + kx];
+                    t.taps[static_cast<size_t>(((p * 4 + tp) * 4 + c) * t.c_in + ic)] = static_cast<float>(acc);
+                }
+        }
+    return t;
+}
+
 Bank subpixel_shuffle_bank(const Bank& b) {
     if (b.k != 3) throw_invariant("sub-pixel shuffle needs k == 3");
     Bank s;
@@ -349,7 +412,7 @@ Bank subpixel_shuffle_bank(const Bank& b) {
 }
 
 void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window& win, float s,
-                 float o, bool silu, cudaStream_t st, float* out32, int shuffle_c) {
+                 float o, bool silu, cudaStream_t st, float* out32, int shuffle_c, bool nhwc32) {
     ConvParams p;
     std::memset(&p, 0, sizeof(p));
     const int sub = L.mode == 1 ? 2 : 1;
@@ -435,6 +498,40 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
     }
     p.out = out.p;
     p.out32 = out32;
+    p.nhwc32 = out32 && nhwc32 ? 1 : 0;
+    if ((!out32 || p.nhwc32) && tma_store_enabled()) {
+        // TMA-store epilogue: each warp's 32 pixels must form one box in
+        // (x, y, img) of the tile, and every parity class a non-empty window
+        uint32_t bxd = 0, byd = 0, bid = 0;
+        const int tp = p.TH * p.TW;
+        if (p.TW % 32 == 0) {
+            bxd = 32, byd = 1, bid = 1;
+        } else if (32 % p.TW == 0 && tp % 32 == 0) {
+            bxd = p.TW, byd = 32 / p.TW, bid = 1;
+        } else if (32 % p.TW == 0 && 32 % tp == 0 && (p.TI * tp) % 32 == 0) {
+            bxd = p.TW, byd = p.TH, bid = 32 / tp;
+        }
+        bool ok = bxd != 0;
+        for (int q = 0; q < L.P; ++q) ok = ok && p.ly1[q] > p.ly0[q] && p.lx1[q] > p.lx0[q];
+        if (ok) {
+            p.tma_out = 1;
+            for (int q = 0; q < L.P; ++q) {
+                const int py = p.py[q], px = p.px[q];
+                const int esz = p.nhwc32 ? 4 : 2;
+                const char* base = (p.nhwc32 ? reinterpret_cast<const char*>(out32) : reinterpret_cast<const char*>(out.p)) +
+                                   (static_cast<int64_t>(p.ly0[q] * sub + py) * out.w + (p.lx0[q] * sub + px)) * out.cs * esz;
+                const uint64_t dims[4] = {static_cast<uint64_t>(out.cs), static_cast<uint64_t>(p.lx1[q] - p.lx0[q]),
+                                          static_cast<uint64_t>(p.ly1[q] - p.ly0[q]), static_cast<uint64_t>(out.n)};
+                const uint64_t strides[3] = {static_cast<uint64_t>(sub) * out.cs * esz,
+                                             static_cast<uint64_t>(sub) * out.w * out.cs * esz,
+                                             static_cast<uint64_t>(out.h) * out.w * out.cs * esz};
+                const uint32_t box[4] = {16, bxd, byd, bid};
+                const uint32_t estr[4] = {1, 1, 1, 1};
+                encode_map(&p.tmO[q], p.nhwc32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
+                           base, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_NONE);
+            }
+        }
+    }
     p.shuffle_c = shuffle_c;
     p.bias = L.bias.as<float>();
     p.corr = L.corr.as<float>();
@@ -442,6 +539,10 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
     p.scale = s / L.wscale;
     p.shift = o;
     p.silu = silu ? 1 : 0;
+    {
+        static const int nostore = std::getenv("LC_DEBUG_NOSTORE") ? std::atoi(std::getenv("LC_DEBUG_NOSTORE")) : 0;
+        p.debug_nostore = nostore;
+    }
     ConvProfiler* prof = conv_profiler();
     if (prof) {
         // algorithmic work of the reference op (conv2d over the concat,
@@ -477,7 +578,7 @@ Engine::Engine(int device) : device_(device) {
         LC_CUDA(cudaEventCreateWithFlags(&ev_evict_[b], cudaEventDisableTiming));
         LC_CUDA(cudaEventCreateWithFlags(&ev_prefetch_[b], cudaEventDisableTiming));
     }
-    LC_CUDA(cudaEventCreateWithFlags(&ev_cache_ready_, cudaEventDisableTiming));
+    for (int b = 0; b < 2; ++b) LC_CUDA(cudaEventCreateWithFlags(&ev_cache_ready_[b], cudaEventDisableTiming));
     LC_CUDA(cudaEventCreate(&ev_start_));
     for (int b = 0; b < 2; ++b) LC_CUDA(cudaEventCreateWithFlags(&ev_join_[b], cudaEventDisableTiming));
     if (const char* e = std::getenv("LC_NO_GRAPH")) use_graphs = (e[0] == '0');
@@ -493,7 +594,7 @@ Engine::~Engine() {
         cudaEventDestroy(ev_evict_[b]);
         cudaEventDestroy(ev_prefetch_[b]);
     }
-    cudaEventDestroy(ev_cache_ready_);
+    for (int b = 0; b < 2; ++b) cudaEventDestroy(ev_cache_ready_[b]);
     cudaEventDestroy(ev_start_);
     for (int b = 0; b < 2; ++b) cudaEventDestroy(ev_join_[b]);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
@@ -576,6 +677,32 @@ void Engine::configure(const RunConfig& cfg) {
         dec0_ = pack_thin_layer(&ledger_, cw_.dec[0]);
         dec_last_ = pack_thin_layer(&ledger_, cw_.dec[static_cast<size_t>(cfg.stages)]);
         head_tc_ = pack_tc_layer(&ledger_, uw_.banks.back(), static_cast<int>(cfg.base_channels), 0);
+        {
+            const Bank& hb = uw_.banks.back();
+            head_tap_tc_.reset();
+            if (hb.c_out <= 4 && hb.k * hb.k * hb.c_out <= 256) {
+                head_tap_tc_ = pack_tc_layer(&ledger_, tap_bank(hb), static_cast<int>(hb.c_in), 0);
+                const int64_t kk = hb.k * hb.k;
+                std::vector<float> ws(static_cast<size_t>(kk * hb.c_out));
+                for (int64_t tp = 0; tp < kk; ++tp)
+                    for (int64_t c = 0; c < hb.c_out; ++c) {
+                        double acc = 0.0;
+                        for (int64_t ic = 0; ic < hb.c_in; ++ic) acc += hb.taps[(c * hb.c_in + ic) * kk + tp];
+                        ws[static_cast<size_t>(tp * hb.c_out + c)] = static_cast<float>(acc);
+                    }
+                head_wsum_ = dev_alloc(&ledger_, static_cast<int64_t>(ws.size() * 4), false);
+                LC_CUDA(cudaMemcpy(head_wsum_.p, ws.data(), ws.size() * 4, cudaMemcpyHostToDevice));
+                head_bias_ = dev_alloc(&ledger_, static_cast<int64_t>(hb.bias.size() * 4), false);
+                LC_CUDA(cudaMemcpy(head_bias_.p, hb.bias.data(), hb.bias.size() * 4, cudaMemcpyHostToDevice));
+            }
+            const Bank& db = cw_.dec[static_cast<size_t>(cfg.stages)];
+            dec_last_tap_tc_.reset();
+            if (db.k == 3 && db.c_out <= 4) {
+                dec_last_tap_tc_ = pack_tc_layer(&ledger_, subpix_tap_bank(db), static_cast<int>(db.c_in), 0);
+                dec_last_bias_ = dev_alloc(&ledger_, static_cast<int64_t>(db.bias.size() * 4), false);
+                LC_CUDA(cudaMemcpy(dec_last_bias_.p, db.bias.data(), db.bias.size() * 4, cudaMemcpyHostToDevice));
+            }
+        }
         {
             const Bank sp = patch_bank(uw_.banks.front());
             stem_kp_ = static_cast<int>(sp.c_in);
@@ -825,22 +952,31 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
     // l == m+1 and caching is on.
     auto U_of = [&](int l) -> const Act& { return l == M ? mid_ : lv_[l].U; };
     const bool writes_cache = full && cfg_.cache_enabled;
-    if (writes_cache && evict_pending_) {
-        // CacheStore::store awaits pending transfers before replacing
-        // entries (cache.cpp:48-52).
-        for (int b = 0; b < 2; ++b) LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_evict_[b], 0));
-        evict_pending_ = false;
-    }
+    // CacheStore::store awaits pending transfers before replacing entries
+    // (cache.cpp:48-52): the compute stream waits on entry b's eviction right
+    // before the block that overwrites entry b.
+    auto await_store = [&](int b) {
+        if (!(writes_cache && evict_pending_)) return;
+        if (b < 0) {
+            for (int e = 0; e < 2; ++e) LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_evict_[e], 0));
+        } else {
+            LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_evict_[b], 0));
+        }
+        if (b != 0) evict_pending_ = false;
+    };
+    auto cache_ready = [&](int b) {
+        for (int e = 0; e < 2; ++e)
+            if (b < 0 || e == b) LC_CUDA(cudaEventRecord(ev_cache_ready_[e], s_compute_));
+        cache_ready_recorded_ = true;
+    };
     if (full) {
         const Act& prev = lv_[M - 1].D;
         LC_CUDA(launch_down2(prev.p, lv_[M].P.p, prev.n, prev.h, prev.w, prev.cs, s_compute_));
         ++launches;
         cond(1 + M, &s, &o);
+        if (m + 1 == M) await_store(-1);
         conv_block(1 + M, lv_[M].P, mid_, s, o, true);
-        if (writes_cache && m + 1 == M && seam == 3) {
-            LC_CUDA(cudaEventRecord(ev_cache_ready_, s_compute_));
-            cache_ready_recorded_ = true;
-        }
+        if (writes_cache && m + 1 == M && seam == 3) cache_ready(-1);
     }
     // Branch-wise seam (async swap with a prefetch in flight): the two CFG
     // entries are separate transfers (CacheStore entries, cache.cpp:43-90),
@@ -860,7 +996,27 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
         return h;
     };
     const int top = full ? M - 1 : m;
-    for (int i = top; i >= 0; --i) {
+    // Per-branch store (async swap, full step whose U_{m+1} is evicted): the
+    // up path above the seam runs on the uncond half, then on the cond half,
+    // so entry 0's eviction starts about half an up path earlier and entry 1
+    // no longer queues behind it on the host link.  Same blocks, same
+    // per-image arithmetic (bit-identical), same transfer issue points.
+    const bool split_store = writes_cache && seam == 3 && cfg_.swap_mode == SwapMode::Async && m + 1 < M &&
+                             split_store_enabled();
+    int first = top;
+    if (split_store) {
+        for (int b = 0; b < 2; ++b) {
+            for (int i = top; i >= m + 1; --i) {
+                const int j = static_cast<int>(block_index(cfg_, "u" + std::to_string(i)));
+                cond(j, &s, &o);
+                if (i == m + 1) await_store(b);
+                up_block(i, half(lv_[i].D, b), half(U_of(i + 1), b), half(U_of(i), b), s, o);
+            }
+            cache_ready(b);
+        }
+        first = m;
+    }
+    for (int i = first; i >= 0; --i) {
         const int j = static_cast<int>(block_index(cfg_, "u" + std::to_string(i)));
         cond(j, &s, &o);
         const Act& out_i = i == 0 ? lv_[0].U : U_of(i);
@@ -874,12 +1030,10 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
             }
             prefetch_pending_ = false;
         } else {
+            if (i == m + 1) await_store(-1);
             up_block(i, lv_[i].D, U_of(i + 1), out_i, s, o);
         }
-        if (writes_cache && i == m + 1 && seam == 3) {
-            LC_CUDA(cudaEventRecord(ev_cache_ready_, s_compute_));
-            cache_ready_recorded_ = true;
-        }
+        if (writes_cache && i == m + 1 && seam == 3) cache_ready(-1);
     }
     // head: affine + conv, no SiLU -> eps (2,T,C,h,w) fp32
     {
@@ -890,9 +1044,41 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
         eps_view.h = lh;
         eps_view.w = lw;
         eps_view.c = head_tc_->c_out;
-        for (const Window& wd : block_windows(cfg_, "head", lh, lw)) {
-            run_tc_conv(*head_tc_, &lv_[0].U, eps_view, wd, s, o, false, s_compute_, eps2_dev);
-            ++launches;
+        if (head_tap_tc_ && tap_gather_enabled()) {
+            // tap-to-N: one K = c_in GEMM over the materialised window into
+            // y[px][tap*C + c], then the tap gather adds the in-window taps
+            Act yv;
+            yv.n = lv_[0].U.n;
+            yv.h = lh;
+            yv.w = lw;
+            yv.c = head_tap_tc_->c_out;
+            yv.cs = head_tap_tc_->n_pad;
+            ensure_buf(&head_y_buf_, yv.elems() * 4);
+            for (const Window& wd : block_windows(cfg_, "head", lh, lw)) {
+                run_tc_conv(*head_tap_tc_, &lv_[0].U, yv,
+                            Window{wd.vy0, wd.vy1, wd.vx0, wd.vx1, wd.vy0, wd.vy1, wd.vx0, wd.vx1}, s, 0.0f, false,
+                            s_compute_, head_y_buf_.as<float>(), 0, true);
+                TapGatherArgs g{};
+                g.y = head_y_buf_.as<float>();
+                g.cs_y = yv.cs;
+                g.n = yv.n;
+                g.H = lh;
+                g.W = lw;
+                g.C = head_tc_->c_out;
+                g.k = head_tc_->k;
+                g.win = wd;
+                g.wsum = head_wsum_.as<float>();
+                g.bias = head_bias_.as<float>();
+                g.o = o;
+                g.out = eps2_dev;
+                LC_CUDA(launch_tap_gather(g, s_compute_));
+                launches += 2;
+            }
+        } else {
+            for (const Window& wd : block_windows(cfg_, "head", lh, lw)) {
+                run_tc_conv(*head_tc_, &lv_[0].U, eps_view, wd, s, o, false, s_compute_, eps2_dev);
+                ++launches;
+            }
         }
     }
 }
@@ -921,11 +1107,12 @@ void Engine::issue_evict(int step) {
     // The entry is complete once U_{m+1} was produced: on a full step that
     // event was recorded right after the producing block (forward_dev), so
     // the copy overlaps the remaining up path; at a seam it is recorded now.
-    if (!cache_ready_recorded_) LC_CUDA(cudaEventRecord(ev_cache_ready_, s_compute_));
+    if (!cache_ready_recorded_)
+        for (int b = 0; b < 2; ++b) LC_CUDA(cudaEventRecord(ev_cache_ready_[b], s_compute_));
     cache_ready_recorded_ = false;
-    if (async) LC_CUDA(cudaStreamWaitEvent(st, ev_cache_ready_, 0));
     const int64_t bytes = cache_.elems();  // one branch: elems()*2 bytes / 2 branches
     for (int b = 0; b < 2; ++b) {
+        if (async) LC_CUDA(cudaStreamWaitEvent(st, ev_cache_ready_[b], 0));
         if (async) d2h_used_ = true;
         record(2, step, bytes, st);
         size_t ci = 0;
@@ -1053,9 +1240,34 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
         vid.h = H;
         vid.w = W;
         vid.c = IC;
-        run_tc_conv(*dec_last_tc_, &e[S - 1], vid, Window{0, hl, 0, wl, 0, hl, 0, wl}, 1.0f, 0.0f, false,
-                    s_compute_, video_dev + g0 * IC * H * W, IC);
-        ++launches;
+        if (dec_last_tap_tc_ && tap_gather_enabled()) {
+            Act yv;
+            yv.n = gs;
+            yv.h = hl;
+            yv.w = wl;
+            yv.c = dec_last_tap_tc_->c_out;
+            yv.cs = dec_last_tap_tc_->n_pad;
+            Act ymax = yv;
+            ymax.n = G;
+            ensure_buf(&dec_y_buf_, ymax.elems() * 4);
+            run_tc_conv(*dec_last_tap_tc_, &e[S - 1], yv, Window{0, hl, 0, wl, 0, hl, 0, wl}, 1.0f, 0.0f, false,
+                        s_compute_, dec_y_buf_.as<float>(), 0, true);
+            SubpixGatherArgs g{};
+            g.y = dec_y_buf_.as<float>();
+            g.cs_y = yv.cs;
+            g.n = gs;
+            g.H = hl;
+            g.W = wl;
+            g.C = IC;
+            g.bias = dec_last_bias_.as<float>();
+            g.out = video_dev + g0 * IC * H * W;
+            LC_CUDA(launch_subpix_gather(g, s_compute_));
+            launches += 2;
+        } else {
+            run_tc_conv(*dec_last_tc_, &e[S - 1], vid, Window{0, hl, 0, wl, 0, hl, 0, wl}, 1.0f, 0.0f, false,
+                        s_compute_, video_dev + g0 * IC * H * W, IC);
+            ++launches;
+        }
         if (video_host_pinned_) {
             // stream this slice's frames to the caller's pinned buffer while
             // the next slice decodes (D2H copy stream, event-ordered)
@@ -1068,6 +1280,12 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
             d2h_used_ = true;
         }
     }
+}
+
+void Engine::ensure_buf(DevBuf* b, int64_t bytes) {
+    if (b->p && b->bytes >= bytes) return;
+    invalidate_graph();
+    *b = dev_alloc(&ledger_, bytes, false);
 }
 
 void Engine::invalidate_graph() {
@@ -1317,6 +1535,7 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
     const bool image = cfg_.mode == "image";
     if (image) prepare_image();
 
+    if (async_pending_) (void)wait();
     cudaEvent_t t_start = ev_start_;
     LC_CUDA(cudaEventRecord(t_start, s_compute_));
     ledger_.enter(kEncode);
@@ -1378,6 +1597,45 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
         ++eager_runs_;
     }
     ledger_.enter(kDecode);
+    return finish_run(st, video_host, latent_host);
+}
+
+// Steady-state resident replay without the host round trip: enqueue the
+// input copy and the graph, return.  Consecutive calls queue back to back on
+// the compute stream (the body joins its copy streams at the end, so runs
+// never overlap); wait() completes the last one.  Before the graph exists
+// (first two runs after a (re)configuration) this is a synchronous run().
+void Engine::run_resident_async() {
+    const bool ready = use_graphs && conv_profiler() == nullptr && graph_exec_ && graph_video_ == nullptr &&
+                       graph_slice_ == decode_slice && T_alloc_ == cfg_.frames;
+    if (!ready) {
+        last_async_ = run(nullptr, nullptr, nullptr, true);
+        async_pending_ = false;
+        return;
+    }
+    LC_CUDA(cudaEventRecord(ev_start_, s_compute_));
+    LC_CUDA(cudaMemcpyAsync(x_.p, x0_.p, static_cast<size_t>(latent_elems()) * 4, cudaMemcpyDeviceToDevice,
+                            s_compute_));
+    LC_CUDA(cudaGraphLaunch(graph_exec_, s_compute_));
+    async_pending_ = true;
+}
+
+RunStats Engine::wait() {
+    if (!async_pending_) return last_async_;
+    async_pending_ = false;
+    video_host_pinned_ = nullptr;
+    RunStats st = graph_stats_;
+    stats_ = &st;
+    ledger_.enter(kDecode);
+    last_async_ = finish_run(st, nullptr, nullptr);
+    return last_async_;
+}
+
+RunStats Engine::finish_run(RunStats st, float* video_host, float* latent_host) {
+    const cudaEvent_t t_start = ev_start_;
+    const int64_t T = cfg_.frames;
+    const int64_t nl = latent_elems();
+    const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
     if (video_host && !video_host_pinned_)
         LC_CUDA(cudaMemcpyAsync(video_host, video_.p, static_cast<size_t>(video_elems()) * 4,
                                 cudaMemcpyDeviceToHost, s_compute_));

@@ -118,8 +118,11 @@ void set_conv_profiler(ConvProfiler* p);
 // output region in output-pixel coordinates.
 // out32 non-null: write fp32 NCHW (out.n, c_out, out.h, out.w) instead of
 // fp16 NHWC into out.p.
+// nhwc32 (with out32): raw fp32 NHWC s*conv(x) into out32 with the channel
+// stride out.cs (tap-to-N GEMMs, no offsets / activation).
 void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window& win, float s,
-                 float o, bool silu, cudaStream_t st, float* out32 = nullptr, int shuffle_c = 0);
+                 float o, bool silu, cudaStream_t st, float* out32 = nullptr, int shuffle_c = 0,
+                 bool nhwc32 = false);
 
 // Bank of a thin-input conv re-expressed as a 1x1 conv over gathered
 // patches (see launch_patch): c_in' = roundup64(c_in*k*k).
@@ -157,6 +160,10 @@ public:
     // pipeline.cpp:115).  video_host may be nullptr (video stays on device
     // in video_dev()).  latent_host receives the final latent if non-null.
     RunStats run(const float* x0_host, float* video_host, float* latent_host, bool resident_input);
+    // Throughput loops: enqueue one resident run (graph replay) without
+    // waiting; wait() completes the queued runs and reports the last one.
+    void run_resident_async();
+    RunStats wait();
 
     // Operator-level entry points (for unit parity).
     // forward_full / forward_cached on x (2,T,C,h,w) host fp32.
@@ -196,6 +203,10 @@ private:
     void enqueue_body(RunStats& st);
     void prepare_noise();
     void invalidate_graph();
+    RunStats finish_run(RunStats st, float* video_host, float* latent_host);
+    bool async_pending_ = false;
+    RunStats last_async_;
+    void ensure_buf(DevBuf* b, int64_t bytes);  // grow-only scratch (invalidates the graph when it grows)
     // seam: 0 no swap, 1 await the prefetch at the seam, 2 await + evict
     // (last consumer), 3 full step with swap (record the cache-ready event
     // after the U_{m+1} producer).  stacked: x_dev holds the explicit (2,T,...) CFG
@@ -222,6 +233,10 @@ private:
     std::unique_ptr<ThinLayer> stem_, head_;
     std::unique_ptr<TcLayer> head_tc_;  // head on the tensor cores (N padded to 16)
     std::unique_ptr<TcLayer> stem_tc_, dec0_tc_, dec_last_tc_;
+    // tap-to-N forms of the thin-output convs: 1x1 GEMM over (tap, channel)
+    // columns + a gather kernel (launch_tap_gather / launch_subpix_gather)
+    std::unique_ptr<TcLayer> head_tap_tc_, dec_last_tap_tc_;
+    DevBuf head_wsum_, head_bias_, dec_last_bias_, head_y_buf_, dec_y_buf_;
     // encoder (image mode, codec.cpp:64-81): patch GEMM + [down2 + conv]xS
     std::unique_ptr<TcLayer> enc0_tc_;
     std::vector<std::unique_ptr<TcLayer>> enc_tc_;
@@ -263,7 +278,7 @@ private:
     };
     std::vector<Mark> marks_;
     cudaEvent_t ev_evict_[2] = {nullptr, nullptr}, ev_prefetch_[2] = {nullptr, nullptr},
-                ev_cache_ready_ = nullptr;
+                ev_cache_ready_[2] = {nullptr, nullptr};  // per CFG entry: U_{m+1} half complete
     bool evict_pending_ = false, prefetch_pending_ = false, cache_ready_recorded_ = false;
     bool d2h_used_ = false, h2d_used_ = false;
     cudaEvent_t ev_start_ = nullptr, ev_den0_ = nullptr, ev_den1_ = nullptr, ev_end_ = nullptr;

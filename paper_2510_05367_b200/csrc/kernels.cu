@@ -182,6 +182,110 @@ __global__ void patch_kernel(const ThinInArgs a, int kp) {
     }
 }
 
+// Fast path of the patch gather: 3x3 taps, kp == 64 (c_in <= 7).  Block =
+// 32 pixels of one output row x 8 tap groups, so a warp writes 4 pixels x
+// 128 B contiguous and all index math is 32-bit with constant divisors.
+__global__ void __launch_bounds__(256) patch3_kernel(const ThinInArgs a) {
+    constexpr int K = 3, KK = 9;
+    const int g = threadIdx.x & 7;
+    const int oh = a.win.oy1 - a.win.oy0;
+    const int ox = a.win.ox0 + static_cast<int>(blockIdx.x) * 32 + (threadIdx.x >> 3);
+    const int row = static_cast<int>(blockIdx.y);
+    const int n = row / oh;
+    const int oy = a.win.oy0 + (row - n * oh);
+    if (ox >= a.win.ox1) return;
+    const int src = n % a.nsrc;
+    const bool branch1 = a.cfg_pair && n >= a.nsrc;
+    const float* xs = a.x + static_cast<size_t>(src) * a.c_in * a.H * a.W;
+    const int KKc = a.c_in * KK;
+    __align__(16) __half h[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int t = g * 8 + j;
+        float v = 0.0f;
+        if (t < KKc) {
+            const int ic = t / KK, rem = t - ic * KK;
+            const int ky = rem / K, kx = rem - ky * K;
+            const int iy = oy + ky - 1, ix = ox + kx - 1;
+            if (iy >= a.win.vy0 && iy < a.win.vy1 && ix >= a.win.vx0 && ix < a.win.vx1) {
+                v = __ldg(xs + (static_cast<size_t>(ic) * a.H + iy) * a.W + ix);
+                if (branch1) v = __fadd_rn(v, a.cond_bias);
+                if (a.apply_affine) v = __fadd_rn(__fmul_rn(v, a.s), a.o);
+            }
+        }
+        h[j] = __float2half_rn(v);
+    }
+    *reinterpret_cast<uint4*>(a.out + ((static_cast<size_t>(n) * a.H + oy) * a.W + ox) * 64 + g * 8) =
+        *reinterpret_cast<const uint4*>(h);
+}
+
+// ------------------------------------------------------- tap gathers
+// One thread per output pixel; consecutive threads walk x, so each tap read
+// is a 16 B (C = 4) load at a 16*k*k-float stride, served from L2 (y was
+// just written by the GEMM).
+__global__ void __launch_bounds__(256) tap_gather_kernel(const TapGatherArgs a) {
+    const int ow = a.win.ox1 - a.win.ox0, oh = a.win.oy1 - a.win.oy0;
+    const int idx = static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= a.n * oh * ow) return;
+    const int row = idx / ow;
+    const int x = a.win.ox0 + (idx - row * ow);
+    const int n = row / oh;
+    const int yy = a.win.oy0 + (row - n * oh);
+    const int r = a.k / 2;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f}, ws[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int dy = -r; dy <= r; ++dy) {
+        const int sy = yy + dy;
+        if (sy < a.win.vy0 || sy >= a.win.vy1) continue;
+        for (int dx = -r; dx <= r; ++dx) {
+            const int sx = x + dx;
+            if (sx < a.win.vx0 || sx >= a.win.vx1) continue;
+            const int t = (dy + r) * a.k + (dx + r);
+            const float* yp = a.y + ((static_cast<size_t>(n) * a.H + sy) * a.W + sx) * a.cs_y + t * a.C;
+            if (a.C == 4) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(yp));
+                acc[0] += v.x, acc[1] += v.y, acc[2] += v.z, acc[3] += v.w;
+            } else {
+                for (int c = 0; c < a.C; ++c) acc[c] += __ldg(yp + c);
+            }
+            for (int c = 0; c < a.C; ++c) ws[c] += __ldg(a.wsum + t * a.C + c);
+        }
+    }
+    const size_t plane = static_cast<size_t>(a.H) * a.W;
+    for (int c = 0; c < a.C; ++c)
+        a.out[(static_cast<size_t>(n) * a.C + c) * plane + static_cast<size_t>(yy) * a.W + x] =
+            acc[c] + fmaf(a.o, ws[c], __ldg(a.bias + c));
+}
+
+// One thread per low-res pixel: its 2x2 output pixels x C channels; each
+// (parity, tap) group is one 16 B load (channels padded to 4 in y).
+__global__ void __launch_bounds__(128) subpix_gather_kernel(const SubpixGatherArgs a) {
+    const int X = static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int row = static_cast<int>(blockIdx.y);
+    const int n = row / a.H, Y = row - n * a.H;
+    if (X >= a.W) return;
+    const int W2 = 2 * a.W;
+    const size_t plane = static_cast<size_t>(4) * a.H * a.W;
+    float bias[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) bias[c] = c < a.C ? __ldg(a.bias + c) : 0.f;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const int py = p >> 1, px = p & 1;
+        float4 acc = make_float4(bias[0], bias[1], bias[2], bias[3]);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int sy = Y + (t >> 1) - 1 + py, sx = X + (t & 1) - 1 + px;
+            if (sy < 0 || sy >= a.H || sx < 0 || sx >= a.W) continue;
+            const float4 v = __ldg(reinterpret_cast<const float4*>(
+                a.y + ((static_cast<size_t>(n) * a.H + sy) * a.W + sx) * a.cs_y + (p * 4 + t) * 4));
+            acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+        }
+        const float av[4] = {acc.x, acc.y, acc.z, acc.w};
+        for (int c = 0; c < a.C; ++c)
+            a.out[(static_cast<size_t>(n) * a.C + c) * plane + static_cast<size_t>(2 * Y + py) * W2 + 2 * X + px] = av[c];
+    }
+}
+
 // ------------------------------------------- upsample + thin-output conv
 // Last decoder conv fused with its nearest upsample (codec.cpp:103-113):
 // one thread per LOW-RES pixel produces the 2x2 output pixels it covers.
@@ -444,7 +548,31 @@ cudaError_t launch_patch(const ThinInArgs& a, int kp, cudaStream_t st) {
     const int nimg = a.cfg_pair ? 2 * a.nsrc : a.nsrc;
     const int64_t work =
         static_cast<int64_t>(nimg) * (a.win.oy1 - a.win.oy0) * (a.win.ox1 - a.win.ox0) * (kp / 8);
+    const int rows = nimg * (a.win.oy1 - a.win.oy0);
+    if (a.k == 3 && kp == 64 && a.c_in * 9 <= 64 && rows < 65536) {
+        const dim3 grid((a.win.ox1 - a.win.ox0 + 31) / 32, rows);
+        if (grid.x > 0 && rows > 0) patch3_kernel<<<grid, 256, 0, st>>>(a);
+        return cudaGetLastError();
+    }
     patch_kernel<<<grid_for(work, 256), 256, 0, st>>>(a, kp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tap_gather(const TapGatherArgs& a, cudaStream_t st) {
+    const int ow = a.win.ox1 - a.win.ox0, rows = a.n * (a.win.oy1 - a.win.oy0);
+    if (ow <= 0 || rows <= 0) return cudaSuccess;
+    if (a.C > 4) return cudaErrorInvalidValue;
+    const int64_t total = static_cast<int64_t>(rows) * ow;
+    if (total >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
+    tap_gather_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_subpix_gather(const SubpixGatherArgs& a, cudaStream_t st) {
+    const int rows = a.n * a.H;
+    if (a.W <= 0 || rows <= 0) return cudaSuccess;
+    if (a.C > 4 || rows >= 65536) return cudaErrorInvalidValue;
+    subpix_gather_kernel<<<dim3((a.W + 127) / 128, rows), 128, 0, st>>>(a);
     return cudaGetLastError();
 }
 

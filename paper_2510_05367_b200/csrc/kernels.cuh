@@ -48,6 +48,39 @@ cudaError_t launch_thin_in(const ThinInArgs& a, cudaStream_t st);
 // patch tensor (nimg, H, W, kp); weights/bias/silu fields are ignored.
 cudaError_t launch_patch(const ThinInArgs& a, int kp, cudaStream_t st);
 
+// Tap gather of a tap-to-N conv.  A thin-output k x k conv (c_out = C <= 4:
+// the denoiser head) runs on the tensor cores as a 1x1 GEMM whose N axis is
+// (tap, channel): y[px][t*C + c] = s * sum_ic w[c][ic][t] x[px][ic] (fp32
+// NHWC).  This kernel sums the in-window taps of each output pixel and adds
+// the folded conditioning o * sum_{in-window t} wsum[t][c] + bias[c]
+// (unet.cpp:78-97 run_conv_block: affine -> zero-padded conv), writing fp32
+// NCHW.
+struct TapGatherArgs {
+    const float* y;
+    int cs_y;
+    int n, H, W, C, k;
+    Window win;         // v*: materialised (zero-padding) window, o*: output window
+    const float* wsum;  // [k*k][C]
+    const float* bias;  // [C]
+    float o;
+    float* out;         // (n, C, H, W)
+};
+cudaError_t launch_tap_gather(const TapGatherArgs& a, cudaStream_t st);
+
+// Sub-pixel tap gather of the last decoder conv (nearest 2x upsample + 3x3,
+// codec.cpp:103-113): y[low-res px][(p*4 + t)*4 + c] (channels padded to 4) holds, per output parity
+// p = (py, px) and merged 2x2 tap t = (dy, dx), the GEMM partial sums; the
+// output pixel (2Y+py, 2X+px) is bias + the sum of its four in-range low-res
+// neighbours (Y+dy-1+py, X+dx-1+px).  fp32 NCHW video (n, C, 2H, 2W).
+struct SubpixGatherArgs {
+    const float* y;
+    int cs_y;
+    int n, H, W, C;     // low-res extents
+    const float* bias;  // [C]
+    float* out;
+};
+cudaError_t launch_subpix_gather(const SubpixGatherArgs& a, cudaStream_t st);
+
 // Thin-output conv (c_out <= 8): fp16 NHWC input -> fp32 NCHW output.
 //  * denoiser head: affine (s,o) then conv, no SiLU;
 //  * last decoder conv with the nearest upsample fused (up2=1: the input is

@@ -169,6 +169,12 @@ def test_graph_replay_is_bit_identical(ctx, oracle, kind, extra):
     ctx.upload_latent(lc.randn(lc.derive_seed(42, 1), ctx.latent_elems()))
     ctx.run_resident()
     assert np.array_equal(ctx.download_video().reshape(outs[0][0].shape), outs[0][0])
+    # queued replays (throughput loop): same bytes, report of the last run
+    for _ in range(3):
+        ctx.run_resident_async()
+    rep_a = ctx.wait()
+    assert np.array_equal(ctx.download_video().reshape(outs[0][0].shape), outs[0][0])
+    assert rep_a["kernel_launches"] == outs[-1][2]["kernel_launches"]
     # pinned host buffers: decoded slices stream out inside the body
     x0 = lc.PinnedArray(ctx.latent_elems())
     x0.array[:] = lc.randn(lc.derive_seed(42, 1), ctx.latent_elems())
