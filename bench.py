@@ -349,7 +349,8 @@ def gpu_arm(args, world, rank, local):
             "uncached": uncached,
             "speedup_vs_uncached": value / uncached["value"],
             "denoise_ms": rep["device_ms"]["denoise"], "decode_ms": rep["device_ms"]["decode"],
-            "swap": {"bytes_per_step": rep["swap"]["bytes"], "stall_ms": rep["timeline"]["stall_ms"]},
+            "swap": {"bytes_per_step": rep["swap"]["bytes"], "bytes_moved_per_step": rep["swap"]["bytes_moved"],
+                     "stall_ms": rep["timeline"]["stall_ms"]},
             "e2e": {"value": e2e, "unit": "frames/s", "h2d_bytes_per_step": n_lat * 4,
                     "d2h_bytes_per_step": n_vid * 4},
             "roofline": {"bound": "tensor", "kernel": "conv_tc_kernel (tcgen05 implicit-GEMM conv)",

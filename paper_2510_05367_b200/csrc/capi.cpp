@@ -63,7 +63,8 @@ std::string report_json(const lc::Engine& e, const lc::RunStats& st) {
        << ",\"cached_steps\":" << st.cached_steps << "},";
     os << "\"cache_bytes\":" << st.cache_bytes_planned << ",\"cache_bytes_physical\":"
        << st.cache_bytes_physical << ",";
-    os << "\"swap\":{\"bytes\":" << st.swap_bytes << ",\"calls\":" << st.swap_calls << "},";
+    os << "\"swap\":{\"bytes\":" << st.swap_bytes << ",\"bytes_moved\":" << st.swap_bytes_moved
+       << ",\"calls\":" << st.swap_calls << "},";
     os << "\"timeline\":{\"makespan_ms\":" << st.makespan_ms << ",\"stall_ms\":" << st.stall_ms
        << ",\"events\":[";
     for (size_t i = 0; i < st.timeline.size(); ++i) {

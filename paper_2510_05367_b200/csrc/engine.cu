@@ -102,6 +102,12 @@ void encode_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* ba
         throw LcError(kCudaError, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
 }
 
+// LC_CLEAN_EVICT=0 moves every eviction's bytes, clean or not (A/B timing)
+bool clean_evict_enabled() {
+    static const bool on = !(std::getenv("LC_CLEAN_EVICT") && std::atoi(std::getenv("LC_CLEAN_EVICT")) == 0);
+    return on;
+}
+
 // LC_SPLIT_STORE=0 runs the cache-producing up path on the whole CFG batch (A/B timing)
 bool split_store_enabled() {
     static const bool on = !(std::getenv("LC_SPLIT_STORE") && std::atoi(std::getenv("LC_SPLIT_STORE")) == 0);
@@ -952,6 +958,7 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
     // l == m+1 and caching is on.
     auto U_of = [&](int l) -> const Act& { return l == M ? mid_ : lv_[l].U; };
     const bool writes_cache = full && cfg_.cache_enabled;
+    if (writes_cache) host_valid_ = false;  // this step stores new entries
     // CacheStore::store awaits pending transfers before replacing entries
     // (cache.cpp:48-52): the compute stream waits on entry b's eviction right
     // before the block that overwrites entry b.
@@ -1111,9 +1118,30 @@ void Engine::issue_evict(int step) {
         for (int b = 0; b < 2; ++b) LC_CUDA(cudaEventRecord(ev_cache_ready_[b], s_compute_));
     cache_ready_recorded_ = false;
     const int64_t bytes = cache_.elems();  // one branch: elems()*2 bytes / 2 branches
+    // Clean eviction: when the pinned host copy already holds these exact
+    // bytes (evicted after the store, prefetched back, only read since),
+    // evict_all moves nothing -- the entries leave the fast tier and the
+    // slow-tier copy stays valid, like a clean page.  Logical transfer,
+    // timeline marks and issue order are the reference's.
+    const bool clean = host_valid_ && clean_evict_enabled();
+    if (clean) {
+        for (int b = 0; b < 2; ++b) {
+            if (async) LC_CUDA(cudaStreamWaitEvent(st, ev_cache_ready_[b], 0));  // issue point, as a dirty one
+            if (async) d2h_used_ = true;
+            record(2, step, bytes, st);
+            record(3, step, bytes, st);
+            LC_CUDA(cudaEventRecord(ev_evict_[b], st));
+            if (stats_) stats_->swap_bytes += bytes;
+        }
+        if (stats_) stats_->swap_calls += 1;
+        evict_pending_ = true;
+        return;
+    }
+    host_valid_ = true;
     for (int b = 0; b < 2; ++b) {
         if (async) LC_CUDA(cudaStreamWaitEvent(st, ev_cache_ready_[b], 0));
         if (async) d2h_used_ = true;
+        if (stats_) stats_->swap_bytes_moved += bytes;
         record(2, step, bytes, st);
         size_t ci = 0;
         for (int64_t off = 0; off < bytes; off += kSwapChunk, ++ci) {
@@ -1151,6 +1179,7 @@ void Engine::issue_prefetch(int issued, int needed) {
         record(3, needed, bytes, st);
         LC_CUDA(cudaEventRecord(ev_prefetch_[b], st));
         if (stats_) stats_->swap_bytes += bytes;
+        if (stats_) stats_->swap_bytes_moved += bytes;
     }
     if (stats_) stats_->swap_calls += 1;
     prefetch_pending_ = true;
@@ -1433,6 +1462,7 @@ void Engine::enqueue_body(RunStats& st) {
     const bool swap = cfg_.cache_enabled && cfg_.swap_mode != SwapMode::Off;
     evict_pending_ = prefetch_pending_ = false;
     d2h_used_ = h2d_used_ = false;
+    host_valid_ = false;
     marks_.clear();
     ev_next_ = 0;
     launches = 0;

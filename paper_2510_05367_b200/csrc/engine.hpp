@@ -138,7 +138,8 @@ struct RunStats {
     double stall_ms = 0, makespan_ms = 0;
     int64_t full_steps = 0, cached_steps = 0;
     int64_t macs_full = 0, macs_cached = 0, denoiser_macs = 0;
-    int64_t swap_bytes = 0, swap_calls = 0;
+    int64_t swap_bytes = 0, swap_calls = 0;  // logical (reference) transfer bytes and calls
+    int64_t swap_bytes_moved = 0;             // bytes that crossed the host link (clean evictions elided)
     int64_t cache_bytes_planned = 0, cache_bytes_physical = 0;
     int64_t peak[4][2] = {};
     int64_t hbm_peak = 0;
@@ -205,6 +206,7 @@ private:
     void invalidate_graph();
     RunStats finish_run(RunStats st, float* video_host, float* latent_host);
     bool async_pending_ = false;
+    bool host_valid_ = false;  // the pinned host copy equals the device cache (clean entries)
     RunStats last_async_;
     void ensure_buf(DevBuf* b, int64_t bytes);  // grow-only scratch (invalidates the graph when it grows)
     // seam: 0 no swap, 1 await the prefetch at the seam, 2 await + evict

@@ -140,6 +140,19 @@ def test_swap_issue_order(ctx):
     assert seq == want, " ".join(seq)
 
 
+def test_swap_bytes_logical_and_moved(ctx):
+    """Logical swap traffic is the reference's (one
+    evict_all/prefetch_all call moves both entries; calls = 2 x full steps
+    with consumers + last consumers + a final consumer-less full step).  Only
+    dirty evictions and prefetches cross the host link: the eviction after a
+    last consumer finds the host copy already valid."""
+    _, _, rep = _run(ctx, dict(TINY, **{"sampler.steps": 7, "cache.n": 3, "swap.mode": "async"}))
+    pair = rep["cache_bytes_physical"]  # both entries of one call
+    assert rep["swap"]["calls"] == 7  # plan F c c F c c F
+    assert rep["swap"]["bytes"] == 7 * pair
+    assert rep["swap"]["bytes_moved"] == 5 * pair  # 3 dirty evictions + 2 prefetches
+
+
 def test_nonfinite_input_raises_shape_error(ctx):
     over = dict(TINY)
     ctx.configure(lc.config_text(over, base=DEFAULT))
