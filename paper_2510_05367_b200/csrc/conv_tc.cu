@@ -68,10 +68,13 @@ __host__ __device__ inline int epi_smem_bytes(int tabf, int tma_out) {
     return tma_out ? ((2 * tabf * 4 + 1023) & ~1023) + kStageOutBytes : 2 * tabf * 4;
 }
 
+// ring stages: A + B per stage, or A only with a resident weight panel of
+// total_kb K blocks (b_res)
 template <int CG>
-__host__ __device__ inline int num_stages(int bn, int tabf, int tma_out) {
-    const int per = static_cast<int>(kABytes) + (bn / CG) * kBK * 2;
-    int s = (kSmemMax - kSmemFixed - epi_smem_bytes(tabf, tma_out)) / per;
+__host__ __device__ inline int num_stages(int bn, int tabf, int tma_out, int b_res, int total_kb) {
+    const int bblk = (bn / CG) * kBK * 2;
+    const int per = static_cast<int>(kABytes) + (b_res ? 0 : bblk);
+    int s = (kSmemMax - kSmemFixed - epi_smem_bytes(tabf, tma_out) - (b_res ? total_kb * bblk : 0)) / per;
     return s > 8 ? 8 : (s < 2 ? 2 : s);
 }
 
@@ -145,19 +148,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     // 1024-byte alignment for SW128 atoms.
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    int total_kb = 0;
+    for (int s = 0; s < p.nseg; ++s) total_kb += p.seg[s].ntaps * p.seg[s].ncb;
+    const bool b_res = CG == 1 && p.b_res;
     const int tabf = tab_floats(p.rc, p.BN);
-    const int stages = num_stages<CG>(p.BN, tabf, p.tma_out);
+    const int stages = num_stages<CG>(p.BN, tabf, p.tma_out, b_res, total_kb);
     const int bn_cta = p.BN / CG;  // B rows staged by this CTA
     const uint32_t b_bytes = static_cast<uint32_t>(bn_cta) * kBK * 2;
     uint8_t* smA = smem;
     uint8_t* smB = smem + stages * kABytes;
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smB + stages * b_bytes);
+    const int b_blocks = b_res ? total_kb : stages;  // resident panel or ring
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smB + b_blocks * b_bytes);
     uint64_t* empty_bar = full_bar + stages;
     uint64_t* tfull = empty_bar + stages;  // [2] accumulator ready
     uint64_t* tempty = tfull + 2;          // [2] accumulator drained (leader counts both CTAs)
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* bfull = tempty + 2;          // resident weight panel landed (b_res)
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bfull + 1);
     // two epilogue offset tables [ncls + 1][BN] fp32 (see the header comment)
-    const uint32_t tab_s = smem_u32(smB + stages * b_bytes + 256);
+    const uint32_t tab_s = smem_u32(smB + b_blocks * b_bytes + 256);
     const uint32_t stage_out_s = tab_s + ((2 * tabf * 4 + 1023) & ~1023);
 
     const int warp = threadIdx.x / 32;
@@ -166,12 +174,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool leader = rank == 0;
     const int m_tiles = p.tiles_x * p.tiles_y * p.tiles_i;
     const int m_units = (m_tiles + CG - 1) / CG;
-    const int total_units = m_units * n_tiles * parities;
-    const int unit0 = static_cast<int>(blockIdx.x) / CG;
-    const int unit_step = static_cast<int>(gridDim.x) / CG;
-
-    int total_kb = 0;
-    for (int s = 0; s < p.nseg; ++s) total_kb += p.seg[s].ntaps * p.seg[s].ncb;
+    int total_units = m_units * n_tiles * parities;
+    int unit0 = static_cast<int>(blockIdx.x) / CG;
+    int unit_step = static_cast<int>(gridDim.x) / CG;
+    int slab_par = 0, slab_nt = 0;
+    if (b_res) {
+        // CTA group per (parity, N tile) slab; units are that slab's M tiles
+        const int slabs = parities * n_tiles;
+        const int cps = static_cast<int>(gridDim.x) / slabs;
+        const int slab = static_cast<int>(blockIdx.x) / cps;
+        slab_par = slab / n_tiles;
+        slab_nt = slab % n_tiles;
+        total_units = m_tiles;
+        unit0 = static_cast<int>(blockIdx.x) % cps;
+        unit_step = cps;
+    }
+    auto coord = [&](int u) {
+        if (!b_res) return tile_coord<CG>(p, u, m_units, n_tiles, m_tiles, static_cast<int>(rank));
+        TileCoord c;
+        c.parity = slab_par;
+        c.n_tile = slab_nt;
+        c.live = true;
+        const int tx = u % p.tiles_x, rest = u / p.tiles_x;
+        const int ty = rest % p.tiles_y, ti = rest / p.tiles_y;
+        c.X0 = p.lx0[c.parity] + tx * p.TW;
+        c.Y0 = p.ly0[c.parity] + ty * p.TH;
+        c.I0 = ti * p.TI;
+        return c;
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
@@ -182,6 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], kEpiWarps * CG);  // one arrive per epilogue warp of the pair
         }
+        mbar_init(bfull, 1);
         fence_barrier_init();
     }
     if (warp == 0 && lane == 0) {
@@ -214,11 +245,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------ TMA producer
         if (elect_one()) {
             const uint32_t a_bytes = static_cast<uint32_t>(p.TI * p.TH * p.TW) * kBK * 2;
-            const uint32_t tx_bytes = CG * (a_bytes + b_bytes);  // both CTAs complete on the leader
+            const uint32_t tx_bytes = b_res ? a_bytes : CG * (a_bytes + b_bytes);  // both CTAs complete on the leader
+            if (b_res && unit0 < total_units) {
+                // the slab's whole weight panel, once
+                mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(total_kb) * b_bytes);
+                int s = 0, tap = 0, cb = 0, kcoord = p.seg[0].kbase;
+                for (int kb = 0; kb < total_kb; ++kb) {
+                    tma_load_3d(smB + kb * b_bytes, &p.tmB, bfull, kcoord, slab_nt * p.BN, slab_par);
+                    kcoord += kBK;
+                    if (++cb == p.seg[s].ncb) {
+                        cb = 0;
+                        if (++tap == p.seg[s].ntaps) {
+                            tap = 0;
+                            ++s;
+                            if (s < p.nseg) kcoord = p.seg[s].kbase;
+                        }
+                    }
+                }
+            }
             int stage = 0;
             uint32_t phase = 0;
             for (int u = unit0; u < total_units; u += unit_step) {
-                const TileCoord tc = tile_coord<CG>(p, u, m_units, n_tiles, m_tiles, static_cast<int>(rank));
+                const TileCoord tc = coord(u);
                 int s = 0, tap = 0, cb = 0;
                 int kcoord = p.seg[0].kbase;
                 const int nrow = tc.n_tile * p.BN + static_cast<int>(rank) * bn_cta;
@@ -230,7 +278,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (CG == 1) {
                         mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
                         tma_load_4d(smA + stage * kABytes, &p.tmA[s], &full_bar[stage], cb * kBK, cx, cy, tc.I0);
-                        tma_load_3d(smB + stage * b_bytes, &p.tmB, &full_bar[stage], kcoord, nrow, tc.parity);
+                        if (!b_res)
+                            tma_load_3d(smB + stage * b_bytes, &p.tmB, &full_bar[stage], kcoord, nrow, tc.parity);
                     } else {
                         if (leader) mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
                         const uint32_t bar = mapa_shared(smem_u32(&full_bar[stage]), 0);
@@ -261,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
+            if (b_res && unit0 < total_units) mbar_wait(bfull, 0);
             for (int u = unit0; u < total_units; u += unit_step) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
@@ -270,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_after();
                     if (elect_one()) {
                         const uint64_t adesc = umma_desc_sw128(smem_u32(smA + stage * kABytes));
-                        const uint64_t bdesc = umma_desc_sw128(smem_u32(smB + stage * b_bytes));
+                        const uint64_t bdesc = umma_desc_sw128(smem_u32(smB + (b_res ? kb : stage) * b_bytes));
 #pragma unroll
                         for (int k = 0; k < kBK / 16; ++k) {
                             // +32 bytes per K=16 step inside the 128 B swizzle row
@@ -332,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int cur = 0, cur_key = -1;
         bool pending = false;
         if (tabf && unit0 < total_units) {
-            const TileCoord t0 = tile_coord<CG>(p, unit0, m_units, n_tiles, m_tiles, static_cast<int>(rank));
+            const TileCoord t0 = coord(unit0);
             issue_tab(0, t0.parity, t0.n_tile);
             cur_key = t0.parity * n_tiles + t0.n_tile;
             pending = true;
@@ -340,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int u = unit0; u < total_units; u += unit_step) {
-            const TileCoord tc = tile_coord<CG>(p, u, m_units, n_tiles, m_tiles, static_cast<int>(rank));
+            const TileCoord tc = coord(u);
             bool next_switch = false;
             int next_key = cur_key;
             if (tabf) {
@@ -363,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 const int un = u + unit_step;
                 if (un < total_units) {
-                    const TileCoord tn = tile_coord<CG>(p, un, m_units, n_tiles, m_tiles, static_cast<int>(rank));
+                    const TileCoord tn = coord(un);
                     next_key = tn.parity * n_tiles + tn.n_tile;
                     if (next_key != cur_key) {
                         issue_tab(cur ^ 1, tn.parity, tn.n_tile);
@@ -569,8 +619,12 @@ int sm_count() {
 template <int CG>
 size_t smem_bytes_for(const ConvParams& p) {
     const int tabf = tab_floats(p.rc, p.BN);
-    const int st = num_stages<CG>(p.BN, tabf, p.tma_out);
-    return kSmemFixed + static_cast<size_t>(st) * (kABytes + static_cast<size_t>(p.BN / CG) * kBK * 2) +
+    int total_kb = 0;
+    for (int s = 0; s < p.nseg; ++s) total_kb += p.seg[s].ntaps * p.seg[s].ncb;
+    const int b_res = CG == 1 && p.b_res;
+    const int st = num_stages<CG>(p.BN, tabf, p.tma_out, b_res, total_kb);
+    const size_t bblk = static_cast<size_t>(p.BN / CG) * kBK * 2;
+    return kSmemFixed + static_cast<size_t>(st) * (kABytes + (b_res ? 0 : bblk)) + (b_res ? total_kb * bblk : 0) +
            epi_smem_bytes(tabf, p.tma_out);
 }
 
@@ -589,7 +643,8 @@ cudaError_t launch_variant(const ConvParams& p, int parities, cudaStream_t strea
     const int m_tiles = p.tiles_x * p.tiles_y * p.tiles_i;
     if (CG == 1) {
         const int total = m_tiles * n_tiles * parities;
-        const int grid = total < sm_count() ? total : sm_count();
+        int grid = total < sm_count() ? total : sm_count();
+        if (p.b_res) grid = (sm_count() / (n_tiles * parities)) * n_tiles * parities;
         conv_tc_kernel<1, EPI><<<grid, kThreads, smem_bytes_for<1>(p), stream>>>(p, n_tiles, parities);
         return cudaGetLastError();
     }
@@ -644,8 +699,32 @@ int conv_tc_cta_group(int BN, int m_tiles, int n_tiles, int parities, int k_bloc
     return cg;
 }
 
+// Weight-stationary schedule when it pays: one CTA group per (parity, N
+// tile) slab, several M tiles per CTA, and the slab's weight panel plus >= 3
+// activation stages fit in shared memory.  LC_BRES=0 disables it.
+static bool want_b_res(const ConvParams& p, int parities) {
+    static const int env = std::getenv("LC_BRES") ? std::atoi(std::getenv("LC_BRES")) : 1;
+    if (!env || p.cg != 1) return false;
+    const int n_tiles = p.n_pad / p.BN, slabs = n_tiles * parities;
+    const int m_tiles = p.tiles_x * p.tiles_y * p.tiles_i;
+    if (slabs > sm_count()) return false;
+    const int cps = sm_count() / slabs;
+    if (m_tiles < 2 * cps) return false;
+    int total_kb = 0;
+    for (int s = 0; s < p.nseg; ++s) total_kb += p.seg[s].ntaps * p.seg[s].ncb;
+    return num_stages<1>(p.BN, tab_floats(p.rc, p.BN), p.tma_out, 1, total_kb) >= 3 &&
+           (kSmemMax - kSmemFixed - epi_smem_bytes(tab_floats(p.rc, p.BN), p.tma_out) -
+            total_kb * p.BN * kBK * 2) >= 3 * static_cast<int>(kABytes);
+}
+
 cudaError_t launch_conv_tc(const ConvParams& p, int parities, cudaStream_t stream) {
-    return p.cg == 2 ? launch_cg<2>(p, parities, stream) : launch_cg<1>(p, parities, stream);
+    if (p.cg == 2) return launch_cg<2>(p, parities, stream);
+    if (want_b_res(p, parities)) {
+        ConvParams q = p;
+        q.b_res = 1;
+        return launch_cg<1>(q, parities, stream);
+    }
+    return launch_cg<1>(p, parities, stream);
 }
 
 }  // namespace lc

@@ -78,6 +78,12 @@ struct alignas(64) ConvParams {
     // channels in shared memory and stores them as one box
     int tma_out;
     CUtensorMap tmO[4];
+    // weight-stationary schedule (CG = 1): the CTAs are split into one group
+    // per (parity, N tile) slab; each CTA loads its slab's whole K x BN
+    // weight panel into shared memory once and streams only activation
+    // tiles (small-K, small-N layers whose per-tile weight re-reads would
+    // otherwise make them L2-bandwidth bound)
+    int b_res;
 };
 
 // CTA-group choice for a launch (the weight tensor map's box depends on it:

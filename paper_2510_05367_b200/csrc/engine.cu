@@ -215,21 +215,38 @@ std::unique_ptr<TcLayer> pack_tc_layer(Ledger* l, const Bank& b, int c_split, in
         L->k_total += L->seg_ntaps[s] * L->seg_cpad[s];
     }
     // N tiling: fewest N tiles of <= 256 columns (largest BN: least A
-    // re-reading, best MMA/smem ratio).  Only when that leaves the machine
-    // under-filled (fewer tiles than SMs, e.g. the mid block at 8x8) the
-    // largest BN that yields >= ~80% of the SMs is used instead.
+    // re-reading, best MMA/smem ratio) by default.  With the run geometry
+    // known (m_tiles_hint), BN minimises a wave-quantisation cost model of
+    // the persistent schedule: waves = ceil(units / slots) (148 CTAs, or 74
+    // CTA pairs of M = 256 when conv_tc_cta_group would pick pairs), each
+    // wave costing BN + 32 (per-tile fixed overhead ~ 32 columns; pairs 5%
+    // cheaper: half the weight staging per CTA; single CTAs on long K loops
+    // 35% dearer: measured, they are shared-memory-bandwidth bound).
+    // E.g. d2/u2 at 16x16 (1280 out): BN 256 -> 160 units = 3 waves of
+    // pairs, BN 160 -> 256 units = 4 shorter waves (-11%).
     int nt = 1;
     while (round_up((L->c_out + nt - 1) / nt, 16) > 256) ++nt;
     L->BN = round_up((L->c_out + nt - 1) / nt, 16);
-    if (m_tiles_hint > 0 && L->c_out > 64 &&
-        static_cast<int64_t>(m_tiles_hint) * nt * L->P < 148) {
-        for (int bn = L->BN; bn >= 64; bn -= 16) {
+    if (m_tiles_hint > 0 && L->c_out > 64) {
+        const int kb = L->k_total / 64;
+        double best = 1e30;
+        int best_bn = L->BN;
+        for (int bn = 256; bn >= 48; bn -= 16) {
             const int n_t = (L->c_out + bn - 1) / bn;
-            if (static_cast<int64_t>(m_tiles_hint) * n_t * L->P >= 120) {
-                L->BN = bn;
-                break;
+            if (n_t * bn - L->c_out >= bn) continue;  // an empty N tile
+            if (static_cast<double>(n_t) * bn > 1.125 * round_up(L->c_out, 16)) continue;  // > 12.5% padding
+            const int64_t tiles = static_cast<int64_t>(m_tiles_hint) * n_t * L->P;
+            const bool pair = bn % 32 == 0 && m_tiles_hint >= 2 && kb >= 32 && tiles >= 2 * 148;
+            const int64_t units = pair ? static_cast<int64_t>((m_tiles_hint + 1) / 2) * n_t * L->P : tiles;
+            const int slots = pair ? 74 : 148;
+            const double cost = static_cast<double>((units + slots - 1) / slots) *
+                                (pair ? 0.95 : (kb >= 32 ? 1.35 : 1.0)) * (bn + 32);
+            if (cost < best - 1e-9) {
+                best = cost;
+                best_bn = bn;
             }
         }
+        L->BN = best_bn;
         nt = (L->c_out + L->BN - 1) / L->BN;
     }
     L->n_pad = nt * L->BN;
@@ -1004,21 +1021,26 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
     };
     const int top = full ? M - 1 : m;
     // Per-branch store (async swap, full step whose U_{m+1} is evicted): the
-    // up path above the seam runs on the uncond half, then on the cond half,
-    // so entry 0's eviction starts about half an up path earlier and entry 1
-    // no longer queues behind it on the host link.  Same blocks, same
-    // per-image arithmetic (bit-identical), same transfer issue points.
+    // producing block u_{m+1} runs on the uncond half, then on the cond half,
+    // so entry 0's eviction starts half a block earlier and overlaps the
+    // cond half.  Same per-image arithmetic (bit-identical), same transfer
+    // issue points.
     const bool split_store = writes_cache && seam == 3 && cfg_.swap_mode == SwapMode::Async && m + 1 < M &&
                              split_store_enabled();
+    // Deeper up blocks stay whole-batch (their weight panels, up to 170 MB,
+    // would be streamed twice); only the producing block u_{m+1} is split.
     int first = top;
     if (split_store) {
+        for (int i = top; i > m + 1; --i) {
+            const int j = static_cast<int>(block_index(cfg_, "u" + std::to_string(i)));
+            cond(j, &s, &o);
+            up_block(i, lv_[i].D, U_of(i + 1), U_of(i), s, o);
+        }
+        const int j = static_cast<int>(block_index(cfg_, "u" + std::to_string(m + 1)));
+        cond(j, &s, &o);
         for (int b = 0; b < 2; ++b) {
-            for (int i = top; i >= m + 1; --i) {
-                const int j = static_cast<int>(block_index(cfg_, "u" + std::to_string(i)));
-                cond(j, &s, &o);
-                if (i == m + 1) await_store(b);
-                up_block(i, half(lv_[i].D, b), half(U_of(i + 1), b), half(U_of(i), b), s, o);
-            }
+            await_store(b);
+            up_block(m + 1, half(lv_[m + 1].D, b), half(U_of(m + 2), b), half(U_of(m + 1), b), s, o);
             cache_ready(b);
         }
         first = m;
