@@ -28,6 +28,7 @@
 // smem-bandwidth bound at BN <= 160).
 #include "conv_tc.cuh"
 #include "ptx.cuh"
+#include "pdl.cuh"
 
 #include <cstdlib>
 
@@ -44,8 +45,6 @@ constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
 constexpr int kSmemMax = 232448;             // 227 KB opt-in dynamic shared memory
 constexpr int kSmemFixed = 1024 + 256;       // alignment slack + barriers
 constexpr int kMaxTabClasses = 16;           // border classes staged in smem (3x3 kernels)
-constexpr int kStageChunk = 2048;                      // one staged box: 32 px x 16 ch (fp32; fp16 uses half)
-constexpr int kStageOutBytes = kEpiWarps * 2 * kStageChunk;  // TMA-store staging: 2 chunks per warp
 
 // Epilogue flavours (compile-time, so the inner loop carries no mode tests).
 enum Epi : int {
@@ -63,18 +62,24 @@ __host__ __device__ inline int tab_floats(int rc, int bn) {
     return ncls <= kMaxTabClasses ? (ncls + 1) * bn : 0;
 }
 
-__host__ __device__ inline int epi_smem_bytes(int tabf, int tma_out) {
-    // offset tables, then (1024-aligned) the TMA-store staging buffers
-    return tma_out ? ((2 * tabf * 4 + 1023) & ~1023) + kStageOutBytes : 2 * tabf * 4;
+// one staged TMA-store box: 32 px x 16 channels (fp32 raw or fp16)
+__host__ __device__ inline int stage_chunk(int wide) { return wide ? 2048 : 1024; }
+// offset tables: double-buffered, single with a weight-stationary schedule
+// (one (parity, N tile) slab per CTA)
+__host__ __device__ inline int tab_bytes(int tabf, int b_res) { return (b_res ? 1 : 2) * tabf * 4; }
+__host__ __device__ inline int epi_smem_bytes(int tabf, int tma_out, int wide, int b_res) {
+    // offset tables, then (1024-aligned) the TMA-store staging (2 boxes per epilogue warp)
+    const int tb = tab_bytes(tabf, b_res);
+    return tma_out ? ((tb + 1023) & ~1023) + kEpiWarps * 2 * stage_chunk(wide) : tb;
 }
 
 // ring stages: A + B per stage, or A only with a resident weight panel of
 // total_kb K blocks (b_res)
 template <int CG>
-__host__ __device__ inline int num_stages(int bn, int tabf, int tma_out, int b_res, int total_kb) {
+__host__ __device__ inline int num_stages(int bn, int tabf, int tma_out, int b_res, int total_kb, int wide) {
     const int bblk = (bn / CG) * kBK * 2;
     const int per = static_cast<int>(kABytes) + (b_res ? 0 : bblk);
-    int s = (kSmemMax - kSmemFixed - epi_smem_bytes(tabf, tma_out) - (b_res ? total_kb * bblk : 0)) / per;
+    int s = (kSmemMax - kSmemFixed - epi_smem_bytes(tabf, tma_out, wide, b_res) - (b_res ? total_kb * bblk : 0)) / per;
     return s > 8 ? 8 : (s < 2 ? 2 : s);
 }
 
@@ -152,7 +157,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < p.nseg; ++s) total_kb += p.seg[s].ntaps * p.seg[s].ncb;
     const bool b_res = CG == 1 && p.b_res;
     const int tabf = tab_floats(p.rc, p.BN);
-    const int stages = num_stages<CG>(p.BN, tabf, p.tma_out, b_res, total_kb);
+    const int stages = num_stages<CG>(p.BN, tabf, p.tma_out, b_res, total_kb, p.nhwc32);
+    const int schunk = stage_chunk(p.nhwc32);
     const int bn_cta = p.BN / CG;  // B rows staged by this CTA
     const uint32_t b_bytes = static_cast<uint32_t>(bn_cta) * kBK * 2;
     uint8_t* smA = smem;
@@ -166,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bfull + 1);
     // two epilogue offset tables [ncls + 1][BN] fp32 (see the header comment)
     const uint32_t tab_s = smem_u32(smB + b_blocks * b_bytes + 256);
-    const uint32_t stage_out_s = tab_s + ((2 * tabf * 4 + 1023) & ~1023);
+    const uint32_t stage_out_s = tab_s + ((tab_bytes(tabf, b_res) + 1023) & ~1023);
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -240,6 +246,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
     const uint32_t acc_stride = ncols / 2;  // column offset of accumulator buffer 1
+    // everything above overlapped the previous kernel's tail (PDL); inputs
+    // and outputs are touched only below
+    pdl_trigger();
+    pdl_wait();
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
@@ -490,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (EPI == kEpiF32Raw) {
                         if (p.tma_out) {
                             const uint32_t sb =
-                                stage_out_s + static_cast<uint32_t>(((warp - 2) * 2 + hh) * kStageChunk + lane * 64);
+                                stage_out_s + static_cast<uint32_t>(((warp - 2) * 2 + hh) * schunk + lane * 64);
 #pragma unroll
                             for (int j = 0; j < 16; j += 4)
                                 sts128(sb + 4 * j, make_float4(__uint_as_float(v[j]) * hscale,
@@ -549,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             h[j / 2] = __floats2half2_rn(a, b);
                         }
                         if (p.tma_out) {
-                            const uint32_t sb = stage_out_s + static_cast<uint32_t>(((warp - 2) * 2 + hh) * kStageChunk + lane * 32);
+                            const uint32_t sb = stage_out_s + static_cast<uint32_t>(((warp - 2) * 2 + hh) * schunk + lane * 32);
                             sts128u(sb, *reinterpret_cast<uint4*>(&h[0]));
                             sts128u(sb + 16, *reinterpret_cast<uint4*>(&h[4]));
                         } else {
@@ -567,9 +577,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                     if (lane == 0 && warp_store) {
                         const int nb0 = tc.n_tile * p.BN + c00;
-                        const uint32_t sb = stage_out_s + static_cast<uint32_t>((warp - 2) * 2 * kStageChunk);
+                        const uint32_t sb = stage_out_s + static_cast<uint32_t>((warp - 2) * 2 * schunk);
                         if (nb0 < p.cs_out) tma_store_4d(&p.tmO[tc.parity], sb, nb0, bx, by, bi);
-                        if (two && nb0 + 32 < p.cs_out) tma_store_4d(&p.tmO[tc.parity], sb + kStageChunk, nb0 + 32, bx, by, bi);
+                        if (two && nb0 + 32 < p.cs_out) tma_store_4d(&p.tmO[tc.parity], sb + schunk, nb0 + 32, bx, by, bi);
                         bulk_commit();
                     }
                 }
@@ -622,10 +632,10 @@ size_t smem_bytes_for(const ConvParams& p) {
     int total_kb = 0;
     for (int s = 0; s < p.nseg; ++s) total_kb += p.seg[s].ntaps * p.seg[s].ncb;
     const int b_res = CG == 1 && p.b_res;
-    const int st = num_stages<CG>(p.BN, tabf, p.tma_out, b_res, total_kb);
+    const int st = num_stages<CG>(p.BN, tabf, p.tma_out, b_res, total_kb, p.nhwc32);
     const size_t bblk = static_cast<size_t>(p.BN / CG) * kBK * 2;
     return kSmemFixed + static_cast<size_t>(st) * (kABytes + (b_res ? 0 : bblk)) + (b_res ? total_kb * bblk : 0) +
-           epi_smem_bytes(tabf, p.tma_out);
+           epi_smem_bytes(tabf, p.tma_out, p.nhwc32, b_res);
 }
 
 int g_cta_group_override = -1;  // LC_CTA_GROUP env: 1 or 2 forces the variant
@@ -645,8 +655,8 @@ cudaError_t launch_variant(const ConvParams& p, int parities, cudaStream_t strea
         const int total = m_tiles * n_tiles * parities;
         int grid = total < sm_count() ? total : sm_count();
         if (p.b_res) grid = (sm_count() / (n_tiles * parities)) * n_tiles * parities;
-        conv_tc_kernel<1, EPI><<<grid, kThreads, smem_bytes_for<1>(p), stream>>>(p, n_tiles, parities);
-        return cudaGetLastError();
+        return launch_pdl(conv_tc_kernel<1, EPI>, dim3(grid), dim3(kThreads), smem_bytes_for<1>(p), stream, p,
+                          n_tiles, parities);
     }
     const int units = ((m_tiles + 1) / 2) * n_tiles * parities;
     const int pairs = units < sm_count() / 2 ? units : sm_count() / 2;
@@ -655,13 +665,15 @@ cudaError_t launch_variant(const ConvParams& p, int parities, cudaStream_t strea
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem_bytes_for<2>(p);
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, conv_tc_kernel<CG, EPI>, p, n_tiles, parities);
 }
 
@@ -712,8 +724,8 @@ static bool want_b_res(const ConvParams& p, int parities) {
     if (m_tiles < 2 * cps) return false;
     int total_kb = 0;
     for (int s = 0; s < p.nseg; ++s) total_kb += p.seg[s].ntaps * p.seg[s].ncb;
-    return num_stages<1>(p.BN, tab_floats(p.rc, p.BN), p.tma_out, 1, total_kb) >= 3 &&
-           (kSmemMax - kSmemFixed - epi_smem_bytes(tab_floats(p.rc, p.BN), p.tma_out) -
+    return num_stages<1>(p.BN, tab_floats(p.rc, p.BN), p.tma_out, 1, total_kb, p.nhwc32) >= 3 &&
+           (kSmemMax - kSmemFixed - epi_smem_bytes(tab_floats(p.rc, p.BN), p.tma_out, p.nhwc32, 1) -
             total_kb * p.BN * kBK * 2) >= 3 * static_cast<int>(kABytes);
 }
 

@@ -1,5 +1,6 @@
 // HBM-bound and thin-channel kernels; see kernels.cuh.
 #include "kernels.cuh"
+#include "pdl.cuh"
 
 namespace lc {
 
@@ -145,6 +146,7 @@ __global__ void __launch_bounds__(128) thin_in_fast_kernel(const ThinInArgs a, i
 // One thread per (output pixel, 8-tap group): writes 16 bytes of the fp16
 // patch row; groups past c_in*k*k are zero.
 __global__ void patch_kernel(const ThinInArgs a, int kp) {
+    pdl_wait();
     const int kk = a.k * a.k, KK = a.c_in * kk;
     const int oh = a.win.oy1 - a.win.oy0, ow = a.win.ox1 - a.win.ox0;
     const int nimg = a.cfg_pair ? 2 * a.nsrc : a.nsrc;
@@ -186,6 +188,7 @@ __global__ void patch_kernel(const ThinInArgs a, int kp) {
 // 32 pixels of one output row x 8 tap groups, so a warp writes 4 pixels x
 // 128 B contiguous and all index math is 32-bit with constant divisors.
 __global__ void __launch_bounds__(256) patch3_kernel(const ThinInArgs a) {
+    pdl_wait();
     constexpr int K = 3, KK = 9;
     const int g = threadIdx.x & 7;
     const int oh = a.win.oy1 - a.win.oy0;
@@ -224,6 +227,7 @@ __global__ void __launch_bounds__(256) patch3_kernel(const ThinInArgs a) {
 // is a 16 B (C = 4) load at a 16*k*k-float stride, served from L2 (y was
 // just written by the GEMM).
 __global__ void __launch_bounds__(256) tap_gather_kernel(const TapGatherArgs a) {
+    pdl_wait();
     const int ow = a.win.ox1 - a.win.ox0, oh = a.win.oy1 - a.win.oy0;
     const int idx = static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= a.n * oh * ow) return;
@@ -259,6 +263,7 @@ __global__ void __launch_bounds__(256) tap_gather_kernel(const TapGatherArgs a) 
 // One thread per low-res pixel: its 2x2 output pixels x C channels; each
 // (parity, tap) group is one 16 B load (channels padded to 4 in y).
 __global__ void __launch_bounds__(128) subpix_gather_kernel(const SubpixGatherArgs a) {
+    pdl_wait();
     const int X = static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int row = static_cast<int>(blockIdx.y);
     const int n = row / a.H, Y = row - n * a.H;
@@ -446,6 +451,7 @@ __global__ void thin_out_kernel(const ThinOutArgs a) {
 // ------------------------------------------------------------- resampling
 __global__ void down2_kernel(const __half* __restrict__ in, __half* __restrict__ out, int nimg,
                              int H, int W, int cs) {
+    pdl_wait();
     const int h2 = H / 2, w2 = W / 2, cv = cs / 8;
     const int64_t total = static_cast<int64_t>(nimg) * h2 * w2 * cv;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -499,6 +505,7 @@ __global__ void up2_kernel(const __half* __restrict__ in, __half* __restrict__ o
 
 // ------------------------------------------------------------ step update
 __global__ void step_kernel(const StepArgs a) {
+    pdl_wait();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < a.n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const float eu = a.eps2[i], ec = a.eps2[a.n + i];
@@ -511,12 +518,14 @@ __global__ void step_kernel(const StepArgs a) {
 }
 
 __global__ void linear_kernel(float a, const float* x, float b, const float* y, float* out, int64_t n) {
+    pdl_wait();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         out[i] = __fadd_rn(__fmul_rn(a, x[i]), __fmul_rn(b, y[i]));
 }
 
 __global__ void isfinite_kernel(const float* x, int64_t n, int* bad) {
+    pdl_wait();
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         if (!isfinite(x[i])) atomicOr(bad, 1);
@@ -551,11 +560,10 @@ cudaError_t launch_patch(const ThinInArgs& a, int kp, cudaStream_t st) {
     const int rows = nimg * (a.win.oy1 - a.win.oy0);
     if (a.k == 3 && kp == 64 && a.c_in * 9 <= 64 && rows < 65536) {
         const dim3 grid((a.win.ox1 - a.win.ox0 + 31) / 32, rows);
-        if (grid.x > 0 && rows > 0) patch3_kernel<<<grid, 256, 0, st>>>(a);
+        if (grid.x > 0 && rows > 0) return launch_pdl(patch3_kernel, grid, dim3(256), 0, st, a);
         return cudaGetLastError();
     }
-    patch_kernel<<<grid_for(work, 256), 256, 0, st>>>(a, kp);
-    return cudaGetLastError();
+    return launch_pdl(patch_kernel, dim3(grid_for(work, 256)), dim3(256), 0, st, a, kp);
 }
 
 cudaError_t launch_tap_gather(const TapGatherArgs& a, cudaStream_t st) {
@@ -564,16 +572,14 @@ cudaError_t launch_tap_gather(const TapGatherArgs& a, cudaStream_t st) {
     if (a.C > 4) return cudaErrorInvalidValue;
     const int64_t total = static_cast<int64_t>(rows) * ow;
     if (total >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
-    tap_gather_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(tap_gather_kernel, dim3(static_cast<unsigned>((total + 255) / 256)), dim3(256), 0, st, a);
 }
 
 cudaError_t launch_subpix_gather(const SubpixGatherArgs& a, cudaStream_t st) {
     const int rows = a.n * a.H;
     if (a.W <= 0 || rows <= 0) return cudaSuccess;
     if (a.C > 4 || rows >= 65536) return cudaErrorInvalidValue;
-    subpix_gather_kernel<<<dim3((a.W + 127) / 128, rows), 128, 0, st>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(subpix_gather_kernel, dim3((a.W + 127) / 128, rows), dim3(128), 0, st, a);
 }
 
 cudaError_t launch_upconv_thin(const UpThinArgs& a, cudaStream_t st) {
@@ -652,8 +658,7 @@ cudaError_t launch_thin_out(const ThinOutArgs& a, cudaStream_t st) {
 
 cudaError_t launch_down2(const __half* in, __half* out, int nimg, int H, int W, int cs, cudaStream_t st) {
     const int64_t work = static_cast<int64_t>(nimg) * (H / 2) * (W / 2) * (cs / 8);
-    down2_kernel<<<grid_for(work, 256), 256, 0, st>>>(in, out, nimg, H, W, cs);
-    return cudaGetLastError();
+    return launch_pdl(down2_kernel, dim3(grid_for(work, 256)), dim3(256), 0, st, in, out, nimg, H, W, cs);
 }
 
 cudaError_t launch_up2(const __half* in, __half* out, int nimg, int H, int W, int cs, cudaStream_t st) {
@@ -663,19 +668,16 @@ cudaError_t launch_up2(const __half* in, __half* out, int nimg, int H, int W, in
 }
 
 cudaError_t launch_step(const StepArgs& a, cudaStream_t st) {
-    step_kernel<<<grid_for(a.n, 256), 256, 0, st>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(step_kernel, dim3(grid_for(a.n, 256)), dim3(256), 0, st, a);
 }
 
 cudaError_t launch_linear(float a, const float* x, float b, const float* y, float* out, int64_t n,
                           cudaStream_t st) {
-    linear_kernel<<<grid_for(n, 256), 256, 0, st>>>(a, x, b, y, out, n);
-    return cudaGetLastError();
+    return launch_pdl(linear_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, a, x, b, y, out, n);
 }
 
 cudaError_t launch_isfinite(const float* x, int64_t n, int* bad, cudaStream_t st) {
-    isfinite_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, bad);
-    return cudaGetLastError();
+    return launch_pdl(isfinite_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, x, n, bad);
 }
 
 }  // namespace lc
