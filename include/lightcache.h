@@ -98,6 +98,13 @@ int lc_forward(lc_ctx* ctx, const float* x, int64_t T, int64_t timestep, const f
 /* decode_batch / decode_sliced (proj/src/codec.cpp:117-145) of n latents
  * (n,1,C,h,w) -> (n,1,3,H,W); `slice` frames per launch group. */
 int lc_decode(lc_ctx* ctx, const float* latents, int64_t n, int64_t slice, float* video);
+/* Quality metrics: per-frame PSNR (dB, capped at 99) and
+ * mean 7x7-window SSIM of two b=1 videos {t,c,h,w} fp32 (host or device
+ * pointers), data range L.  Replaces psnr / ssim / video_series
+ * (proj/src/metrics.cpp:10-104).  Errors: data_range <= 0 -> 2 (ConfigError),
+ * h or w < 7 -> 1 (ShapeError). */
+int lc_video_metrics(lc_ctx* ctx, const float* a, const float* b, int64_t t, int64_t c, int64_t h,
+                     int64_t w, double data_range, double* psnr, double* ssim);
 /* conv2d (proj/src/tensor.cpp:151-197) of affine(x, s, o) with optional SiLU
  * on the tensor-core kernel: x (b,t,c_in,h,w), taps [c_out][c_in][k][k]. */
 int lc_conv2d(lc_ctx* ctx, const float* x, int64_t b, int64_t t, int64_t c_in, int64_t h,

@@ -267,6 +267,16 @@ class Restatement:
         return self.lib.lco_flops_estimate(ctypes.byref(cfg), ctypes.c_int64(B), ctypes.c_int64(T),
                                            ctypes.c_int64(h), ctypes.c_int64(w), ctypes.c_int(int(cached)))
 
+    def video_metrics(self, a, b, data_range=1.0):
+        """psnr/ssim video_series (proj/src/metrics.cpp:10-104) of two b=1 videos."""
+        a, b = _f32(a), _f32(b)
+        t, c, h, w = a.shape[-4:]
+        ps, ss = np.empty(t, np.float64), np.empty(t, np.float64)
+        i64 = ctypes.c_int64
+        self._chk(self.lib.lco_video_metrics(_p(a), _p(b), i64(t), i64(c), i64(h), i64(w), ctypes.c_double(data_range),
+                                _p(ps), _p(ss)))
+        return ps, ss
+
 
 class Reference:
     """The reference itself (oracle/_ref) via its C shim oracle/ref_capi.cpp."""
@@ -359,3 +369,19 @@ class Reference:
             ctypes.c_int(halo_kind), ctypes.c_int64(halo_px), ctypes.c_int64(k), _p(regions),
             ctypes.byref(halo)))
         return regions.reshape(-1, 3, 4), halo.value
+
+    def video_metrics(self, a, b, data_range=1.0):
+        """psnr/ssim video_series (proj/src/metrics.cpp:10-104) of two b=1 videos."""
+        a, b = _f32(a), _f32(b)
+        t, c, h, w = a.shape[-4:]
+        ps, ss = np.empty(t, np.float64), np.empty(t, np.float64)
+        i64 = ctypes.c_int64
+        self._chk(self.lib.ref_video_metrics(_p(a), _p(b), i64(t), i64(c), i64(h), i64(w), ctypes.c_double(data_range),
+                                _p(ps), _p(ss)))
+        return ps, ss
+
+    def write_video_raw(self, path, video):
+        v = _f32(video)
+        t, c, h, w = v.shape[-4:]
+        i64 = ctypes.c_int64
+        self._chk(self.lib.ref_write_video_raw(path.encode(), _p(v), i64(t), i64(c), i64(h), i64(w)))

@@ -15,6 +15,7 @@
 #include "stagecache/chunk.hpp"
 #include "stagecache/codec.hpp"
 #include "stagecache/config.hpp"
+#include "stagecache/metrics.hpp"
 #include "stagecache/pipeline.hpp"
 #include "stagecache/unet.hpp"
 
@@ -234,6 +235,32 @@ int ref_model_numbers(const char* config_text, int64_t* out) {
         out[5] = cs.h;
         out[6] = cs.w;
         out[7] = cache_bytes(cfg.cache_policy(), cfg.unet, in);
+    });
+}
+
+// video_series(psnr/ssim) over two b=1 videos {t,c,h,w} (proj/src/metrics.cpp:10-104).
+int ref_video_metrics(const float* a, const float* b, int64_t t, int64_t c, int64_t h, int64_t w,
+                      double data_range, double* psnr_out, double* ssim_out) {
+    return guarded([&] {
+        Tensor5 ta = Tensor5::uninit({1, t, c, h, w});
+        Tensor5 tb = Tensor5::uninit({1, t, c, h, w});
+        std::memcpy(ta.data(), a, static_cast<size_t>(ta.bytes()));
+        std::memcpy(tb.data(), b, static_cast<size_t>(tb.bytes()));
+        const MetricSeries ps = video_series(&psnr, ta, tb, data_range);
+        const MetricSeries ss = video_series(&ssim, ta, tb, data_range);
+        for (int64_t i = 0; i < t; ++i) {
+            psnr_out[i] = ps.per_frame[static_cast<size_t>(i)];
+            ssim_out[i] = ss.per_frame[static_cast<size_t>(i)];
+        }
+    });
+}
+
+// write_video_raw (proj/src/codec.cpp:172-182): the artifact format.
+int ref_write_video_raw(const char* path, const float* video, int64_t t, int64_t c, int64_t h, int64_t w) {
+    return guarded([&] {
+        Tensor5 v = Tensor5::uninit({1, t, c, h, w});
+        std::memcpy(v.data(), video, static_cast<size_t>(v.bytes()));
+        write_video_raw(path, v);
     });
 }
 

@@ -94,7 +94,7 @@ EXPORTS = [
     "lc_config_to_text", "lc_configure", "lc_latent_elems", "lc_video_elems", "lc_run_pipeline",
     "lc_upload_latent", "lc_run_resident", "lc_run_resident_async", "lc_wait", "lc_download_video",
     "lc_set_decode_slice",
-    "lc_forward", "lc_decode", "lc_conv2d", "lc_up_conv2d", "lc_plan_steps", "lc_split",
+    "lc_forward", "lc_decode", "lc_video_metrics", "lc_conv2d", "lc_up_conv2d", "lc_plan_steps", "lc_split",
     "lc_model_numbers", "lc_derive_seed", "lc_randn", "lc_shard_frames", "lc_nccl_unique_id",
     "lc_nccl_init", "lc_decode_sharded", "lc_timer_start", "lc_timer_stop", "lc_set_conv_profile",
     "lc_conv_profile", "lc_alloc_pinned", "lc_free_pinned",
@@ -326,6 +326,18 @@ class Context:
         out = np.empty((lat.shape[0], lat.shape[1], 3, lat.shape[3] * s, lat.shape[4] * s), np.float32)
         _check(lib().lc_decode(self._h, _p(lat), I64(n), I64(slice_frames), _p(out)))
         return out
+
+    def video_metrics(self, a, b, data_range: float = 1.0):
+        """Per-frame PSNR and SSIM of two b=1 videos (t,c,h,w) on the GPU
+        (psnr / ssim / video_series, proj/src/metrics.cpp:10-104)."""
+        a, b = _f32(a), _f32(b)
+        if a.shape != b.shape:
+            raise ShapeError("video_metrics: shape mismatch")
+        t, c, h, w = a.shape[-4:]
+        ps, ss = np.empty(t, np.float64), np.empty(t, np.float64)
+        _check(lib().lc_video_metrics(self._h, _p(a), _p(b), I64(t), I64(c), I64(h), I64(w),
+                                      ctypes.c_double(data_range), _p(ps), _p(ss)))
+        return ps, ss
 
     def conv2d(self, x, taps, bias, s=1.0, o=0.0, silu=False):
         x, taps, bias = _f32(x), _f32(taps), _f32(bias)

@@ -9,6 +9,7 @@
 #include <string>
 
 #include "engine.hpp"
+#include "metrics.cuh"
 
 struct lc_ctx {
     explicit lc_ctx(int dev) : device(dev), engine(dev) {}
@@ -228,6 +229,37 @@ int lc_free_pinned(void* p) {
 int lc_forward(lc_ctx* ctx, const float* x, int64_t T, int64_t timestep, const float* deep_in,
                float* deep_out, float* eps) {
     return guarded([&] { ctx->engine.forward(x, T, timestep, deep_in, deep_out, eps); });
+}
+int lc_video_metrics(lc_ctx* ctx, const float* a, const float* b, int64_t t, int64_t c, int64_t h, int64_t w,
+                     double data_range, double* psnr, double* ssim) {
+    return guarded([&] {
+        if (!(data_range > 0.0)) lc::throw_config("psnr: data_range must be positive");
+        if (h < 7 || w < 7) lc::throw_shape("ssim: frame smaller than the 7x7 window");
+        if (t < 1 || c < 1) lc::throw_shape("video_metrics: empty video");
+        const size_t bytes = static_cast<size_t>(t * c * h * w) * 4;
+        auto on_device = [](const void* p) {
+            cudaPointerAttributes pa{};
+            const bool dev = cudaPointerGetAttributes(&pa, p) == cudaSuccess &&
+                             (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged);
+            cudaGetLastError();
+            return dev;
+        };
+        lc::DevBuf da, db;
+        const float* pa = a;
+        const float* pb = b;
+        cudaStream_t st = ctx->engine.stream();
+        if (!on_device(a)) {
+            da = lc::dev_alloc(nullptr, static_cast<int64_t>(bytes), false);
+            LC_CUDA(cudaMemcpyAsync(da.p, a, bytes, cudaMemcpyHostToDevice, st));
+            pa = da.as<float>();
+        }
+        if (!on_device(b)) {
+            db = lc::dev_alloc(nullptr, static_cast<int64_t>(bytes), false);
+            LC_CUDA(cudaMemcpyAsync(db.p, b, bytes, cudaMemcpyHostToDevice, st));
+            pb = db.as<float>();
+        }
+        LC_CUDA(lc::video_metrics(pa, pb, t, c, h, w, data_range, psnr, ssim, st));
+    });
 }
 int lc_decode(lc_ctx* ctx, const float* latents, int64_t n, int64_t slice, float* video) {
     return guarded([&] { ctx->engine.decode(latents, n, video, slice); });

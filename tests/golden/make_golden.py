@@ -97,6 +97,29 @@ def slice0(name, over):
     print(name, f"{time.time() - t:.1f}s", flush=True)
 
 
+def metrics():
+    """psnr / ssim per frame (proj/src/metrics.cpp) from the reference on
+    seeded videos: a perturbed pair, an identical pair, and the tiny
+    baseline-vs-cached pipeline videos (the compare/sweep use)."""
+    ref = lco.Reference()
+    rng = np.random.default_rng(11)
+    out = {}
+    a = rng.random((1, 3, 3, 20, 29)).astype(np.float32)
+    b = np.clip(a + 0.03 * rng.standard_normal(a.shape), 0, 1).astype(np.float32)
+    for name, (x, y) in {"noise": (a, b), "same": (a, a.copy())}.items():
+        ps, ss = ref.video_metrics(x[0], y[0], 1.0)
+        out[name + "_a"], out[name + "_b"], out[name + "_psnr"], out[name + "_ssim"] = x, y, ps, ss
+    tiny = dict(SMALL["tiny"])
+    base = kv_of(dict(tiny, **{"cache.enabled": "false", "chunk.enabled": "false", "decode.sliced": "false",
+                               "swap.mode": "off"}))
+    var = kv_of(dict(tiny, **{"cache.n": 3}))
+    va = ref.run_pipeline(base)[0]
+    vb = ref.run_pipeline(var)[0]
+    ps, ss = ref.video_metrics(va[0], vb[0], 1.0)
+    out.update(pipe_a=va, pipe_b=vb, pipe_psnr=ps, pipe_ssim=ss)
+    np.savez_compressed(os.path.join(HERE, "metrics.npz"), **out)
+
+
 if __name__ == "__main__":
     what = sys.argv[1:] or ["small"]
     if "small" in what:
@@ -105,3 +128,5 @@ if __name__ == "__main__":
         slice0("b_frame0", B0)
     if "c0" in what:
         slice0("c_frame0", C0)
+    if "metrics" in what:
+        metrics()
