@@ -73,6 +73,15 @@ int lc_download_video(lc_ctx* ctx, float* video);
  * key; the output is identical for every value). */
 int lc_set_decode_slice(lc_ctx* ctx, int64_t frames);
 
+/* Memory ledger: the engine's physical event log in the
+ * reference's ledger.csv format (write_ledger_csv, proj/src/ledger.cpp:224-242:
+ * seq,clock,kind,tier,bytes,alloc_id,occupancy_bytes,stage), and its summary
+ * (write_ledger_json content: per-stage fast/slow peaks and event counts,
+ * overall peaks, current occupancy, event count) as JSON.  `needed` receives
+ * the full text length; text beyond `cap` is truncated. */
+int lc_ledger_csv(lc_ctx* ctx, char* buf, int64_t cap, int64_t* needed);
+int lc_ledger_summary(lc_ctx* ctx, char* buf, int64_t cap);
+
 /* Measurement helpers (bench.py) ------------------------------------------ */
 /* CUDA events on the context's compute stream bracketing any number of
  * calls; lc_timer_stop synchronises and returns the elapsed device ms. */

@@ -94,7 +94,7 @@ EXPORTS = [
     "lc_config_to_text", "lc_configure", "lc_latent_elems", "lc_video_elems", "lc_run_pipeline",
     "lc_upload_latent", "lc_run_resident", "lc_run_resident_async", "lc_wait", "lc_download_video",
     "lc_set_decode_slice",
-    "lc_forward", "lc_decode", "lc_video_metrics", "lc_conv2d", "lc_up_conv2d", "lc_plan_steps", "lc_split",
+    "lc_forward", "lc_decode", "lc_video_metrics", "lc_ledger_csv", "lc_ledger_summary", "lc_conv2d", "lc_up_conv2d", "lc_plan_steps", "lc_split",
     "lc_model_numbers", "lc_derive_seed", "lc_randn", "lc_shard_frames", "lc_nccl_unique_id",
     "lc_nccl_init", "lc_decode_sharded", "lc_timer_start", "lc_timer_stop", "lc_set_conv_profile",
     "lc_conv_profile", "lc_alloc_pinned", "lc_free_pinned",

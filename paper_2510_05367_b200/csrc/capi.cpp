@@ -230,6 +230,44 @@ int lc_forward(lc_ctx* ctx, const float* x, int64_t T, int64_t timestep, const f
                float* deep_out, float* eps) {
     return guarded([&] { ctx->engine.forward(x, T, timestep, deep_in, deep_out, eps); });
 }
+int lc_ledger_csv(lc_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
+    return guarded([&] {
+        static const char* kinds[5] = {"alloc", "free", "move_start", "move_end", "stage_enter"};
+        static const char* stages[4] = {"setup", "encode", "denoise", "decode"};
+        const lc::Ledger& l = ctx->engine.ledger();
+        std::ostringstream os;
+        os << "seq,clock,kind,tier,bytes,alloc_id,occupancy_bytes,stage\n";
+        int64_t occ[2] = {0, 0};
+        for (const lc::LedgerEvent& e : l.events) {
+            if (e.kind == 0) occ[e.tier] += e.bytes;
+            if (e.kind == 1) occ[e.tier] -= e.bytes;
+            os << e.seq << ',' << e.clock << ',' << kinds[e.kind] << ',' << (e.tier ? "slow" : "fast") << ','
+               << e.bytes << ',' << e.alloc_id << ',' << occ[e.tier] << ',' << stages[e.stage] << "\n";
+        }
+        const std::string t = os.str();
+        if (needed) *needed = static_cast<int64_t>(t.size()) + 1;
+        put(buf, cap, t);
+    });
+}
+int lc_ledger_summary(lc_ctx* ctx, char* buf, int64_t cap) {
+    return guarded([&] {
+        static const char* stages[4] = {"setup", "encode", "denoise", "decode"};
+        const lc::Ledger& l = ctx->engine.ledger();
+        std::ostringstream os;
+        int64_t over[2] = {0, 0};
+        os << "{\"clock\":\"monotonic\",\"stages\":{";
+        for (int s = 0; s < 4; ++s) {
+            over[0] = std::max(over[0], l.peak[s][0]);
+            over[1] = std::max(over[1], l.peak[s][1]);
+            os << (s ? "," : "") << "\"" << stages[s] << "\":{\"fast_peak_bytes\":" << l.peak[s][0]
+               << ",\"slow_peak_bytes\":" << l.peak[s][1] << ",\"events\":" << l.events_per_stage[s] << "}";
+        }
+        os << "},\"overall\":{\"fast_peak_bytes\":" << over[0] << ",\"slow_peak_bytes\":" << over[1]
+           << "},\"current\":{\"fast_bytes\":" << l.occ[0] << ",\"slow_bytes\":" << l.occ[1]
+           << "},\"event_count\":" << l.events.size() << "}";
+        put(buf, cap, os.str());
+    });
+}
 int lc_video_metrics(lc_ctx* ctx, const float* a, const float* b, int64_t t, int64_t c, int64_t h, int64_t w,
                      double data_range, double* psnr, double* ssim) {
     return guarded([&] {

@@ -7,6 +7,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <chrono>
+
 namespace lc {
 
 void cuda_check(cudaError_t e, const char* what) {
@@ -15,11 +17,19 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 
 // ---------------------------------------------------------------- ledger
+double Ledger::now() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+void Ledger::record(int kind, int tier, int64_t bytes, uint64_t id) {
+    events.push_back({kind, bytes, tier, stage, id, static_cast<uint64_t>(events.size()), now() - t0});
+    ++events_per_stage[stage];
+}
 void Ledger::enter(int s) {
     stage = s;
     for (int t = 0; t < 2; ++t) peak[s][t] = std::max(peak[s][t], occ[t]);
+    record(4, 0, 0, 0);
 }
-void Ledger::alloc(int tier, int64_t bytes) {
+uint64_t Ledger::alloc(int tier, int64_t bytes) {
     if (tier == 0 && budget_fast > 0 && occ[0] + bytes > budget_fast) {
         static const char* names[4] = {"setup", "encode", "denoise", "decode"};
         throw LcError(kBudgetError, std::string("fast-tier budget exceeded in stage ") + names[stage] +
@@ -28,8 +38,14 @@ void Ledger::alloc(int tier, int64_t bytes) {
     }
     occ[tier] += bytes;
     peak[stage][tier] = std::max(peak[stage][tier], occ[tier]);
+    const uint64_t id = next_id++;
+    record(0, tier, bytes, id);
+    return id;
 }
-void Ledger::free(int tier, int64_t bytes) { occ[tier] -= bytes; }
+void Ledger::free(int tier, int64_t bytes, uint64_t id) {
+    occ[tier] -= bytes;
+    record(1, tier, bytes, id);
+}
 
 DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
     if (this != &o) {
@@ -38,6 +54,7 @@ DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
         bytes = o.bytes;
         ledger = o.ledger;
         tier = o.tier;
+        id = o.id;
         o.p = nullptr;
         o.bytes = 0;
     }
@@ -47,7 +64,7 @@ void DevBuf::reset() {
     if (p) {
         if (tier == 0) cudaFree(p);
         else cudaFreeHost(p);
-        if (ledger) ledger->free(tier, bytes);
+        if (ledger) ledger->free(tier, bytes, id);
     }
     p = nullptr;
     bytes = 0;
@@ -55,7 +72,7 @@ void DevBuf::reset() {
 DevBuf dev_alloc(Ledger* l, int64_t bytes, bool zero) {
     DevBuf b;
     if (bytes <= 0) return b;
-    if (l) l->alloc(0, bytes);
+    if (l) b.id = l->alloc(0, bytes);
     LC_CUDA(cudaMalloc(&b.p, static_cast<size_t>(bytes)));
     if (zero) LC_CUDA(cudaMemset(b.p, 0, static_cast<size_t>(bytes)));
     b.bytes = bytes;
@@ -66,7 +83,7 @@ DevBuf dev_alloc(Ledger* l, int64_t bytes, bool zero) {
 DevBuf host_alloc(Ledger* l, int64_t bytes) {
     DevBuf b;
     if (bytes <= 0) return b;
-    if (l) l->alloc(1, bytes);
+    if (l) b.id = l->alloc(1, bytes);
     LC_CUDA(cudaHostAlloc(&b.p, static_cast<size_t>(bytes), cudaHostAllocDefault));
     b.bytes = bytes;
     b.ledger = l;

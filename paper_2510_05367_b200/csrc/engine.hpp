@@ -27,14 +27,36 @@ void cuda_check(cudaError_t e, const char* what);
 // by the engine, Slow = pinned host bytes (cf. MemLedger,
 // proj/include/stagecache/ledger.hpp:69-146; peaks per stage, fast budget).
 enum Stage { kSetup = 0, kEncode = 1, kDenoise = 2, kDecode = 3 };
+// Physical memory ledger of the engine (the reference's
+// MemLedger, proj/src/ledger.cpp:35-123): every HBM (fast) and pinned-host
+// (slow) allocation and free is an event with an id, the stage it happened
+// in and a monotonic clock; stage entries are events too.  Peaks per
+// (stage, tier), the fast-tier budget (BudgetError naming the stage) and
+// the CSV / JSON writers' content (proj/src/ledger.cpp:200-242) come from it.
+// Swap transfers do not change occupancy here: the device cache buffer and
+// its pinned host copy are both resident for the whole run.
+struct LedgerEvent {
+    int kind;  // 0 alloc, 1 free, 4 stage_enter (ledger.hpp MemEventKind)
+    int64_t bytes;
+    int tier;  // 0 fast (HBM), 1 slow (pinned host)
+    int stage;
+    uint64_t alloc_id, seq;
+    double clock;  // seconds since the ledger was created
+};
 struct Ledger {
     int stage = kSetup;
     int64_t occ[2] = {0, 0};
     int64_t peak[4][2] = {};
+    int64_t events_per_stage[4] = {};
     int64_t budget_fast = 0;
+    std::vector<LedgerEvent> events;
+    uint64_t next_id = 1;
+    double t0 = now();
+    static double now();
     void enter(int s);
-    void alloc(int tier, int64_t bytes);
-    void free(int tier, int64_t bytes);
+    uint64_t alloc(int tier, int64_t bytes);
+    void free(int tier, int64_t bytes, uint64_t id);
+    void record(int kind, int tier, int64_t bytes, uint64_t id);
 };
 
 struct DevBuf {
@@ -42,6 +64,7 @@ struct DevBuf {
     int64_t bytes = 0;
     Ledger* ledger = nullptr;
     int tier = 0;  // 0 device, 1 pinned host
+    uint64_t id = 0;  // ledger allocation id
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
