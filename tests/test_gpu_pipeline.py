@@ -239,3 +239,51 @@ def test_full_shape_frame0_equals_single_frame_run(ctx, shape):
     # physical cache: fp16 U_{m+1} before the upsample = 1/8 of the fp32 geometry
     assert rep["cache_bytes_physical"] * 8 == cb
     assert np.isfinite(vT).all()
+
+
+# ------------------------------------------------ memory ledger (§8 f1)
+def _peaks(rep):
+    return {s: rep["peaks"][s]["fast"] for s in ("setup", "encode", "denoise", "decode")}
+
+
+def test_budget_split_aborts_in_decode():
+    """Acceptance C10 (proj/tests/acceptance_main.cpp:447-478) on the
+    physical HBM ledger: a fast-tier budget between the sliced run's
+    overall peak and the unsliced decode peak lets the sliced run through
+    and aborts the unsliced one in the decode stage (each run on a fresh
+    engine, as each reference run has a fresh ledger)."""
+    over = dict(TINY, **{"run.frames": 12, "swap.mode": "sync"})
+
+    def fresh_run(extra):
+        c = lc.Context(0)
+        try:
+            c.configure(lc.config_text(dict(over, **extra), base=DEFAULT))
+            return c.run_pipeline()[2]
+        finally:
+            c.close()
+
+    opt, fat = fresh_run({}), fresh_run({"decode.sliced": "false"})
+    opt_peak = max(_peaks(opt).values())
+    fat_decode = _peaks(fat)["decode"]
+    assert fat_decode > opt_peak
+    budget = (opt_peak + fat_decode) // 2
+    fresh_run({"budget.fast_bytes": budget})
+    with pytest.raises(lc.BudgetError, match="stage decode"):
+        fresh_run({"decode.sliced": "false", "budget.fast_bytes": budget})
+
+
+def test_slicing_changes_only_the_decode_peak(ctx):
+    """Acceptance C6's slicing row (acceptance_main.cpp:322-327): -slicing
+    raises the decode peak and leaves the denoise peak alone."""
+    over = dict(TINY, **{"run.frames": 12})
+    c1, c2 = lc.Context(0), lc.Context(0)
+    try:
+        c1.configure(lc.config_text(over, base=DEFAULT))
+        _, _, on = c1.run_pipeline()
+        c2.configure(lc.config_text(dict(over, **{"decode.sliced": "false"}), base=DEFAULT))
+        _, _, off = c2.run_pipeline()
+    finally:
+        c1.close()
+        c2.close()
+    assert _peaks(off)["decode"] > _peaks(on)["decode"]
+    assert _peaks(off)["denoise"] == _peaks(on)["denoise"]
