@@ -16,7 +16,7 @@ import paper_2510_05367_b200 as lc  # noqa: E402
 GOLD = os.path.join(ROOT, "tests", "golden")
 out = {}
 ctx = lc.Context(0)
-for name in ["tiny", "tiny_ancestral", "tiny_ddim_m1", "tiny_halo_none", "tiny_k5", "default", "config_a",
+for name in ["tiny", "tiny_ancestral", "tiny_ddim_m1", "tiny_halo_none", "tiny_k5", "tiny_image", "default", "config_a",
              "b_frame0", "c_frame0"]:
     g = np.load(os.path.join(GOLD, f"{name}.npz"))
     text = str(g["config"])

@@ -1,0 +1,19 @@
+#!/bin/bash
+# Round profile refresh (run on the GPU box from the repo root via gpurun):
+# bench lines (B, C, reference arm), parity, ncu launch lists (B with DRAM
+# bytes, C) and one `ncu --set full` capture of the top conv launch of B.
+# Outputs land in gpurun_out/; tools/collect_profiles.py copies the
+# summaries into profiles/.
+set -x
+mkdir -p gpurun_out
+python bench.py > gpurun_out/bench_b.json 2> gpurun_out/bench_b.err
+python bench.py --workload C > gpurun_out/bench_c.json 2> gpurun_out/bench_c.err
+python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+python tools/parity_report.py > gpurun_out/parity.json 2> gpurun_out/parity.err
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file gpurun_out/launch_b.csv python tools/profile_step.py B 3 > gpurun_out/ncu_b.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/launch_c.csv python tools/profile_step.py C 2 > gpurun_out/ncu_c.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:conv_tc --launch-skip ${TOPIDX:-115} --launch-count 1 \
+    -o gpurun_out/full_top python tools/profile_step.py B 3 > gpurun_out/ncu_full.log 2>&1
+ls -la gpurun_out
