@@ -38,8 +38,14 @@ namespace {
 
 constexpr int kBM = 128;           // UMMA M per CTA (pixels per tile, padded)
 constexpr int kBK = 64;            // K elements per stage (one 128 B row per pixel)
-constexpr int kThreads = 320;      // w0 TMA, w1 MMA+TMEM, w2..w9 epilogue
-constexpr int kEpiWarps = 8;
+#ifndef LC_EPI_WARPS
+#define LC_EPI_WARPS 16
+#endif
+constexpr int kEpiWarps = LC_EPI_WARPS;             // epilogue warps: 4 TMEM lane quarters x kEpiGroups
+constexpr int kEpiGroups = kEpiWarps / 4;           // warps sharing one lane quarter (column groups)
+constexpr int kChunks = kEpiWarps >= 16 ? 1 : 2;    // 16-column chunks per TMEM wait (register budget)
+constexpr int kPair = 16 * kEpiGroups;              // column distance of a warp's consecutive chunks
+constexpr int kThreads = 64 + kEpiWarps * 32;       // w0 TMA, w1 MMA+TMEM, w2.. epilogue
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr uint32_t kABytes = kBM * kBK * 2;  // 16 KB
 constexpr int kSmemMax = 232448;             // 227 KB opt-in dynamic shared memory
@@ -64,13 +70,17 @@ __host__ __device__ inline int tab_floats(int rc, int bn) {
 
 // one staged TMA-store box: 32 px x 16 channels (fp32 raw or fp16)
 __host__ __device__ inline int stage_chunk(int wide) { return wide ? 2048 : 1024; }
+// TMA-store staging slots per epilogue warp: one per chunk of a TMEM wait,
+// or (one chunk per wait, fp32 raw output) a 2-slot ring so the next box is
+// staged while the previous one is still being read by the TMA unit
+__host__ __device__ inline int stage_slots(int wide) { return (kChunks == 2 || wide) ? 2 : 1; }
 // offset tables: double-buffered, single with a weight-stationary schedule
 // (one (parity, N tile) slab per CTA)
 __host__ __device__ inline int tab_bytes(int tabf, int b_res) { return (b_res ? 1 : 2) * tabf * 4; }
 __host__ __device__ inline int epi_smem_bytes(int tabf, int tma_out, int wide, int b_res) {
     // offset tables, then (1024-aligned) the TMA-store staging (2 boxes per epilogue warp)
     const int tb = tab_bytes(tabf, b_res);
-    return tma_out ? ((tb + 1023) & ~1023) + kEpiWarps * 2 * stage_chunk(wide) : tb;
+    return tma_out ? ((tb + 1023) & ~1023) + kEpiWarps * stage_slots(wide) * stage_chunk(wide) : tb;
 }
 
 // ring stages: A + B per stage, or A only with a resident weight panel of
@@ -158,7 +168,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool b_res = CG == 1 && p.b_res;
     const int tabf = tab_floats(p.rc, p.BN);
     const int stages = num_stages<CG>(p.BN, tabf, p.tma_out, b_res, total_kb, p.nhwc32);
+    // fp32 raw (tap-to-N) epilogues need no offset registers: two chunks per wait
+    constexpr int kCh = EPI == kEpiF32Raw ? 2 : kChunks;
     const int schunk = stage_chunk(p.nhwc32);
+    const int slots = stage_slots(p.nhwc32);
+    const bool ring = kCh == 1 && slots == 2;
     const int bn_cta = p.BN / CG;  // B rows staged by this CTA
     const uint32_t b_bytes = static_cast<uint32_t>(bn_cta) * kBK * 2;
     uint8_t* smA = smem;
@@ -363,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------ epilogue warps
         const int et = threadIdx.x - 64;  // 0..255
         const int q = warp & 3;           // TMEM lane quarter this warp may access
-        const int eh = (warp - 2) >> 2;   // column half: two warps per lane quarter
+        const int eg = (warp - 2) >> 2;   // column group: kEpiGroups warps per lane quarter
         const int m = q * 32 + lane;
         const int tile_px = p.TH * p.TW;
         const int li = m / tile_px;
@@ -399,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         int acc = 0;
         uint32_t acc_phase = 0;
+        uint32_t stage_it = 0;  // TMA-store staging ring position
         for (int u = unit0; u < total_units; u += unit_step) {
             const TileCoord tc = coord(u);
             bool next_switch = false;
@@ -460,20 +475,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t t_row = tmem_base + acc * acc_stride + (static_cast<uint32_t>(q * 32) << 16);
-            // this warp owns the 16-column chunks eh, eh+2, eh+4, ...; two
-            // TMEM loads in flight per wait
-            for (int c00 = 16 * eh; c00 < p.BN; c00 += 64) {
-                const bool two = c00 + 32 < p.BN;
-                uint32_t vv[32];
+            // this warp owns the 16-column chunks eg, eg+G, eg+2G, ... (G =
+            // kEpiGroups); two TMEM loads in flight per wait
+            for (int c00 = 16 * eg; c00 < p.BN; c00 += kCh * kPair) {
+                const bool two = kCh == 2 && c00 + kPair < p.BN;
+                uint32_t vv[16 * kCh];
                 tmem_ld16(t_row + c00, *reinterpret_cast<uint32_t(*)[16]>(&vv[0]));
-                if (two) tmem_ld16(t_row + c00 + 32, *reinterpret_cast<uint32_t(*)[16]>(&vv[16]));
+                if (two) tmem_ld16(t_row + c00 + kPair, *reinterpret_cast<uint32_t(*)[16]>(&vv[16 * (kCh - 1)]));
                 // offsets hs * (bias + o * corr[class]) for the two chunks
-                float offv[32];
+                float offv[16 * kCh];
 #pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
+                for (int hh = 0; hh < kCh; ++hh) {
                     if (hh == 1 && !two) break;
                     if (EPI == kEpiF32Raw) break;
-                    const int c0 = c00 + 32 * hh;
+                    const int c0 = c00 + kPair * hh;
                     if (tabf) {
 #pragma unroll
                         for (int j = 0; j < 16; j += 4)
@@ -488,19 +503,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_ld_wait();
                 if (kTma && p.tma_out) {
                     // the previous chunk pair's stores have finished reading the staging buffers
-                    if (lane == 0) bulk_wait_read0();
+                    if (lane == 0) {
+                        if (ring) bulk_wait_read1();
+                        else bulk_wait_read0();
+                    }
                     __syncwarp();
                 }
 #pragma unroll
-                for (int hh = 0; hh < 2; ++hh) {
+                for (int hh = 0; hh < kCh; ++hh) {
                     if (hh == 1 && !two) break;
                     const uint32_t* v = vv + 16 * hh;
                     const float* off = offv + 16 * hh;
-                    const int nb = tc.n_tile * p.BN + c00 + 32 * hh;
+                    const int nb = tc.n_tile * p.BN + c00 + kPair * hh;
                     if (EPI == kEpiF32Raw) {
                         if (p.tma_out) {
                             const uint32_t sb =
-                                stage_out_s + static_cast<uint32_t>(((warp - 2) * 2 + hh) * schunk + lane * 64);
+                                stage_out_s + static_cast<uint32_t>(((warp - 2) * slots + (ring ? (stage_it & 1) : hh)) * schunk + lane * 64);
 #pragma unroll
                             for (int j = 0; j < 16; j += 4)
                                 sts128(sb + 4 * j, make_float4(__uint_as_float(v[j]) * hscale,
@@ -559,7 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             h[j / 2] = __floats2half2_rn(a, b);
                         }
                         if (p.tma_out) {
-                            const uint32_t sb = stage_out_s + static_cast<uint32_t>(((warp - 2) * 2 + hh) * schunk + lane * 32);
+                            const uint32_t sb = stage_out_s + static_cast<uint32_t>(((warp - 2) * slots + (ring ? (stage_it & 1) : hh)) * schunk + lane * 32);
                             sts128u(sb, *reinterpret_cast<uint4*>(&h[0]));
                             sts128u(sb + 16, *reinterpret_cast<uint4*>(&h[4]));
                         } else {
@@ -577,11 +595,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                     if (lane == 0 && warp_store) {
                         const int nb0 = tc.n_tile * p.BN + c00;
-                        const uint32_t sb = stage_out_s + static_cast<uint32_t>((warp - 2) * 2 * schunk);
+                        const uint32_t sb = stage_out_s + static_cast<uint32_t>(((warp - 2) * slots + (ring ? (stage_it & 1) : 0)) * schunk);
                         if (nb0 < p.cs_out) tma_store_4d(&p.tmO[tc.parity], sb, nb0, bx, by, bi);
-                        if (two && nb0 + 32 < p.cs_out) tma_store_4d(&p.tmO[tc.parity], sb + schunk, nb0 + 32, bx, by, bi);
+                        if (two && nb0 + kPair < p.cs_out)
+                            tma_store_4d(&p.tmO[tc.parity], sb + schunk, nb0 + kPair, bx, by, bi);
                         bulk_commit();
                     }
+                    ++stage_it;
                 }
             }
             // release the accumulator buffer to the MMA warp (the leader's barrier)
