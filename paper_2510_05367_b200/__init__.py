@@ -92,7 +92,7 @@ I64 = ctypes.c_int64
 EXPORTS = [
     "lc_version", "lc_last_error", "lc_ctx_create", "lc_ctx_destroy", "lc_config_check",
     "lc_config_to_text", "lc_configure", "lc_latent_elems", "lc_video_elems", "lc_run_pipeline",
-    "lc_upload_latent", "lc_run_resident", "lc_run_resident_async", "lc_wait", "lc_download_video",
+    "lc_upload_latent", "lc_run_resident", "lc_run_resident_async", "lc_run_pipeline_async", "lc_wait", "lc_download_video",
     "lc_set_decode_slice",
     "lc_forward", "lc_decode", "lc_video_metrics", "lc_ledger_csv", "lc_ledger_summary", "lc_conv2d", "lc_up_conv2d", "lc_plan_steps", "lc_split",
     "lc_model_numbers", "lc_derive_seed", "lc_randn", "lc_shard_frames", "lc_nccl_unique_id",
@@ -270,6 +270,11 @@ class Context:
     def run_resident_async(self) -> None:
         """Queue one resident run (graph replay) without waiting; see wait()."""
         _check(lib().lc_run_resident_async(self._h))
+
+    def run_e2e_async(self, x0_pinned: "PinnedArray", video_pinned: "PinnedArray") -> None:
+        """Queue one run with pinned host input/output (H2D + D2H inside);
+        consecutive runs overlap compute with the previous video download."""
+        _check(lib().lc_run_pipeline_async(self._h, x0_pinned.ptr, video_pinned.ptr))
 
     def wait(self) -> dict:
         """Complete the queued resident runs; report of the last one."""

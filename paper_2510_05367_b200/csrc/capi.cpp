@@ -170,6 +170,9 @@ int lc_run_resident(lc_ctx* ctx, char* report, int64_t cap) {
 int lc_run_resident_async(lc_ctx* ctx) {
     return guarded([&] { ctx->engine.run_resident_async(); });
 }
+int lc_run_pipeline_async(lc_ctx* ctx, const float* x0, float* video) {
+    return guarded([&] { ctx->engine.run_e2e_async(x0, video); });
+}
 int lc_wait(lc_ctx* ctx, char* report, int64_t cap) {
     return guarded([&] {
         const lc::RunStats st = ctx->engine.wait();

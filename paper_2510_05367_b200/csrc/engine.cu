@@ -621,6 +621,7 @@ Engine::Engine(int device) : device_(device) {
     for (int b = 0; b < 2; ++b) LC_CUDA(cudaEventCreateWithFlags(&ev_cache_ready_[b], cudaEventDisableTiming));
     LC_CUDA(cudaEventCreate(&ev_start_));
     for (int b = 0; b < 2; ++b) LC_CUDA(cudaEventCreateWithFlags(&ev_join_[b], cudaEventDisableTiming));
+    LC_CUDA(cudaEventCreateWithFlags(&ev_vid_done_, cudaEventDisableTiming));
     if (const char* e = std::getenv("LC_NO_GRAPH")) use_graphs = (e[0] == '0');
 }
 
@@ -637,6 +638,7 @@ Engine::~Engine() {
     for (int b = 0; b < 2; ++b) cudaEventDestroy(ev_cache_ready_[b]);
     cudaEventDestroy(ev_start_);
     for (int b = 0; b < 2; ++b) cudaEventDestroy(ev_join_[b]);
+    cudaEventDestroy(ev_vid_done_);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
     cudaStreamDestroy(s_compute_);
     cudaStreamDestroy(s_d2h_);
@@ -1264,6 +1266,14 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
     }
     const int C = static_cast<int>(cfg_.latent_channels), IC = static_cast<int>(cfg_.image_channels);
     const int H = static_cast<int>(cfg_.height), W = static_cast<int>(cfg_.width);
+    if (out_slices_) {
+        // the previous run's video download must have read the device video
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        LC_CUDA(cudaStreamIsCapturing(s_compute_, &cs));
+        LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_vid_done_,
+                                    cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
+        slice_spans_.clear();
+    }
     for (int64_t g0 = 0; g0 < n; g0 += G) {
         const int gs = static_cast<int>(std::min<int64_t>(G, n - g0));
         Act e[8];
@@ -1336,18 +1346,29 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
                         s_compute_, video_dev + g0 * IC * H * W, IC);
             ++launches;
         }
-        if (video_host_pinned_) {
-            // stream this slice's frames to the caller's pinned buffer while
-            // the next slice decodes (D2H copy stream, event-ordered)
-            cudaEvent_t ev = chunk_event(2, static_cast<size_t>(g0 / G));
-            LC_CUDA(cudaEventRecord(ev, s_compute_));
-            LC_CUDA(cudaStreamWaitEvent(s_d2h_, ev, 0));
-            const int64_t frame = static_cast<int64_t>(IC) * H * W;
-            LC_CUDA(cudaMemcpyAsync(video_host_pinned_ + g0 * frame, video_dev + g0 * frame,
-                                    static_cast<size_t>(gs * frame) * 4, cudaMemcpyDeviceToHost, s_d2h_));
-            d2h_used_ = true;
+        if (out_slices_) {
+            // slice g0 is final: the host side streams it to the caller's
+            // pinned buffer on the D2H stream (enqueue_video_out), outside
+            // the captured body, while the next slice decodes
+            record_timing(chunk_event(2, slice_spans_.size()), s_compute_);
+            slice_spans_.push_back({g0, gs});
         }
     }
+}
+
+// After a body launch: per decoded slice, wait for its event and copy it to
+// the caller's pinned buffer on the D2H stream; ev_vid_done_ marks the last
+// byte read, and the next body's decode waits for it before overwriting the
+// device video (so back-to-back runs may overlap this download).
+void Engine::enqueue_video_out(float* pinned) {
+    const int64_t frame = static_cast<int64_t>(cfg_.image_channels) * cfg_.height * cfg_.width;
+    for (size_t i = 0; i < slice_spans_.size(); ++i) {
+        LC_CUDA(cudaStreamWaitEvent(s_d2h_, chunk_event(2, i), 0));
+        const int64_t g0 = slice_spans_[i].first, gs = slice_spans_[i].second;
+        LC_CUDA(cudaMemcpyAsync(pinned + g0 * frame, video_.as<float>() + g0 * frame,
+                                static_cast<size_t>(gs * frame) * 4, cudaMemcpyDeviceToHost, s_d2h_));
+    }
+    LC_CUDA(cudaEventRecord(ev_vid_done_, s_d2h_));
 }
 
 void Engine::ensure_buf(DevBuf* b, int64_t bytes) {
@@ -1573,7 +1594,9 @@ void Engine::enqueue_body(RunStats& st) {
     x_final_ = xa;
     record_timing(ev_den1_, s_compute_);
     ledger_.enter(kDecode);
+    out_slices_ = true;
     decode_dev(xa, T, video_.as<float>());
+    out_slices_ = false;
     // join the copy streams that were used (required to close a graph
     // capture; the last eviction stays in flight through decode as in the
     // reference, proj/README.md "Swap schedule")
@@ -1638,8 +1661,7 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
             pinned = video_host;
         cudaGetLastError();  // clear a "not a CUDA pointer" status for pageable memory
     }
-    if (graph_exec_ && (graph_slice_ != decode_slice || graph_video_ != pinned)) invalidate_graph();
-    graph_video_ = pinned;
+    if (graph_exec_ && graph_slice_ != decode_slice) invalidate_graph();
     video_host_pinned_ = pinned;
     graph_slice_ = decode_slice;
     if (can_graph && graph_exec_) {
@@ -1665,8 +1687,28 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
         enqueue_body(st);
         ++eager_runs_;
     }
+    if (pinned) enqueue_video_out(pinned);
     ledger_.enter(kDecode);
     return finish_run(st, video_host, latent_host);
+}
+
+// Throughput form of run() with pinned host buffers: H2D of the latent, the
+// graph, and the per-slice video download are queued without a host round
+// trip, so run k+1's denoise overlaps run k's download; wait() completes.
+void Engine::run_e2e_async(const float* x0_pinned, float* video_pinned) {
+    const bool ready = use_graphs && conv_profiler() == nullptr && graph_exec_ && graph_slice_ == decode_slice &&
+                       T_alloc_ == cfg_.frames && cfg_.mode != "image";
+    if (!ready) {
+        last_async_ = run(x0_pinned, video_pinned, nullptr, false);
+        async_pending_ = false;
+        return;
+    }
+    LC_CUDA(cudaEventRecord(ev_start_, s_compute_));
+    LC_CUDA(cudaMemcpyAsync(x_.p, x0_pinned, static_cast<size_t>(latent_elems()) * 4, cudaMemcpyHostToDevice,
+                            s_compute_));
+    LC_CUDA(cudaGraphLaunch(graph_exec_, s_compute_));
+    enqueue_video_out(video_pinned);
+    async_pending_ = true;
 }
 
 // Steady-state resident replay without the host round trip: enqueue the
@@ -1675,8 +1717,8 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
 // never overlap); wait() completes the last one.  Before the graph exists
 // (first two runs after a (re)configuration) this is a synchronous run().
 void Engine::run_resident_async() {
-    const bool ready = use_graphs && conv_profiler() == nullptr && graph_exec_ && graph_video_ == nullptr &&
-                       graph_slice_ == decode_slice && T_alloc_ == cfg_.frames;
+    const bool ready = use_graphs && conv_profiler() == nullptr && graph_exec_ && graph_slice_ == decode_slice &&
+                       T_alloc_ == cfg_.frames;
     if (!ready) {
         last_async_ = run(nullptr, nullptr, nullptr, true);
         async_pending_ = false;

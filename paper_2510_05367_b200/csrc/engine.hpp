@@ -187,6 +187,7 @@ public:
     // Throughput loops: enqueue one resident run (graph replay) without
     // waiting; wait() completes the queued runs and reports the last one.
     void run_resident_async();
+    void run_e2e_async(const float* x0_pinned, float* video_pinned);
     RunStats wait();
 
     // Operator-level entry points (for unit parity).
@@ -308,12 +309,15 @@ private:
     bool d2h_used_ = false, h2d_used_ = false;
     cudaEvent_t ev_start_ = nullptr, ev_den0_ = nullptr, ev_den1_ = nullptr, ev_end_ = nullptr;
     cudaEvent_t ev_join_[2] = {nullptr, nullptr};
+    cudaEvent_t ev_vid_done_ = nullptr;               // last video byte downloaded (see enqueue_video_out)
+    bool out_slices_ = false;                         // decode_dev inside the run body
+    std::vector<std::pair<int64_t, int64_t>> slice_spans_;  // decoded slices (first frame, frames)
+    void enqueue_video_out(float* pinned);
     float* x_final_ = nullptr;
     cudaGraphExec_t graph_exec_ = nullptr;
     RunStats graph_stats_;
     int eager_runs_ = 0;
     int64_t graph_slice_ = -1;
-    float* graph_video_ = nullptr;        // pinned video destination baked into the graph
     float* video_host_pinned_ = nullptr;  // current run's pinned destination (or null)
     std::string z_key_;
     std::vector<cudaEvent_t> ev_chunk_[3];  // [0,1] swap chunks per branch, [2] decoded slices

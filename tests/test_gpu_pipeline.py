@@ -196,6 +196,16 @@ def test_graph_replay_is_bit_identical(ctx, oracle, kind, extra):
         vid.array[:] = -1.0
         ctx.run_e2e(x0, vid)
         assert np.array_equal(vid.array.reshape(outs[0][0].shape), outs[0][0])
+    # queued pinned runs: each download overlaps the next run's compute
+    vid2 = lc.PinnedArray(ctx.video_elems())
+    vid.array[:] = -1.0
+    vid2.array[:] = -1.0
+    for k in range(4):
+        ctx.run_e2e_async(x0, vid if k % 2 == 0 else vid2)
+    ctx.wait()
+    assert np.array_equal(vid.array.reshape(outs[0][0].shape), outs[0][0])
+    assert np.array_equal(vid2.array.reshape(outs[0][0].shape), outs[0][0])
+    vid2.free()
     x0.free()
     vid.free()
 
