@@ -184,42 +184,56 @@ __global__ void patch_kernel(const ThinInArgs a, int kp) {
     }
 }
 
-// Fast path of the patch gather: 3x3 taps, kp == 64 (c_in <= 7).  Block =
-// 32 pixels of one output row x 8 tap groups, so a warp writes 4 pixels x
-// 128 B contiguous and all index math is 32-bit with constant divisors.
+// Fast path of the patch gather: 3x3 taps, kp == 64, c_in = CIN (<= 7).
+// One thread per output pixel: the 3 x 3 x CIN neighbourhood (row / column
+// validity computed once), conditioned with the reference roundings, written
+// as one 128-byte fp16 patch row (taps past CIN*9 are zero).  Consecutive
+// threads walk x, so every tap load is coalesced.
+template <int CIN>
 __global__ void __launch_bounds__(256) patch3_kernel(const ThinInArgs a) {
     pdl_wait();
-    constexpr int K = 3, KK = 9;
-    const int g = threadIdx.x & 7;
-    const int oh = a.win.oy1 - a.win.oy0;
-    const int ox = a.win.ox0 + static_cast<int>(blockIdx.x) * 32 + (threadIdx.x >> 3);
-    const int row = static_cast<int>(blockIdx.y);
+    const int ow = a.win.ox1 - a.win.ox0, oh = a.win.oy1 - a.win.oy0;
+    const int idx = static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int nimg = a.cfg_pair ? 2 * a.nsrc : a.nsrc;
+    if (idx >= nimg * oh * ow) return;
+    const int row = idx / ow;
+    const int ox = a.win.ox0 + (idx - row * ow);
     const int n = row / oh;
     const int oy = a.win.oy0 + (row - n * oh);
-    if (ox >= a.win.ox1) return;
     const int src = n % a.nsrc;
     const bool branch1 = a.cfg_pair && n >= a.nsrc;
-    const float* xs = a.x + static_cast<size_t>(src) * a.c_in * a.H * a.W;
-    const int KKc = a.c_in * KK;
-    __align__(16) __half h[8];
+    const size_t plane = static_cast<size_t>(a.H) * a.W;
+    const float* xs = a.x + static_cast<size_t>(src) * CIN * plane;
+    bool rv[3], cv[3];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const int t = g * 8 + j;
-        float v = 0.0f;
-        if (t < KKc) {
-            const int ic = t / KK, rem = t - ic * KK;
-            const int ky = rem / K, kx = rem - ky * K;
-            const int iy = oy + ky - 1, ix = ox + kx - 1;
-            if (iy >= a.win.vy0 && iy < a.win.vy1 && ix >= a.win.vx0 && ix < a.win.vx1) {
-                v = __ldg(xs + (static_cast<size_t>(ic) * a.H + iy) * a.W + ix);
-                if (branch1) v = __fadd_rn(v, a.cond_bias);
-                if (a.apply_affine) v = __fadd_rn(__fmul_rn(v, a.s), a.o);
-            }
-        }
-        h[j] = __float2half_rn(v);
+    for (int d = 0; d < 3; ++d) {
+        rv[d] = oy + d - 1 >= a.win.vy0 && oy + d - 1 < a.win.vy1;
+        cv[d] = ox + d - 1 >= a.win.vx0 && ox + d - 1 < a.win.vx1;
     }
-    *reinterpret_cast<uint4*>(a.out + ((static_cast<size_t>(n) * a.H + oy) * a.W + ox) * 64 + g * 8) =
-        *reinterpret_cast<const uint4*>(h);
+    float v[64];
+#pragma unroll
+    for (int t = 0; t < 64; ++t) v[t] = 0.0f;
+#pragma unroll
+    for (int ic = 0; ic < CIN; ++ic)
+#pragma unroll
+        for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+            for (int kx = 0; kx < 3; ++kx) {
+                if (rv[ky] && cv[kx]) {
+                    float x = __ldg(xs + ic * plane + static_cast<size_t>(oy + ky - 1) * a.W + (ox + kx - 1));
+                    if (branch1) x = __fadd_rn(x, a.cond_bias);
+                    if (a.apply_affine) x = __fadd_rn(__fmul_rn(x, a.s), a.o);
+                    v[(ic * 3 + ky) * 3 + kx] = x;
+                }
+            }
+    uint4* dst = reinterpret_cast<uint4*>(a.out + ((static_cast<size_t>(n) * a.H + oy) * a.W + ox) * 64);
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+        __align__(16) __half2 h[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) h[j] = __floats2half2_rn(v[8 * g + 2 * j], v[8 * g + 2 * j + 1]);
+        dst[g] = *reinterpret_cast<const uint4*>(h);
+    }
 }
 
 // ------------------------------------------------------- tap gathers
@@ -558,10 +572,22 @@ cudaError_t launch_patch(const ThinInArgs& a, int kp, cudaStream_t st) {
     const int64_t work =
         static_cast<int64_t>(nimg) * (a.win.oy1 - a.win.oy0) * (a.win.ox1 - a.win.ox0) * (kp / 8);
     const int rows = nimg * (a.win.oy1 - a.win.oy0);
-    if (a.k == 3 && kp == 64 && a.c_in * 9 <= 64 && rows < 65536) {
-        const dim3 grid((a.win.ox1 - a.win.ox0 + 31) / 32, rows);
-        if (grid.x > 0 && rows > 0) return launch_pdl(patch3_kernel, grid, dim3(256), 0, st, a);
-        return cudaGetLastError();
+    if (a.k == 3 && kp == 64 && a.c_in * 9 <= 64) {
+        const int64_t px = static_cast<int64_t>(rows) * (a.win.ox1 - a.win.ox0);
+        if (px <= 0) return cudaSuccess;
+        // small launches (a decoder slice): narrower blocks to fill the SMs
+        const int tb = px < 4 * 148 * 256 ? 64 : 256;
+        const dim3 grid(static_cast<unsigned>((px + tb - 1) / tb)), blk(tb);
+        switch (a.c_in) {
+            case 1: return launch_pdl(patch3_kernel<1>, grid, blk, 0, st, a);
+            case 2: return launch_pdl(patch3_kernel<2>, grid, blk, 0, st, a);
+            case 3: return launch_pdl(patch3_kernel<3>, grid, blk, 0, st, a);
+            case 4: return launch_pdl(patch3_kernel<4>, grid, blk, 0, st, a);
+            case 5: return launch_pdl(patch3_kernel<5>, grid, blk, 0, st, a);
+            case 6: return launch_pdl(patch3_kernel<6>, grid, blk, 0, st, a);
+            case 7: return launch_pdl(patch3_kernel<7>, grid, blk, 0, st, a);
+            default: break;
+        }
     }
     return launch_pdl(patch_kernel, dim3(grid_for(work, 256)), dim3(256), 0, st, a, kp);
 }
