@@ -130,26 +130,27 @@ __device__ __forceinline__ TileCoord tile_coord(const ConvParams& p, int u, int 
     // Weight-heavy layers (deep up blocks: up to 170 MB of per-parity
     // weights): M fastest, so one weight slab is streamed by all CTAs.
     TileCoord c;
-    const int P = p.nparity;
     int mu;
     if (p.m_fastest) {
-        mu = u % m_units;
-        const int rest = u / m_units;
-        c.n_tile = rest % n_tiles;
-        c.parity = rest / n_tiles;
+        const int rest = p.fd_units.div(u);
+        mu = u - rest * static_cast<int>(p.fd_units.d);
+        c.parity = p.fd_ntiles.div(rest);
+        c.n_tile = rest - c.parity * static_cast<int>(p.fd_ntiles.d);
     } else {
-        c.n_tile = u % n_tiles;
-        const int rest = u / n_tiles;
-        c.parity = rest % P;
-        mu = rest / P;
+        const int rest = p.fd_ntiles.div(u);
+        c.n_tile = u - rest * static_cast<int>(p.fd_ntiles.d);
+        mu = p.fd_par.div(rest);
+        c.parity = rest - mu * static_cast<int>(p.fd_par.d);
     }
+    (void)m_units;
+    (void)n_tiles;
     int mt = mu * CG + rank;
     c.live = mt < m_tiles;
     if (!c.live) mt = m_tiles - 1;  // keep coordinates sane; results are discarded
-    const int tx = mt % p.tiles_x;
-    mt /= p.tiles_x;
-    const int ty = mt % p.tiles_y;
-    const int ti = mt / p.tiles_y;
+    const int r1 = p.fd_tx.div(mt);
+    const int tx = mt - r1 * static_cast<int>(p.fd_tx.d);
+    const int ti = p.fd_ty.div(r1);
+    const int ty = r1 - ti * static_cast<int>(p.fd_ty.d);
     c.X0 = p.lx0[c.parity] + tx * p.TW;
     c.Y0 = p.ly0[c.parity] + ty * p.TH;
     c.I0 = ti * p.TI;
@@ -188,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tab_s = smem_u32(smB + b_blocks * b_bytes + 256);
     const uint32_t stage_out_s = tab_s + ((tab_bytes(tabf, b_res) + 1023) & ~1023);
 
-    const int warp = threadIdx.x / 32;
+    const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x) / 32, 0);  // warp-uniform
     const int lane = threadIdx.x % 32;
     const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
     const bool leader = rank == 0;
@@ -215,8 +216,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         c.parity = slab_par;
         c.n_tile = slab_nt;
         c.live = true;
-        const int tx = u % p.tiles_x, rest = u / p.tiles_x;
-        const int ty = rest % p.tiles_y, ti = rest / p.tiles_y;
+        const int rest = p.fd_tx.div(u);
+        const int tx = u - rest * p.tiles_x;
+        const int ti = p.fd_ty.div(rest);
+        const int ty = rest - ti * p.tiles_y;
         c.X0 = p.lx0[c.parity] + tx * p.TW;
         c.Y0 = p.ly0[c.parity] + ty * p.TH;
         c.I0 = ti * p.TI;
@@ -661,7 +664,16 @@ size_t smem_bytes_for(const ConvParams& p) {
 int g_cta_group_override = -1;  // LC_CTA_GROUP env: 1 or 2 forces the variant
 
 template <int CG, int EPI>
-cudaError_t launch_variant(const ConvParams& p, int parities, cudaStream_t stream) {
+cudaError_t launch_variant(const ConvParams& p0, int parities, cudaStream_t stream) {
+    ConvParams p = p0;
+    {
+        const int m_tiles = p.tiles_x * p.tiles_y * p.tiles_i;
+        p.fd_units.init(static_cast<uint32_t>((m_tiles + CG - 1) / CG));
+        p.fd_ntiles.init(static_cast<uint32_t>(p.n_pad / p.BN));
+        p.fd_par.init(static_cast<uint32_t>(p.nparity));
+        p.fd_tx.init(static_cast<uint32_t>(p.tiles_x));
+        p.fd_ty.init(static_cast<uint32_t>(p.tiles_y));
+    }
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e =

@@ -39,6 +39,26 @@ struct ConvSegDev {
     int8_t oy[4][kMaxTaps];
 };
 
+// n / d and n % d for 0 <= n < 2^31 with one multiply-high (round-up
+// magic number, set on the host): the per-tile schedule math runs on every
+// epilogue warp, and 32-bit integer division is ~20 instructions.
+struct FastDiv {
+    uint32_t d = 1, m = 0, s = 0;
+    void init(uint32_t div) {
+        d = div;
+        s = 0;
+        while ((1ull << s) < div) ++s;
+        m = static_cast<uint32_t>((((1ull << 32) * ((1ull << s) - div)) / div) + 1);
+        if (div == 1) m = 0;
+    }
+#ifdef __CUDACC__
+    __device__ __forceinline__ int div(int n) const {
+        return static_cast<int>((__umulhi(static_cast<uint32_t>(n), m) + static_cast<uint32_t>(n)) >> s);
+    }
+    __device__ __forceinline__ int mod(int n) const { return n - div(n) * static_cast<int>(d); }
+#endif
+};
+
 struct alignas(64) ConvParams {
     CUtensorMap tmA[2];  // activations, per segment: dims {C, W, H, N}
     CUtensorMap tmB;     // weights: dims {K_total, N_pad, P}
@@ -84,6 +104,7 @@ struct alignas(64) ConvParams {
     // tiles (small-K, small-N layers whose per-tile weight re-reads would
     // otherwise make them L2-bandwidth bound)
     int b_res;
+    FastDiv fd_units, fd_ntiles, fd_par, fd_tx, fd_ty;  // launch-side divisors of tile_coord
 };
 
 // CTA-group choice for a launch (the weight tensor map's box depends on it:

@@ -453,8 +453,7 @@ Bank subpixel_shuffle_bank(const Bank& b) {
 
 void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window& win, float s,
                  float o, bool silu, cudaStream_t st, float* out32, int shuffle_c, bool nhwc32) {
-    ConvParams p;
-    std::memset(&p, 0, sizeof(p));
+    ConvParams p{};
     const int sub = L.mode == 1 ? 2 : 1;
     // per parity class q = (py, px): output pixels 2Y+py in [oy0, oy1)
     int Lh = 0, Lw = 0;
