@@ -386,6 +386,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int li = m / tile_px;
         const int ly = (m / p.TW) % p.TH;
         const int lx = m % p.TW;
+        // this warp's first pixel within a tile (TMA-store box origin)
+        const int m0_x = (q * 32) % p.TW, m0_y = ((q * 32) / p.TW) % p.TH, m0_i = (q * 32) / tile_px;
+        const bool m0_in_tile = q * 32 < p.TI * tile_px;
         const int rr = p.rc + 1;
         const int ncls = rr * rr * rr * rr;
         // SiLU runs on h = x/2: fold the 1/2 into scale and offsets
@@ -440,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     pending = false;
                 }
                 const int un = u + unit_step;
-                if (un < total_units) {
+                if (!b_res && un < total_units) {  // one slab per CTA under b_res: never switches
                     const TileCoord tn = coord(un);
                     next_key = tn.parity * n_tiles + tn.n_tile;
                     if (next_key != cur_key) {
@@ -469,11 +472,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             // relative to the class window, see ConvParams::tmO)
             constexpr bool kF16 = EPI == kEpiF16 || EPI == kEpiF16Silu;
             constexpr bool kTma = kF16 || EPI == kEpiF32Raw;  // epilogues with a TMA-store form
-            const int m0 = q * 32;
-            const bool warp_store = kTma && p.tma_out && tc.live && m0 < p.TI * tile_px && !p.debug_nostore;
-            const int bx = tc.X0 + m0 % p.TW - p.lx0[tc.parity];
-            const int by = tc.Y0 + (m0 / p.TW) % p.TH - p.ly0[tc.parity];
-            const int bi = tc.I0 + m0 / tile_px;
+            const bool warp_store = kTma && p.tma_out && tc.live && m0_in_tile && !p.debug_nostore;
+            const int bx = tc.X0 + m0_x - p.lx0[tc.parity];
+            const int by = tc.Y0 + m0_y - p.ly0[tc.parity];
+            const int bi = tc.I0 + m0_i;
 
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();

@@ -162,10 +162,33 @@ void class_geom(int d_lo, int d_hi, int rc, int* L, int* Y) {
 }  // namespace
 
 // ------------------------------------------------------- layer packing
+// Pixel tile of a launch: TI x TH x TW <= 128 (one UMMA M) with the fewest
+// tiles, i.e. the least padded M; ties keep the widest rows.  Full-width rows
+// first (TW = w), then powers of two.  E.g. the 9x16 lattices of config C
+// (mid, u2): 16x8 tiles leave a 1-row tail per image (56 % useful M); 16x1x8
+// tiles (one row of 8 images) are 89 % useful.
+void choose_tile(int n, int h, int w, int* TW, int* TH, int* TI) {
+    int best = -1, bw = 1, bh = 1, bi = 1;
+    auto consider = [&](int tw) {
+        if (tw < 1 || tw > 128) return;
+        for (int th = std::min(h, 128 / tw); th >= 1; --th) {
+            const int ti = std::max(1, std::min(n, 128 / (tw * th)));
+            const int tiles = ((n + ti - 1) / ti) * ((h + th - 1) / th) * ((w + tw - 1) / tw);
+            if (best < 0 || tiles < best) {
+                best = tiles;
+                bw = tw, bh = th, bi = ti;
+            }
+        }
+    };
+    consider(std::min(w, 128));
+    for (int tw = 128; tw >= 1; tw /= 2)
+        if (tw < std::min(w, 128)) consider(tw);
+    *TW = bw, *TH = bh, *TI = bi;
+}
+
 int est_m_tiles(int n, int h, int w) {
-    const int TW = std::min(w, 128);
-    const int TH = std::max(1, std::min(h, 128 / TW));
-    const int TI = std::max(1, std::min(n, 128 / (TW * TH)));
+    int TW, TH, TI;
+    choose_tile(n, h, w, &TW, &TH, &TI);
     return ((n + TI - 1) / TI) * ((h + TH - 1) / TH) * ((w + TW - 1) / TW);
 }
 
@@ -471,9 +494,7 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
     p.cx0 = win.vx0 / sub;
     p.cx1 = win.vx1 / sub;
     p.n_img = out.n;
-    p.TW = std::min(Lw, 128);
-    p.TH = std::max(1, std::min(Lh, 128 / p.TW));
-    p.TI = std::max(1, std::min(out.n, 128 / (p.TW * p.TH)));
+    choose_tile(out.n, Lh, Lw, &p.TW, &p.TH, &p.TI);
     p.tiles_x = (Lw + p.TW - 1) / p.TW;
     p.tiles_y = (Lh + p.TH - 1) / p.TH;
     p.tiles_i = (out.n + p.TI - 1) / p.TI;
