@@ -98,6 +98,8 @@ int lc_timer_stop(lc_ctx* ctx, float* ms);
 int lc_set_conv_profile(lc_ctx* ctx, int on);
 int lc_conv_profile(lc_ctx* ctx, int64_t* launches, double* ms, double* alg_flops,
                     double* exec_flops);
+/* Per-launch records of the conv profile: JSON [{ms, alg_flops, exec_flops, desc}]. */
+int lc_conv_profile_records(lc_ctx* ctx, char* buf, int64_t cap);
 /* Pinned host buffers for end-to-end copies. */
 void* lc_alloc_pinned(int64_t bytes);
 int lc_free_pinned(void* p);

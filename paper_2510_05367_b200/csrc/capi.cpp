@@ -217,6 +217,9 @@ int lc_set_conv_profile(lc_ctx* ctx, int on) {
 int lc_conv_profile(lc_ctx* ctx, int64_t* launches, double* ms, double* alg, double* exec) {
     return guarded([&] { ctx->prof.summarize(launches, ms, alg, exec); });
 }
+int lc_conv_profile_records(lc_ctx* ctx, char* buf, int64_t cap) {
+    return guarded([&] { put(buf, cap, ctx->prof.records_json()); });
+}
 void* lc_alloc_pinned(int64_t bytes) {
     void* p = nullptr;
     if (cudaHostAlloc(&p, static_cast<size_t>(bytes), cudaHostAllocDefault) != cudaSuccess) {

@@ -616,6 +616,13 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
         r.alg_flops = 2.0 * static_cast<double>(pix) * out.n * L.c_out * L.k * L.k * cin;
         r.exec_flops = 2.0 * static_cast<double>(p.tiles_x) * p.tiles_y * p.tiles_i * L.P * 128.0 *
                        L.n_pad * L.k_total;
+        {
+            const int mt = p.tiles_x * p.tiles_y * p.tiles_i;
+            r.desc = "P" + std::to_string(L.P) + " M" + std::to_string(mt) + "x128 tile " + std::to_string(p.TI) +
+                     "x" + std::to_string(p.TH) + "x" + std::to_string(p.TW) + " N" + std::to_string(L.n_pad) +
+                     "/BN" + std::to_string(L.BN) + " K" + std::to_string(L.k_total) + " cg" + std::to_string(p.cg) +
+                     (out32 ? (nhwc32 ? " raw32" : " f32") : (silu ? " silu" : "")) + (p.tma_out ? " tma" : "");
+        }
         LC_CUDA(cudaEventCreate(&r.e0));
         LC_CUDA(cudaEventCreate(&r.e1));
         LC_CUDA(cudaEventRecord(r.e0, st));
@@ -1154,10 +1161,14 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
 // Swap transfers (TransferEngine evict/prefetch, proj/src/swap.cpp:284-304).
 // One "transfer" = one CFG branch entry (half of the b=2 cache, contiguous
 // since b is the outermost image index).  Each entry moves in chunks of
-// kSwapChunk bytes so the H2D prefetch of chunk i can start as soon as its
+// swap_chunk() bytes (4 MB) so the H2D prefetch of chunk i can start as soon as its
 // D2H eviction lands (PCIe is full duplex); async mode uses dedicated D2H
 // and H2D streams ordered by CUDA events, sync mode serialises on compute.
-static constexpr int64_t kSwapChunk = 4 << 20;
+static int64_t swap_chunk() {
+    static const int64_t c = std::getenv("LC_SWAP_CHUNK_MB") ? std::atoll(std::getenv("LC_SWAP_CHUNK_MB")) << 20
+                                                             : int64_t{4} << 20;
+    return c;
+}
 
 cudaEvent_t Engine::chunk_event(int b, size_t i) {
     while (ev_chunk_[b].size() <= i) {
@@ -1205,8 +1216,8 @@ void Engine::issue_evict(int step) {
         if (stats_) stats_->swap_bytes_moved += bytes;
         record(2, step, bytes, st);
         size_t ci = 0;
-        for (int64_t off = 0; off < bytes; off += kSwapChunk, ++ci) {
-            const int64_t len = std::min(kSwapChunk, bytes - off);
+        for (int64_t off = 0; off < bytes; off += swap_chunk(), ++ci) {
+            const int64_t len = std::min(swap_chunk(), bytes - off);
             LC_CUDA(cudaMemcpyAsync(cache_host_.as<char>() + b * bytes + off,
                                     reinterpret_cast<char*>(cache_.p) + b * bytes + off, static_cast<size_t>(len),
                                     cudaMemcpyDeviceToHost, st));
@@ -1229,8 +1240,8 @@ void Engine::issue_prefetch(int issued, int needed) {
     for (int b = 0; b < 2; ++b) {
         if (async) h2d_used_ = true;
         size_t ci = 0;
-        for (int64_t off = 0; off < bytes; off += kSwapChunk, ++ci) {
-            const int64_t len = std::min(kSwapChunk, bytes - off);
+        for (int64_t off = 0; off < bytes; off += swap_chunk(), ++ci) {
+            const int64_t len = std::min(swap_chunk(), bytes - off);
             if (async) LC_CUDA(cudaStreamWaitEvent(st, chunk_event(b, ci), 0));
             if (ci == 0) record(2, needed, bytes, st);  // start = first byte can move
             LC_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(cache_.p) + b * bytes + off,
@@ -1971,6 +1982,19 @@ void ConvProfiler::clear() {
         cudaEventDestroy(r.e1);
     }
     recs.clear();
+}
+
+std::string ConvProfiler::records_json() const {
+    std::string o = "[";
+    for (size_t i = 0; i < recs.size(); ++i) {
+        float t = 0;
+        LC_CUDA(cudaEventSynchronize(recs[i].e1));
+        LC_CUDA(cudaEventElapsedTime(&t, recs[i].e0, recs[i].e1));
+        o += (i ? ",{" : "{");
+        o += "\"ms\":" + std::to_string(t) + ",\"alg_flops\":" + std::to_string(recs[i].alg_flops) +
+             ",\"exec_flops\":" + std::to_string(recs[i].exec_flops) + ",\"desc\":\"" + recs[i].desc + "\"}";
+    }
+    return o + "]";
 }
 
 void ConvProfiler::summarize(int64_t* n, double* ms, double* alg, double* exec) const {

@@ -126,11 +126,13 @@ struct ConvProfiler {
     struct Rec {
         double alg_flops = 0, exec_flops = 0;
         cudaEvent_t e0 = nullptr, e1 = nullptr;
+        std::string desc;  // shape / schedule of the launch (per-layer report)
     };
     std::vector<Rec> recs;
     void clear();
     // totals: launches, ms, algorithmic FLOPs, executed MMA FLOPs
     void summarize(int64_t* n, double* ms, double* alg, double* exec) const;
+    std::string records_json() const;  // [{"ms","alg_flops","exec_flops","desc"}, ...]
 };
 ConvProfiler* conv_profiler();
 void set_conv_profiler(ConvProfiler* p);
