@@ -297,3 +297,50 @@ def test_slicing_changes_only_the_decode_peak(ctx):
         c2.close()
     assert _peaks(off)["decode"] > _peaks(on)["decode"]
     assert _peaks(off)["denoise"] == _peaks(on)["denoise"]
+
+
+# ------------------------------------------ randomised configurations
+def _random_configs(k=16, seed=2024):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < k:
+        depth = int(rng.integers(1, 4))
+        stages = int(rng.integers(1, 3))
+        unit = (1 << depth) * (1 << stages)
+        over = {
+            "run.frames": int(rng.integers(1, 5)),
+            "run.height": unit * int(rng.integers(1, 5)),
+            "run.width": unit * int(rng.integers(1, 5)),
+            "unet.depth": depth, "codec.stages": stages,
+            "unet.base_channels": int(rng.choice([8, 16, 24])),
+            "codec.width": int(rng.choice([8, 16])),
+            "unet.kernel": int(rng.choice([1, 3, 3, 5])),
+            "unet.cache_depth": int(rng.integers(0, depth)),
+            "sampler.steps": int(rng.integers(2, 7)),
+            "sampler.kind": str(rng.choice(["euler", "ddim", "ancestral"])),
+            "cache.n": int(rng.integers(1, 4)),
+            "swap.mode": str(rng.choice(["off", "sync", "async"])),
+            "chunk.enabled": str(rng.choice(["true", "false"])),
+            "chunk.halo": str(rng.choice(["exact", "none"])),
+            "chunk.eta": int(rng.choice([1, 2])), "chunk.omega": int(rng.choice([1, 2])),
+            "chunk.targets": str(rng.choice(["u0", "stem,u0", "d0,u0,head"])),
+            "decode.sliced": str(rng.choice(["true", "false"])),
+            "run.mode": "image" if len(out) % 4 == 3 else "text",
+        }
+        try:
+            lc.check_config(lc.config_text(over, base=DEFAULT))
+        except lc.LightCacheError:
+            continue
+        out.append(over)
+    return out
+
+
+@pytest.mark.parametrize("over", _random_configs())
+def test_random_configs_match_oracle(ctx, oracle, over):
+    """Seeded random shapes, depths, kernels, samplers, swap / chunk /
+    slicing modes and image mode against the oracle (the tile chooser,
+    schedules and epilogue variants see shapes the named tests do not)."""
+    video, lat, _ = _run(ctx, over)
+    want_v, want_l = oracle.run_pipeline(_kv(over))
+    assert lc.rel_l2(lat, want_l) < TOL
+    assert lc.rel_l2(video, want_v) < TOL
