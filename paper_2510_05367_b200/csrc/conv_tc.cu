@@ -521,7 +521,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float* off = offv + 16 * hh;
                     const int nb = tc.n_tile * p.BN + c00 + kPair * hh;
                     if (EPI == kEpiF32Raw) {
-                        if (p.tma_out) {
+                        if (p.tma_out && p.planar32) {
+                            // planar {x, y, img, channel} box: smem [16 ch][32 px], one
+                            // conflict-free 4-byte store per channel
+                            const uint32_t sb = stage_out_s +
+                                                static_cast<uint32_t>(((warp - 2) * slots + (ring ? (stage_it & 1) : hh)) * schunk +
+                                                                      lane * 4);
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + j * 128u),
+                                             "f"(__uint_as_float(v[j]) * hscale)
+                                             : "memory");
+                        } else if (p.tma_out) {
                             const uint32_t sb =
                                 stage_out_s + static_cast<uint32_t>(((warp - 2) * slots + (ring ? (stage_it & 1) : hh)) * schunk + lane * 64);
 #pragma unroll
@@ -530,6 +541,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                                __uint_as_float(v[j + 1]) * hscale,
                                                                __uint_as_float(v[j + 2]) * hscale,
                                                                __uint_as_float(v[j + 3]) * hscale));
+                        } else if (valid && nb < p.cs_out && p.planar32) {
+                            const size_t plane = static_cast<size_t>(p.n_img) * p.out_h * p.out_w;
+                            const size_t pix = (static_cast<size_t>(img) * p.out_h + oy) * p.out_w + ox;
+#pragma unroll
+                            for (int j = 0; j < 16; ++j)
+                                if (nb + j < p.cs_out) p.out32[(nb + j) * plane + pix] = __uint_as_float(v[j]) * hscale;
                         } else if (valid && nb < p.cs_out) {
                             float4* o4 = reinterpret_cast<float4*>(
                                 p.out32 + ((static_cast<size_t>(img) * p.out_h + oy) * p.out_w + ox) * p.cs_out + nb);
@@ -601,9 +618,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (lane == 0 && warp_store) {
                         const int nb0 = tc.n_tile * p.BN + c00;
                         const uint32_t sb = stage_out_s + static_cast<uint32_t>(((warp - 2) * slots + (ring ? (stage_it & 1) : 0)) * schunk);
-                        if (nb0 < p.cs_out) tma_store_4d(&p.tmO[tc.parity], sb, nb0, bx, by, bi);
-                        if (two && nb0 + kPair < p.cs_out)
-                            tma_store_4d(&p.tmO[tc.parity], sb + schunk, nb0 + kPair, bx, by, bi);
+                        if (p.planar32) {
+                            if (nb0 < p.cs_out) tma_store_4d(&p.tmO[tc.parity], sb, bx, by, bi, nb0);
+                            if (two && nb0 + kPair < p.cs_out)
+                                tma_store_4d(&p.tmO[tc.parity], sb + schunk, bx, by, bi, nb0 + kPair);
+                        } else {
+                            if (nb0 < p.cs_out) tma_store_4d(&p.tmO[tc.parity], sb, nb0, bx, by, bi);
+                            if (two && nb0 + kPair < p.cs_out)
+                                tma_store_4d(&p.tmO[tc.parity], sb + schunk, nb0 + kPair, bx, by, bi);
+                        }
                         bulk_commit();
                     }
                     ++stage_it;

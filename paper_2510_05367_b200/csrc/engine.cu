@@ -417,14 +417,14 @@ Bank tap_bank(const Bank& b) {
 }
 
 // Sub-pixel tap-to-N bank of nearest-upsample + 3x3 (the last decoder conv):
-// output channel (p*4 + t)*4 + c = merged weights of parity p = (py, px) and
-// low-res tap t = (dy, dx), channels padded to 4 (see launch_subpix_gather).
+// output channel (p*4 + t)*C + c = merged weights of parity p = (py, px) and
+// low-res tap t = (dy, dx) (see launch_subpix_gather; written channel-planar).
 Bank subpix_tap_bank(const Bank& b) {
     if (b.k != 3) throw_invariant("sub-pixel tap bank needs k == 3");
     Bank t;
     t.c_in = b.c_in;
     if (b.c_out > 4) throw_invariant("sub-pixel tap bank needs c_out <= 4");
-    t.c_out = 64;
+    t.c_out = 16 * b.c_out;
     t.k = 1;
     t.taps.assign(static_cast<size_t>(t.c_out * t.c_in), 0.0f);
     t.bias.assign(static_cast<size_t>(t.c_out), 0.0f);
@@ -438,7 +438,7 @@ Bank subpix_tap_bank(const Bank& b) {
                     for (int ky = lo[py][dy]; ky < hi[py][dy]; ++ky)
                         for (int kx = lo[px][dx]; kx < hi[px][dx]; ++kx)
                             acc += b.taps[((c * b.c_in + ic) * 3 + ky) * 3 + kx];
-                    t.taps[static_cast<size_t>(((p * 4 + tp) * 4 + c) * t.c_in + ic)] = static_cast<float>(acc);
+                    t.taps[static_cast<size_t>(((p * 4 + tp) * b.c_out + c) * t.c_in + ic)] = static_cast<float>(acc);
                 }
         }
     return t;
@@ -475,7 +475,7 @@ Bank subpixel_shuffle_bank(const Bank& b) {
 }
 
 void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window& win, float s,
-                 float o, bool silu, cudaStream_t st, float* out32, int shuffle_c, bool nhwc32) {
+                 float o, bool silu, cudaStream_t st, float* out32, int shuffle_c, bool nhwc32, bool planar) {
     ConvParams p{};
     const int sub = L.mode == 1 ? 2 : 1;
     // per parity class q = (py, px): output pixels 2Y+py in [oy0, oy1)
@@ -559,6 +559,8 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
     p.out = out.p;
     p.out32 = out32;
     p.nhwc32 = out32 && nhwc32 ? 1 : 0;
+    p.planar32 = p.nhwc32 && planar ? 1 : 0;
+    if (p.planar32 && sub != 1) throw_invariant("planar raw output needs a non-sub-pixel layer");
     if ((!out32 || p.nhwc32) && tma_store_enabled()) {
         // TMA-store epilogue: each warp's 32 pixels must form one box in
         // (x, y, img) of the tile, and every parity class a non-empty window
@@ -571,13 +573,29 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
         } else if (32 % p.TW == 0 && 32 % tp == 0 && (p.TI * tp) % 32 == 0) {
             bxd = p.TW, byd = p.TH, bid = 32 / tp;
         }
-        bool ok = bxd != 0;
+        bool ok = bxd != 0 && (!p.planar32 || bxd >= 4);  // planar fp32 boxes need >= 16 B rows
         for (int q = 0; q < L.P; ++q) ok = ok && p.ly1[q] > p.ly0[q] && p.lx1[q] > p.lx0[q];
         if (ok) {
             p.tma_out = 1;
             for (int q = 0; q < L.P; ++q) {
                 const int py = p.py[q], px = p.px[q];
                 const int esz = p.nhwc32 ? 4 : 2;
+                if (p.planar32) {
+                    // [channel][img][y][x]: dims {x, y, img, channel}
+                    const char* pbase = reinterpret_cast<const char*>(out32) +
+                                        (static_cast<int64_t>(p.ly0[q]) * out.w + p.lx0[q]) * 4;
+                    const uint64_t pdims[4] = {static_cast<uint64_t>(p.lx1[q] - p.lx0[q]),
+                                               static_cast<uint64_t>(p.ly1[q] - p.ly0[q]),
+                                               static_cast<uint64_t>(out.n), static_cast<uint64_t>(out.cs)};
+                    const uint64_t pstr[3] = {static_cast<uint64_t>(out.w) * 4,
+                                              static_cast<uint64_t>(out.h) * out.w * 4,
+                                              static_cast<uint64_t>(out.n) * out.h * out.w * 4};
+                    const uint32_t pbox[4] = {bxd, byd, bid, 16};
+                    const uint32_t pestr[4] = {1, 1, 1, 1};
+                    encode_map(&p.tmO[q], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, pbase, pdims, pstr, pbox, pestr,
+                               CU_TENSOR_MAP_SWIZZLE_NONE);
+                    continue;
+                }
                 const char* base = (p.nhwc32 ? reinterpret_cast<const char*>(out32) : reinterpret_cast<const char*>(out.p)) +
                                    (static_cast<int64_t>(p.ly0[q] * sub + py) * out.w + (p.lx0[q] * sub + px)) * out.cs * esz;
                 const uint64_t dims[4] = {static_cast<uint64_t>(out.cs), static_cast<uint64_t>(p.lx1[q] - p.lx0[q]),
@@ -1360,7 +1378,7 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
             ymax.n = G;
             ensure_buf(&dec_y_buf_, ymax.elems() * 4);
             run_tc_conv(*dec_last_tap_tc_, &e[S - 1], yv, Window{0, hl, 0, wl, 0, hl, 0, wl}, 1.0f, 0.0f, false,
-                        s_compute_, dec_y_buf_.as<float>(), 0, true);
+                        s_compute_, dec_y_buf_.as<float>(), 0, true, true);
             SubpixGatherArgs g{};
             g.y = dec_y_buf_.as<float>();
             g.cs_y = yv.cs;

@@ -144,10 +144,11 @@ void set_conv_profiler(ConvProfiler* p);
 // out32 non-null: write fp32 NCHW (out.n, c_out, out.h, out.w) instead of
 // fp16 NHWC into out.p.
 // nhwc32 (with out32): raw fp32 NHWC s*conv(x) into out32 with the channel
-// stride out.cs (tap-to-N GEMMs, no offsets / activation).
+// stride out.cs (tap-to-N GEMMs, no offsets / activation); planar: the same
+// values channel-planar [out.cs][out.n][out.h][out.w] (coalesced gathers).
 void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window& win, float s,
                  float o, bool silu, cudaStream_t st, float* out32 = nullptr, int shuffle_c = 0,
-                 bool nhwc32 = false);
+                 bool nhwc32 = false, bool planar = false);
 
 // Bank of a thin-input conv re-expressed as a 1x1 conv over gathered
 // patches (see launch_patch): c_in' = roundup64(c_in*k*k).

@@ -274,35 +274,38 @@ __global__ void __launch_bounds__(256) tap_gather_kernel(const TapGatherArgs a) 
             acc[c] + fmaf(a.o, ws[c], __ldg(a.bias + c));
 }
 
-// One thread per low-res pixel: its 2x2 output pixels x C channels; each
-// (parity, tap) group is one 16 B load (channels padded to 4 in y).
+// One thread per (low-res pixel, output parity): its output pixel x C
+// channels.  y is channel-planar ([(p*4 + t)*C + c][n][H][W]), so each of the
+// 4*C loads is coalesced across the warp (consecutive X).
 __global__ void __launch_bounds__(128) subpix_gather_kernel(const SubpixGatherArgs a) {
     pdl_wait();
     const int X = static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int row = static_cast<int>(blockIdx.y);
+    const int p = static_cast<int>(blockIdx.z);
     const int n = row / a.H, Y = row - n * a.H;
     if (X >= a.W) return;
-    const int W2 = 2 * a.W;
-    const size_t plane = static_cast<size_t>(4) * a.H * a.W;
-    float bias[4];
+    const int py = p >> 1, px = p & 1;
+    const size_t plane = static_cast<size_t>(a.n) * a.H * a.W;  // one y channel
+    float acc[4];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) bias[c] = c < a.C ? __ldg(a.bias + c) : 0.f;
+    for (int c = 0; c < 4; ++c) acc[c] = c < a.C ? __ldg(a.bias + c) : 0.f;
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
-        const int py = p >> 1, px = p & 1;
-        float4 acc = make_float4(bias[0], bias[1], bias[2], bias[3]);
+    for (int t = 0; t < 4; ++t) {
+        const int sy = Y + (t >> 1) - 1 + py, sx = X + (t & 1) - 1 + px;
+        const bool in = sy >= 0 && sy < a.H && sx >= 0 && sx < a.W;
+        const float* yp = a.y + (static_cast<size_t>(n) * a.H + (in ? sy : Y)) * a.W + (in ? sx : X) +
+                          (p * 4 + t) * a.C * plane;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            const int sy = Y + (t >> 1) - 1 + py, sx = X + (t & 1) - 1 + px;
-            if (sy < 0 || sy >= a.H || sx < 0 || sx >= a.W) continue;
-            const float4 v = __ldg(reinterpret_cast<const float4*>(
-                a.y + ((static_cast<size_t>(n) * a.H + sy) * a.W + sx) * a.cs_y + (p * 4 + t) * 4));
-            acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
-        }
-        const float av[4] = {acc.x, acc.y, acc.z, acc.w};
-        for (int c = 0; c < a.C; ++c)
-            a.out[(static_cast<size_t>(n) * a.C + c) * plane + static_cast<size_t>(2 * Y + py) * W2 + 2 * X + px] = av[c];
+        for (int c = 0; c < 4; ++c)
+            if (c < a.C) {
+                const float v = __ldg(yp + c * plane);
+                acc[c] += in ? v : 0.f;
+            }
     }
+    const int W2 = 2 * a.W;
+    const size_t vplane = static_cast<size_t>(4) * a.H * a.W;  // one video channel
+    for (int c = 0; c < a.C; ++c)
+        a.out[(static_cast<size_t>(n) * a.C + c) * vplane + static_cast<size_t>(2 * Y + py) * W2 + 2 * X + px] = acc[c];
 }
 
 // ------------------------------------------- upsample + thin-output conv
@@ -605,7 +608,7 @@ cudaError_t launch_subpix_gather(const SubpixGatherArgs& a, cudaStream_t st) {
     const int rows = a.n * a.H;
     if (a.W <= 0 || rows <= 0) return cudaSuccess;
     if (a.C > 4 || rows >= 65536) return cudaErrorInvalidValue;
-    return launch_pdl(subpix_gather_kernel, dim3((a.W + 127) / 128, rows), dim3(128), 0, st, a);
+    return launch_pdl(subpix_gather_kernel, dim3((a.W + 127) / 128, rows, 4), dim3(128), 0, st, a);
 }
 
 cudaError_t launch_upconv_thin(const UpThinArgs& a, cudaStream_t st) {

@@ -68,7 +68,7 @@ struct TapGatherArgs {
 cudaError_t launch_tap_gather(const TapGatherArgs& a, cudaStream_t st);
 
 // Sub-pixel tap gather of the last decoder conv (nearest 2x upsample + 3x3,
-// codec.cpp:103-113): y[low-res px][(p*4 + t)*4 + c] (channels padded to 4) holds, per output parity
+// codec.cpp:103-113): y[(p*4 + t)*C + c][n][H][W] (channel-planar) holds, per output parity
 // p = (py, px) and merged 2x2 tap t = (dy, dx), the GEMM partial sums; the
 // output pixel (2Y+py, 2X+px) is bias + the sum of its four in-range low-res
 // neighbours (Y+dy-1+py, X+dx-1+px).  fp32 NCHW video (n, C, 2H, 2W).
