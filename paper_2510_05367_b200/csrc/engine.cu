@@ -1150,7 +1150,7 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
             for (const Window& wd : block_windows(cfg_, "head", lh, lw)) {
                 run_tc_conv(*head_tap_tc_, &lv_[0].U, yv,
                             Window{wd.vy0, wd.vy1, wd.vx0, wd.vx1, wd.vy0, wd.vy1, wd.vx0, wd.vx1}, s, 0.0f, false,
-                            s_compute_, head_y_buf_.as<float>(), 0, true);
+                            s_compute_, head_y_buf_.as<float>(), 0, true, true);
                 TapGatherArgs g{};
                 g.y = head_y_buf_.as<float>();
                 g.cs_y = yv.cs;

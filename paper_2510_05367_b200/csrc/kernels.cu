@@ -240,38 +240,39 @@ __global__ void __launch_bounds__(256) patch3_kernel(const ThinInArgs a) {
 // One thread per output pixel; consecutive threads walk x, so each tap read
 // is a 16 B (C = 4) load at a 16*k*k-float stride, served from L2 (y was
 // just written by the GEMM).
+template <int K>
 __global__ void __launch_bounds__(256) tap_gather_kernel(const TapGatherArgs a) {
     pdl_wait();
     const int ow = a.win.ox1 - a.win.ox0, oh = a.win.oy1 - a.win.oy0;
     const int idx = static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int c = static_cast<int>(blockIdx.y);  // output channel
     if (idx >= a.n * oh * ow) return;
     const int row = idx / ow;
     const int x = a.win.ox0 + (idx - row * ow);
     const int n = row / oh;
     const int yy = a.win.oy0 + (row - n * oh);
-    const int r = a.k / 2;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f}, ws[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int dy = -r; dy <= r; ++dy) {
-        const int sy = yy + dy;
-        if (sy < a.win.vy0 || sy >= a.win.vy1) continue;
-        for (int dx = -r; dx <= r; ++dx) {
-            const int sx = x + dx;
-            if (sx < a.win.vx0 || sx >= a.win.vx1) continue;
-            const int t = (dy + r) * a.k + (dx + r);
-            const float* yp = a.y + ((static_cast<size_t>(n) * a.H + sy) * a.W + sx) * a.cs_y + t * a.C;
-            if (a.C == 4) {
-                const float4 v = __ldg(reinterpret_cast<const float4*>(yp));
-                acc[0] += v.x, acc[1] += v.y, acc[2] += v.z, acc[3] += v.w;
-            } else {
-                for (int c = 0; c < a.C; ++c) acc[c] += __ldg(yp + c);
-            }
-            for (int c = 0; c < a.C; ++c) ws[c] += __ldg(a.wsum + t * a.C + c);
+    constexpr int r = K / 2;
+    const size_t plane = static_cast<size_t>(a.n) * a.H * a.W;  // one (tap, channel) plane of y
+    const float* base = a.y + static_cast<size_t>(c) * plane + static_cast<size_t>(n) * a.H * a.W;
+    float acc = 0.f, ws = 0.f;
+#pragma unroll
+    for (int ky = 0; ky < K; ++ky) {
+        const int sy = yy + ky - r;
+        const bool rin = sy >= a.win.vy0 && sy < a.win.vy1;
+#pragma unroll
+        for (int kx = 0; kx < K; ++kx) {
+            const int sx = x + kx - r;
+            const bool in = rin && sx >= a.win.vx0 && sx < a.win.vx1;
+            const int t = ky * K + kx;
+            // every tap load issued (clamped address), out-of-window ones discarded
+            const float v = __ldg(base + static_cast<size_t>(t * a.C) * plane + static_cast<size_t>(in ? sy : yy) * a.W +
+                                  (in ? sx : x));
+            acc += in ? v : 0.f;
+            ws += in ? __ldg(a.wsum + t * a.C + c) : 0.f;
         }
     }
-    const size_t plane = static_cast<size_t>(a.H) * a.W;
-    for (int c = 0; c < a.C; ++c)
-        a.out[(static_cast<size_t>(n) * a.C + c) * plane + static_cast<size_t>(yy) * a.W + x] =
-            acc[c] + fmaf(a.o, ws[c], __ldg(a.bias + c));
+    a.out[(static_cast<size_t>(n) * a.C + c) * a.H * a.W + static_cast<size_t>(yy) * a.W + x] =
+        acc + fmaf(a.o, ws, __ldg(a.bias + c));
 }
 
 // One thread per (low-res pixel, output parity): its output pixel x C
@@ -601,7 +602,14 @@ cudaError_t launch_tap_gather(const TapGatherArgs& a, cudaStream_t st) {
     if (a.C > 4) return cudaErrorInvalidValue;
     const int64_t total = static_cast<int64_t>(rows) * ow;
     if (total >= (int64_t{1} << 31)) return cudaErrorInvalidValue;
-    return launch_pdl(tap_gather_kernel, dim3(static_cast<unsigned>((total + 255) / 256)), dim3(256), 0, st, a);
+    const dim3 grid(static_cast<unsigned>((total + 255) / 256), a.C);
+    switch (a.k) {
+        case 1: return launch_pdl(tap_gather_kernel<1>, grid, dim3(256), 0, st, a);
+        case 3: return launch_pdl(tap_gather_kernel<3>, grid, dim3(256), 0, st, a);
+        case 5: return launch_pdl(tap_gather_kernel<5>, grid, dim3(256), 0, st, a);
+        case 7: return launch_pdl(tap_gather_kernel<7>, grid, dim3(256), 0, st, a);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 cudaError_t launch_subpix_gather(const SubpixGatherArgs& a, cudaStream_t st) {

@@ -50,8 +50,8 @@ cudaError_t launch_patch(const ThinInArgs& a, int kp, cudaStream_t st);
 
 // Tap gather of a tap-to-N conv.  A thin-output k x k conv (c_out = C <= 4:
 // the denoiser head) runs on the tensor cores as a 1x1 GEMM whose N axis is
-// (tap, channel): y[px][t*C + c] = s * sum_ic w[c][ic][t] x[px][ic] (fp32
-// NHWC).  This kernel sums the in-window taps of each output pixel and adds
+// (tap, channel): y[t*C + c][px] = s * sum_ic w[c][ic][t] x[px][ic] (fp32,
+// channel-planar [t*C + c][n][H][W]).  This kernel sums the in-window taps of each output pixel and adds
 // the folded conditioning o * sum_{in-window t} wsum[t][c] + bias[c]
 // (unet.cpp:78-97 run_conv_block: affine -> zero-padded conv), writing fp32
 // NCHW.
