@@ -809,26 +809,8 @@ void Engine::configure(const RunConfig& cfg) {
             enc_alloc_ = -1;
             img_key_.clear();
         }
-        {
-            // merged sub-pixel taps of the last decoder conv: wm[p][dy*2+dx][c][4]
-            const Bank& b = cw_.dec[static_cast<size_t>(cfg.stages)];
-            const int ci = static_cast<int>(b.c_in), co = static_cast<int>(b.c_out);
-            if (co > 4) throw_config("codec image channels > 4 not supported on the GPU decoder");
-            std::vector<float> wm(static_cast<size_t>(16) * ci * 4, 0.0f);
-            const int lo[2][2] = {{0, 1}, {0, 2}}, hi[2][2] = {{1, 3}, {2, 3}};  // rows(parity, d)
-            for (int p = 0; p < 4; ++p)
-                for (int t = 0; t < 4; ++t)
-                    for (int c = 0; c < ci; ++c)
-                        for (int o = 0; o < co; ++o) {
-                            double acc = 0.0;
-                            for (int ky = lo[p / 2][t / 2]; ky < hi[p / 2][t / 2]; ++ky)
-                                for (int kx = lo[p % 2][t % 2]; kx < hi[p % 2][t % 2]; ++kx)
-                                    acc += b.taps[((static_cast<size_t>(o) * ci + c) * 3 + ky) * 3 + kx];
-                            wm[((static_cast<size_t>(p) * 4 + t) * ci + c) * 4 + o] = static_cast<float>(acc);
-                        }
-            dec_last_wm_ = dev_alloc(&ledger_, static_cast<int64_t>(wm.size() * 4), false);
-            LC_CUDA(cudaMemcpy(dec_last_wm_.p, wm.data(), wm.size() * 4, cudaMemcpyHostToDevice));
-        }
+        if (cw_.dec[static_cast<size_t>(cfg.stages)].c_out > 4)
+            throw_config("codec image channels > 4 not supported on the GPU decoder");
         dec_tc_.clear();
         for (int64_t i = 1; i < cfg.stages; ++i) dec_tc_.push_back(pack_tc_layer(&ledger_, cw_.dec[i], 0, 1));
         cfg_key_ = key;

@@ -281,7 +281,6 @@ private:
     Act patch_;                          // stem patch rows (2T, h, w, kp)
     DevBuf patch_buf_, dec_patch_buf_;
     Act dec_patch_;
-    DevBuf dec_last_wm_;                // merged sub-pixel weights of the last decoder conv
     std::vector<std::unique_ptr<TcLayer>> dec_tc_;  // decoder stages 1..S-1
     std::unique_ptr<ThinLayer> dec0_, dec_last_;
     std::vector<Level> lv_;

@@ -7,141 +7,6 @@ namespace lc {
 namespace {
 
 
-// ------------------------------------------------------------- thin input
-// One thread per (output pixel, output channel); weights staged in shared
-// memory as [c_in*k*k][c_out] so a warp (consecutive oc) reads consecutive
-// banks.  Exact reference order: bias, then (ic, ky, kx) ascending with
-// out-of-window taps skipped, separate multiply and add roundings.
-__global__ void thin_in_kernel(const ThinInArgs a) {
-    extern __shared__ float wsm[];
-    const int kk = a.k * a.k;
-    const int nw = a.c_out * a.c_in * kk;
-    for (int i = threadIdx.x; i < nw; i += blockDim.x) {
-        const int oc = i / (a.c_in * kk), rest = i % (a.c_in * kk);
-        wsm[rest * a.c_out + oc] = a.w[i];
-    }
-    __syncthreads();
-    const int oh = a.win.oy1 - a.win.oy0, ow = a.win.ox1 - a.win.ox0;
-    const int nimg = a.cfg_pair ? 2 * a.nsrc : a.nsrc;
-    const int64_t total = static_cast<int64_t>(nimg) * oh * ow * a.c_out;
-    const int r = (a.k - 1) / 2;
-    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int oc = static_cast<int>(idx % a.c_out);
-        int64_t px = idx / a.c_out;
-        const int ox = a.win.ox0 + static_cast<int>(px % ow);
-        px /= ow;
-        const int oy = a.win.oy0 + static_cast<int>(px % oh);
-        const int n = static_cast<int>(px / oh);
-        const int src = n % a.nsrc;
-        const bool branch1 = a.cfg_pair && n >= a.nsrc;
-        const float* xs = a.x + static_cast<int64_t>(src) * a.c_in * a.H * a.W;
-        float acc = a.bias[oc];
-        for (int ic = 0; ic < a.c_in; ++ic) {
-            for (int ky = 0; ky < a.k; ++ky) {
-                const int iy = oy + ky - r;
-                if (iy < a.win.vy0 || iy >= a.win.vy1) continue;
-                for (int kx = 0; kx < a.k; ++kx) {
-                    const int ix = ox + kx - r;
-                    if (ix < a.win.vx0 || ix >= a.win.vx1) continue;
-                    float v = xs[(static_cast<int64_t>(ic) * a.H + iy) * a.W + ix];
-                    if (branch1) v = __fadd_rn(v, a.cond_bias);
-                    if (a.apply_affine) v = __fadd_rn(__fmul_rn(v, a.s), a.o);
-                    acc = __fadd_rn(acc, __fmul_rn(wsm[((ic * a.k + ky) * a.k + kx) * a.c_out + oc], v));
-                }
-            }
-        }
-        if (a.silu) acc = acc / (1.0f + expf(-acc));
-        a.out[((static_cast<int64_t>(n) * a.H + oy) * a.W + ox) * a.cs_out + oc] = __float2half_rn(acc);
-    }
-}
-
-// Fast path (c_in*k*k <= MAXIN): one thread per output pixel.  The
-// conditioned input patch is formed once in registers (same roundings as
-// above), then output channels are produced 8 at a time against weights
-// staged in shared memory as [tap][cpad8] (warp-broadcast 16-byte reads),
-// stored as one 16-byte fp16 vector.  Per output channel the accumulation is
-// still bias, then (ic, ky, kx) ascending with skipped out-of-window taps.
-template <int MAXIN>
-__global__ void __launch_bounds__(128) thin_in_fast_kernel(const ThinInArgs a, int cpad8) {
-    extern __shared__ float wsm[];
-    const int kk = a.k * a.k, KK = a.c_in * kk;
-    for (int i = threadIdx.x; i < KK * cpad8; i += blockDim.x) {
-        const int t = i / cpad8, oc = i % cpad8;
-        wsm[i] = oc < a.c_out ? a.w[oc * KK + t] : 0.0f;
-    }
-    float* bsm = wsm + KK * cpad8;
-    for (int i = threadIdx.x; i < cpad8; i += blockDim.x) bsm[i] = i < a.c_out ? a.bias[i] : 0.0f;
-    __syncthreads();
-    const int oh = a.win.oy1 - a.win.oy0, ow = a.win.ox1 - a.win.ox0;
-    const int nimg = a.cfg_pair ? 2 * a.nsrc : a.nsrc;
-    const int64_t total = static_cast<int64_t>(nimg) * oh * ow;
-    const int r = (a.k - 1) / 2;
-    const int cmax = cpad8 < a.cs_out ? cpad8 : a.cs_out;
-    // 8 lanes per pixel: lane g produces channel chunks g, g+8, ... so one
-    // warp store instruction writes 4 pixels x 128 contiguous bytes.
-    for (int64_t item = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; item < total * 8;
-         item += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int g = static_cast<int>(item & 7);
-        const int64_t idx = item >> 3;
-        const int ox = a.win.ox0 + static_cast<int>(idx % ow);
-        const int oy = a.win.oy0 + static_cast<int>((idx / ow) % oh);
-        const int n = static_cast<int>(idx / (static_cast<int64_t>(ow) * oh));
-        const int src = n % a.nsrc;
-        const bool branch1 = a.cfg_pair && n >= a.nsrc;
-        const float* xs = a.x + static_cast<int64_t>(src) * a.c_in * a.H * a.W;
-        float v[MAXIN];
-        uint64_t live = 0;
-#pragma unroll
-        for (int t = 0; t < MAXIN; ++t) {
-            v[t] = 0.0f;
-            if (t < KK) {
-                const int ic = t / kk, ky = (t % kk) / a.k, kx = t % a.k;
-                const int iy = oy + ky - r, ix = ox + kx - r;
-                if (iy >= a.win.vy0 && iy < a.win.vy1 && ix >= a.win.vx0 && ix < a.win.vx1) {
-                    float x = xs[(static_cast<int64_t>(ic) * a.H + iy) * a.W + ix];
-                    if (branch1) x = __fadd_rn(x, a.cond_bias);
-                    if (a.apply_affine) x = __fadd_rn(__fmul_rn(x, a.s), a.o);
-                    v[t] = x;
-                    live |= 1ull << t;
-                }
-            }
-        }
-        __half* dst = a.out + ((static_cast<int64_t>(n) * a.H + oy) * a.W + ox) * a.cs_out;
-        for (int oc0 = g * 8; oc0 < cmax; oc0 += 64) {
-            float acc[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = bsm[oc0 + j];
-#pragma unroll
-            for (int t = 0; t < MAXIN; ++t) {
-                if (t < KK && ((live >> t) & 1)) {
-                    const float4 w0 = *reinterpret_cast<const float4*>(wsm + t * cpad8 + oc0);
-                    const float4 w1 = *reinterpret_cast<const float4*>(wsm + t * cpad8 + oc0 + 4);
-                    acc[0] = __fadd_rn(acc[0], __fmul_rn(w0.x, v[t]));
-                    acc[1] = __fadd_rn(acc[1], __fmul_rn(w0.y, v[t]));
-                    acc[2] = __fadd_rn(acc[2], __fmul_rn(w0.z, v[t]));
-                    acc[3] = __fadd_rn(acc[3], __fmul_rn(w0.w, v[t]));
-                    acc[4] = __fadd_rn(acc[4], __fmul_rn(w1.x, v[t]));
-                    acc[5] = __fadd_rn(acc[5], __fmul_rn(w1.y, v[t]));
-                    acc[6] = __fadd_rn(acc[6], __fmul_rn(w1.z, v[t]));
-                    acc[7] = __fadd_rn(acc[7], __fmul_rn(w1.w, v[t]));
-                }
-            }
-            __align__(16) __half2 h[4];
-#pragma unroll
-            for (int j = 0; j < 8; j += 2) {
-                float p = acc[j], q = acc[j + 1];
-                if (a.silu) {
-                    p = __fdividef(p, 1.0f + __expf(-p));
-                    q = __fdividef(q, 1.0f + __expf(-q));
-                }
-                h[j / 2] = __floats2half2_rn(p, q);
-            }
-            *reinterpret_cast<uint4*>(dst + oc0) = *reinterpret_cast<const uint4*>(h);
-        }
-    }
-}
-
 // --------------------------------------------------------- patch gather
 // One thread per (output pixel, 8-tap group): writes 16 bytes of the fp16
 // patch row; groups past c_in*k*k are zero.
@@ -309,163 +174,6 @@ __global__ void __launch_bounds__(128) subpix_gather_kernel(const SubpixGatherAr
         a.out[(static_cast<size_t>(n) * a.C + c) * vplane + static_cast<size_t>(2 * Y + py) * W2 + 2 * X + px] = acc[c];
 }
 
-// ------------------------------------------- upsample + thin-output conv
-// Last decoder conv fused with its nearest upsample (codec.cpp:103-113):
-// one thread per LOW-RES pixel produces the 2x2 output pixels it covers.
-// Per output parity (py,px) the 3x3 conv over the upsampled image is a 2x2
-// conv over the low-res image with merged taps (sub-pixel decomposition);
-// the 3x3 low-res neighbourhood feeds 16 (parity, tap) pairs.  Merged
-// weights wm[p][dy*2+dx][c][4] (COUT <= 4, zero padded) are prepared on the
-// host and read as one 16-byte shared-memory vector per (pair, channel).
-// Each thread covers two horizontally adjacent low-res pixels so every
-// weight vector feeds 2 pixels x COUT FMAs.
-template <int COUT>
-__global__ void __launch_bounds__(128) upconv_thin_kernel(const UpThinArgs a) {
-    extern __shared__ float4 wsm4[];
-    const int nw = 16 * a.c_in;
-    for (int i = threadIdx.x; i < nw; i += blockDim.x) wsm4[i] = reinterpret_cast<const float4*>(a.wm)[i];
-    __syncthreads();
-    const int H = 2 * a.Hin, W = 2 * a.Win;
-    const int wpairs = (a.Win + 1) / 2;
-    const int64_t total = static_cast<int64_t>(a.nimg) * a.Hin * wpairs;
-    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int X0 = 2 * static_cast<int>(idx % wpairs);
-        const int Y = static_cast<int>((idx / wpairs) % a.Hin);
-        const int n = static_cast<int>(idx / (static_cast<int64_t>(wpairs) * a.Hin));
-        float acc[2][4][COUT];
-#pragma unroll
-        for (int q = 0; q < 2; ++q)
-#pragma unroll
-            for (int p = 0; p < 4; ++p)
-#pragma unroll
-                for (int o = 0; o < COUT; ++o) acc[q][p][o] = 0.0f;
-        const __half* base = a.x + static_cast<int64_t>(n) * a.Hin * a.Win * a.cs_in;
-        for (int c0 = 0; c0 < a.c_in; c0 += 8) {
-            // 3 rows x 4 columns (X0-1 .. X0+2) of 8-channel vectors
-            uint4 nb[3][4];
-#pragma unroll
-            for (int ry = 0; ry < 3; ++ry) {
-                const int iy = Y + ry - 1;
-#pragma unroll
-                for (int cx = 0; cx < 4; ++cx) {
-                    const int ix = X0 + cx - 1;
-                    if (iy >= 0 && iy < a.Hin && ix >= 0 && ix < a.Win)
-                        nb[ry][cx] = *reinterpret_cast<const uint4*>(
-                            base + (static_cast<int64_t>(iy) * a.Win + ix) * a.cs_in + c0);
-                    else
-                        nb[ry][cx] = make_uint4(0, 0, 0, 0);
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                if (c0 + j >= a.c_in) break;
-                float v[3][4];
-#pragma unroll
-                for (int ry = 0; ry < 3; ++ry)
-#pragma unroll
-                    for (int cx = 0; cx < 4; ++cx)
-                        v[ry][cx] = __half2float(reinterpret_cast<const __half*>(&nb[ry][cx])[j]);
-#pragma unroll
-                for (int p = 0; p < 4; ++p) {
-                    const int py = p / 2, px = p % 2;
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const int dy = t / 2, dx = t % 2;
-                        const float4 w = wsm4[(p * 4 + t) * a.c_in + c0 + j];
-                        const int ry = dy - 1 + py + 1;  // row index into nb
-#pragma unroll
-                        for (int q = 0; q < 2; ++q) {
-                            const float x = v[ry][q + dx - 1 + px + 1];
-                            acc[q][p][0] = fmaf(w.x, x, acc[q][p][0]);
-                            if (COUT > 1) acc[q][p][1 % COUT] = fmaf(w.y, x, acc[q][p][1 % COUT]);
-                            if (COUT > 2) acc[q][p][2 % COUT] = fmaf(w.z, x, acc[q][p][2 % COUT]);
-                            if (COUT > 3) acc[q][p][3 % COUT] = fmaf(w.w, x, acc[q][p][3 % COUT]);
-                        }
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            if (X0 + q >= a.Win) break;
-#pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                const int oy = 2 * Y + p / 2, ox = 2 * (X0 + q) + p % 2;
-#pragma unroll
-                for (int o = 0; o < COUT; ++o)
-                    a.out[((static_cast<int64_t>(n) * COUT + o) * H + oy) * W + ox] = acc[q][p][o] + a.bias[o];
-            }
-        }
-    }
-}
-
-// ------------------------------------------------------------ thin output
-// One thread per output pixel, all (<= 8) output channels; taps outer,
-// channels inner with 16-byte fp16 loads.  Weights in shared memory as
-// [ky][kx][ic][c_out].
-template <int COUT>
-__global__ void thin_out_kernel(const ThinOutArgs a) {
-    extern __shared__ float wsm[];
-    const int kk = a.k * a.k;
-    const int nw = COUT * a.c_in * kk;
-    for (int i = threadIdx.x; i < nw; i += blockDim.x) {
-        const int oc = i / (a.c_in * kk), rest = i % (a.c_in * kk);
-        const int ic = rest / kk, t = rest % kk;
-        wsm[(t * a.c_in + ic) * COUT + oc] = a.w[i];
-    }
-    __syncthreads();
-    const int H = a.up2 ? 2 * a.Hin : a.Hin, W = a.up2 ? 2 * a.Win : a.Win;
-    const int oh = a.win.oy1 - a.win.oy0, ow = a.win.ox1 - a.win.ox0;
-    const int64_t total = static_cast<int64_t>(a.nimg) * oh * ow;
-    const int r = (a.k - 1) / 2;
-    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int ox = a.win.ox0 + static_cast<int>(idx % ow);
-        const int oy = a.win.oy0 + static_cast<int>((idx / ow) % oh);
-        const int n = static_cast<int>(idx / (static_cast<int64_t>(ow) * oh));
-        float acc[COUT];
-#pragma unroll
-        for (int o = 0; o < COUT; ++o) acc[o] = 0.0f;
-        for (int ky = 0; ky < a.k; ++ky) {
-            const int uy = oy + ky - r;
-            if (uy < a.win.vy0 || uy >= a.win.vy1) continue;
-            const int iy = a.up2 ? (uy >> 1) : uy;
-            for (int kx = 0; kx < a.k; ++kx) {
-                const int ux = ox + kx - r;
-                if (ux < a.win.vx0 || ux >= a.win.vx1) continue;
-                const int ix = a.up2 ? (ux >> 1) : ux;
-                const __half* px = a.x + ((static_cast<int64_t>(n) * a.Hin + iy) * a.Win + ix) * a.cs_in;
-                const float* wt = wsm + (ky * a.k + kx) * a.c_in * COUT;
-                for (int c0 = 0; c0 < a.c_in; c0 += 8) {
-                    const uint4 raw = *reinterpret_cast<const uint4*>(px + c0);
-                    const __half2* h2 = reinterpret_cast<const __half2*>(&raw);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        float2 f = __half22float2(h2[j]);
-                        if (a.apply_affine) {
-                            f.x = f.x * a.s + a.o;
-                            f.y = f.y * a.s + a.o;
-                        }
-                        const int c = c0 + 2 * j;
-                        if (c < a.c_in) {
-#pragma unroll
-                            for (int o = 0; o < COUT; ++o) acc[o] = fmaf(wt[c * COUT + o], f.x, acc[o]);
-                        }
-                        if (c + 1 < a.c_in) {
-#pragma unroll
-                            for (int o = 0; o < COUT; ++o) acc[o] = fmaf(wt[(c + 1) * COUT + o], f.y, acc[o]);
-                        }
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int o = 0; o < COUT; ++o)
-            a.out[((static_cast<int64_t>(n) * COUT + o) * H + oy) * W + ox] = acc[o] + a.bias[o];
-    }
-}
-
 // ------------------------------------------------------------- resampling
 __global__ void down2_kernel(const __half* __restrict__ in, __half* __restrict__ out, int nimg,
                              int H, int W, int cs) {
@@ -556,21 +264,6 @@ int grid_for(int64_t work, int threads) {
 
 }  // namespace
 
-template <int MAXIN>
-static cudaError_t launch_thin_in_fast(const ThinInArgs& a, cudaStream_t st) {
-    const int cpad8 = (a.c_out + 7) / 8 * 8;
-    const size_t smem = sizeof(float) * static_cast<size_t>((a.c_in * a.k * a.k + 1) * cpad8);
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(thin_in_fast_kernel<MAXIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-    }
-    const int nimg = a.cfg_pair ? 2 * a.nsrc : a.nsrc;
-    const int64_t work = 8 * static_cast<int64_t>(nimg) * (a.win.oy1 - a.win.oy0) * (a.win.ox1 - a.win.ox0);
-    thin_in_fast_kernel<MAXIN><<<grid_for(work, 128), 128, smem, st>>>(a, cpad8);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_patch(const ThinInArgs& a, int kp, cudaStream_t st) {
     const int nimg = a.cfg_pair ? 2 * a.nsrc : a.nsrc;
     const int64_t work =
@@ -617,80 +310,6 @@ cudaError_t launch_subpix_gather(const SubpixGatherArgs& a, cudaStream_t st) {
     if (a.W <= 0 || rows <= 0) return cudaSuccess;
     if (a.C > 4 || rows >= 65536) return cudaErrorInvalidValue;
     return launch_pdl(subpix_gather_kernel, dim3((a.W + 127) / 128, rows, 4), dim3(128), 0, st, a);
-}
-
-cudaError_t launch_upconv_thin(const UpThinArgs& a, cudaStream_t st) {
-    const size_t smem = sizeof(float) * static_cast<size_t>(16 * a.c_in * 4);
-    const int64_t work = static_cast<int64_t>(a.nimg) * a.Hin * ((a.Win + 1) / 2);
-#define LC_UPTHIN(N)                                                                                \
-    case N: {                                                                                       \
-        if (smem > 48 * 1024) {                                                                     \
-            cudaError_t e = cudaFuncSetAttribute(upconv_thin_kernel<N>,                             \
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,       \
-                                                 static_cast<int>(smem));                           \
-            if (e != cudaSuccess) return e;                                                         \
-        }                                                                                           \
-        upconv_thin_kernel<N><<<grid_for(work, 128), 128, smem, st>>>(a);                           \
-        break;                                                                                      \
-    }
-    switch (a.c_out) {
-        LC_UPTHIN(1)
-        LC_UPTHIN(2)
-        LC_UPTHIN(3)
-        LC_UPTHIN(4)
-        default: return cudaErrorInvalidValue;
-    }
-#undef LC_UPTHIN
-    return cudaGetLastError();
-}
-
-cudaError_t launch_thin_in(const ThinInArgs& a, cudaStream_t st) {
-    const int kk_in = a.c_in * a.k * a.k;
-    if (a.cs_out % 8 == 0) {
-        if (kk_in <= 9) return launch_thin_in_fast<9>(a, st);
-        if (kk_in <= 36) return launch_thin_in_fast<36>(a, st);
-        if (kk_in <= 64) return launch_thin_in_fast<64>(a, st);
-    }
-    const size_t smem = sizeof(float) * static_cast<size_t>(a.c_out * a.c_in * a.k * a.k);
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(thin_in_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-    }
-    const int nimg = a.cfg_pair ? 2 * a.nsrc : a.nsrc;
-    const int64_t work = static_cast<int64_t>(nimg) * (a.win.oy1 - a.win.oy0) * (a.win.ox1 - a.win.ox0) * a.c_out;
-    thin_in_kernel<<<grid_for(work, 256), 256, smem, st>>>(a);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_thin_out(const ThinOutArgs& a, cudaStream_t st) {
-    const size_t smem = sizeof(float) * static_cast<size_t>(8 * a.c_in * a.k * a.k);
-    const int64_t work = static_cast<int64_t>(a.nimg) * (a.win.oy1 - a.win.oy0) * (a.win.ox1 - a.win.ox0);
-    const int grid = grid_for(work, 128);
-#define LC_THIN_OUT(N)                                                                              \
-    case N: {                                                                                       \
-        if (smem > 48 * 1024) {                                                                     \
-            cudaError_t e = cudaFuncSetAttribute(thin_out_kernel<N>,                                \
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,       \
-                                                 static_cast<int>(smem));                           \
-            if (e != cudaSuccess) return e;                                                         \
-        }                                                                                           \
-        thin_out_kernel<N><<<grid, 128, smem, st>>>(a);                                             \
-        break;                                                                                      \
-    }
-    switch (a.c_out) {
-        LC_THIN_OUT(1)
-        LC_THIN_OUT(2)
-        LC_THIN_OUT(3)
-        LC_THIN_OUT(4)
-        LC_THIN_OUT(5)
-        LC_THIN_OUT(6)
-        LC_THIN_OUT(7)
-        LC_THIN_OUT(8)
-        default: return cudaErrorInvalidValue;
-    }
-#undef LC_THIN_OUT
-    return cudaGetLastError();
 }
 
 cudaError_t launch_down2(const __half* in, __half* out, int nimg, int H, int W, int cs, cudaStream_t st) {

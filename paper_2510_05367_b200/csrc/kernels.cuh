@@ -38,7 +38,6 @@ struct ThinInArgs {
     int cs_out;
     Window win;
 };
-cudaError_t launch_thin_in(const ThinInArgs& a, cudaStream_t st);
 
 // Patch gather for a thin-input conv run on the tensor cores: writes, per
 // output pixel, the conditioned k*k*c_in input taps (zero for taps outside
@@ -81,35 +80,6 @@ struct SubpixGatherArgs {
 };
 cudaError_t launch_subpix_gather(const SubpixGatherArgs& a, cudaStream_t st);
 
-// Thin-output conv (c_out <= 8): fp16 NHWC input -> fp32 NCHW output.
-//  * denoiser head: affine (s,o) then conv, no SiLU;
-//  * last decoder conv with the nearest upsample fused (up2=1: the input is
-//    the low-res tensor, output extents are 2x).
-struct ThinOutArgs {
-    const __half* x;  // (nimg, Hin, Win, cs_in)
-    int nimg, Hin, Win, cs_in, c_in;
-    int up2;
-    float s, o;
-    int apply_affine;
-    const float* w;   // [c_out][c_in][k][k]
-    const float* bias;
-    int c_out, k;
-    float* out;       // (nimg, c_out, H, W), H = Hin*(up2?2:1)
-    Window win;       // in output coordinates
-};
-cudaError_t launch_thin_out(const ThinOutArgs& a, cudaStream_t st);
-
-// Nearest-upsample + 3x3 conv with c_out <= 8 (last decoder conv), as a
-// sub-pixel 2x2 conv per output parity over the low-res input.
-struct UpThinArgs {
-    const __half* x;  // (nimg, Hin, Win, cs_in) low-res
-    int nimg, Hin, Win, cs_in, c_in;
-    const float* wm;  // merged weights [4 parities][4 taps][c_in][c_out]
-    const float* bias;
-    int c_out;
-    float* out;       // (nimg, c_out, 2*Hin, 2*Win) fp32
-};
-cudaError_t launch_upconv_thin(const UpThinArgs& a, cudaStream_t st);
 
 // 2x2 mean pool 0.25f*(a+b+c+d) (tensor.cpp:206-225), fp16 NHWC.
 cudaError_t launch_down2(const __half* in, __half* out, int nimg, int H, int W, int cs,
