@@ -39,6 +39,10 @@ WORKLOADS = {
           "unet.base_channels": 320, "unet.depth": 3, "sampler.steps": 25, "cache.n": 2, "swap.mode": "async"},
     # configs[0]: tiny desk config
     "A": {"run.height": 128, "run.width": 128, "cache.n": 3, "chunk.eta": 2, "chunk.omega": 1},
+    # configs[3]: SVD-XT VAE decode alone (latent 25x4x72x128 -> 25 frames of 1024x576),
+    # latent slices sharded over the GPUs, NCCL gather to rank 0
+    "D": {"run.frames": 25, "run.height": 576, "run.width": 1024, "codec.stages": 3, "codec.width": 128,
+          "unet.base_channels": 320, "unet.depth": 3},
 }
 DESCR = {
     "B": "AnimateDiff-Lightning-shaped U-Net: 16 frames, latent 4x64x64 (512x512 video), 4 Euler steps, "
@@ -47,6 +51,8 @@ DESCR = {
     "C": "SVD-XT-shaped U-Net: 25 frames, latent 4x72x128 (1024x576 video), 25 Euler steps, cache N=2, "
          "async swap, chunk u0 2x2, sliced decode, base 320, depth 3, codec W=128 S=3",
     "A": "tiny desk config: 8 frames, latent 4x32x32, 25 steps, N=3, chunk u0 2x1",
+    "D": "SVD-XT VAE decode: latent 25x4x72x128 -> 25 frames 1024x576, codec W=128 S=3, 4-frame slices, "
+         "contiguous frame blocks per GPU, NCCL gather of the decoded frames to rank 0",
 }
 
 
@@ -231,13 +237,43 @@ def cpu_measure(lc, over: dict, workers: int, reps: int):
     return fps, kind, desc
 
 
+def _cpu_decode_worker(text):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+
+    import lco
+    kv = lco.parse_text(text)
+    s = 1 << int(kv["codec.stages"])
+    lat = np.random.default_rng(0).standard_normal(
+        (1, 1, 4, int(kv["run.height"]) // s, int(kv["run.width"]) // s)).astype(np.float32)
+    lib = lco.Reference() if lco.Reference.available() else lco.Restatement()
+    t = time.time()
+    lib.decode(kv, lat)
+    return time.time() - t
+
+
 def reference_arm(args, world, rank):
     import paper_2510_05367_b200 as lc
     if rank != 0:
         return
     over = WORKLOADS[args.workload]
     workers = min(os.cpu_count() or 1, 64)
-    fps, kind, desc = cpu_measure(lc, over, workers, args.steps)
+    if args.workload == "D":
+        # the reference's decode of one frame per host process (decode is frame-wise)
+        import multiprocessing as mp
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import lco
+        kind = "reference" if lco.Reference.available() else "port"
+        text = lc.config_text(over, base=lc.DEFAULT_CONFIG)
+        with mp.get_context("fork").Pool(workers) as pool:
+            t0 = time.time()
+            for _ in range(max(1, args.steps // 10)):
+                pool.map(_cpu_decode_worker, [text] * workers)
+            wall = time.time() - t0
+        fps = workers * max(1, args.steps // 10) / wall
+        desc = f"1 frame decoded per host process, {workers} processes, {max(1, args.steps // 10)} rounds"
+    else:
+        fps, kind, desc = cpu_measure(lc, over, workers, args.steps)
     line = {"metric": "video_frames_per_sec", "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * WORKLOADS_FRAMES(over) / fps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
@@ -372,6 +408,91 @@ def gpu_arm(args, world, rank, local):
     ctx.close()
 
 
+def decode_arm(args, world, rank, local):
+    """Workload D (BASELINE.json configs[3]): sliced decode sharded over N
+    GPUs (lc_decode_sharded: contiguous frame blocks, grouped NCCL
+    send/recv to rank 0).  A step decodes the whole 25-frame latent video;
+    value = frames / device time of (latent shard H2D + decode + gather),
+    max over ranks; e2e adds the D2H of the full video on rank 0."""
+    import numpy as np
+
+    import paper_2510_05367_b200 as lc
+    over = WORKLOADS["D"]
+    text = lc.config_text(over, base=lc.DEFAULT_CONFIG)
+    kv = lc.parse_config(text)
+    T, s = int(kv["run.frames"]), 1 << int(kv["codec.stages"])
+    H, W = int(kv["run.height"]), int(kv["run.width"])
+    ctx = lc.Context(local)
+    ctx.configure(text)
+    if world > 1:
+        import torch.distributed as dist
+        uid = [lc.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.nccl_init(uid[0], world, rank)
+    lat = lc.randn(lc.derive_seed(int(kv["run.seed"]), 1), T * 4 * (H // s) * (W // s)).reshape(
+        1, T, 4, H // s, W // s)
+    lat_p = lc.PinnedArray(lat.size)  # pinned host buffers: the API's fast path
+    lat_p.array[:] = lat.reshape(-1)
+    vid_p = lc.PinnedArray(T * 3 * H * W)
+    clocks = ClockSampler(local).start()
+    for _ in range(args.warmup):
+        ctx.decode_sharded(lat_p, args.decode_slice, out=vid_p)
+    barrier(world)
+    ctx.timer_start()
+    dev_ms = 0.0
+    for _ in range(args.steps):
+        video, ms = ctx.decode_sharded(lat_p, args.decode_slice, out=vid_p)
+        dev_ms += ms
+    ms_e = allmax(world, ctx.timer_stop())
+    dev_ms = allmax(world, dev_ms)
+    clk = clocks.stop()
+    value = T * args.steps / (dev_ms / 1e3)
+    e2e = T * args.steps / (ms_e / 1e3)
+    # roofline: the decoder convs of one single-GPU decode, event-timed
+    ctx.set_conv_profile(True)
+    ctx.decode(lat[:, :min(T, 4)], args.decode_slice)
+    prof = ctx.conv_profile()
+    ctx.set_conv_profile(False)
+    peak, peak_src = peaks()
+    achieved = prof["alg_flops"] / (prof["ms"] / 1e3) / 1e12 if prof["ms"] > 0 else 0.0
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import lco
+            kind = "reference" if lco.Reference.available() else "port"
+            lib = lco.Reference() if kind == "reference" else lco.Restatement()
+            t0 = time.time()
+            lib.decode(lco.parse_text(text), lat[:, :1])
+            dt = time.time() - t0
+            cpu = {"value": 1.0 / dt, "unit": "frames/s", "cores": 1, "kind": kind,
+                   "sample": f"1 frame decoded by the {kind} CPU decoder ({dt:.1f} s)"}
+        line = {
+            "metric": "video_frames_per_sec", "value": value, "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "fp16 (fp32 accumulate; fp32 latent and video)",
+            "data": "synthetic (seeded randn latent, random-init codec weights of the reference architecture)",
+            "config": {"workload": DESCR["D"], "frames_per_step": T, "parallelism": f"decode sharded x{world}",
+                       "l2": "video 177 MB > 126 MB L2 (outputs larger than L2)",
+                       "decode_slice_frames": args.decode_slice},
+            "e2e": {"value": e2e, "unit": "frames/s", "h2d_bytes_per_step": int(lat.nbytes) // world,
+                    "d2h_bytes_per_step": int(video.nbytes)},
+            "roofline": {"bound": "tensor", "kernel": "conv_tc_kernel (decoder convs)", "achieved": achieved,
+                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": None, "peak_source": peak_src},
+            "gpu_launches": None,
+            "clocks": clk,
+            "video_finite": bool(np.isfinite(video).all()) if rank == 0 else None,
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    lat_p.free()
+    vid_p.free()
+    ctx.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -387,6 +508,8 @@ def main():
     world, rank, local = dist_init()
     if args.impl == "reference":
         reference_arm(args, world, rank)
+    elif args.workload == "D":
+        decode_arm(args, world, rank, local)
     else:
         gpu_arm(args, world, rank, local)
     if world > 1:

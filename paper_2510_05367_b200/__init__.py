@@ -374,15 +374,25 @@ class Context:
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
         _check(lib().lc_nccl_init(self._h, buf, ctypes.c_int(world), ctypes.c_int(rank)))
 
-    def decode_sharded(self, latents: np.ndarray, slice_frames: int = 4):
-        lat = _f32(latents)
+    def decode_sharded(self, latents, slice_frames: int = 4, out=None):
+        """lc_decode_sharded; `latents` / `out` may be PinnedArray (fast host
+        copies) or numpy arrays.  Returns (video, device ms)."""
         cfg = parse_config(self._text)
         s = 1 << int(cfg["codec.stages"])
-        T = lat.shape[0] * lat.shape[1]
-        out = np.empty((1, T, 3, lat.shape[3] * s, lat.shape[4] * s), np.float32)
+        if isinstance(latents, PinnedArray):
+            lat_ptr, T = latents.ptr, int(cfg["run.frames"])
+            h, w = int(cfg["run.height"]) // s, int(cfg["run.width"]) // s
+        else:
+            lat = _f32(latents)
+            lat_ptr, T = _p(lat), lat.shape[0] * lat.shape[1]
+            h, w = lat.shape[3], lat.shape[4]
+        if out is None:
+            out = np.empty((1, T, 3, h * s, w * s), np.float32)
+        out_ptr = out.ptr if isinstance(out, PinnedArray) else _p(out)
         ms = ctypes.c_float()
-        _check(lib().lc_decode_sharded(self._h, _p(lat), I64(T), I64(slice_frames), _p(out), ctypes.byref(ms)))
-        return out, ms.value
+        _check(lib().lc_decode_sharded(self._h, lat_ptr, I64(T), I64(slice_frames), out_ptr, ctypes.byref(ms)))
+        video = out.array.reshape(1, T, 3, h * s, w * s) if isinstance(out, PinnedArray) else out
+        return video, ms.value
 
 
 class PinnedArray:

@@ -1917,21 +1917,22 @@ void Engine::decode_sharded(const float* lat_host, int64_t T, int64_t slice, flo
     };
     int64_t f0, cnt;
     shard(rank, &f0, &cnt);
-    invalidate_graph();
-    DevBuf lat = dev_alloc(nullptr, std::max<int64_t>(1, cnt) * lat_frame * 4, false);
-    DevBuf vid = dev_alloc(nullptr, T * vid_frame * 4, false);
+    // shard buffers persist across calls (grow-only), like the run's
+    ensure_buf(&shard_lat_, std::max<int64_t>(1, cnt) * lat_frame * 4);
+    ensure_buf(&shard_vid_, T * vid_frame * 4);
+    const DevBuf& lat = shard_lat_;
+    const DevBuf& vid = shard_vid_;
+    cudaEvent_t e0, e1;
+    LC_CUDA(cudaEventCreate(&e0));
+    LC_CUDA(cudaEventCreate(&e1));
+    LC_CUDA(cudaEventRecord(e0, s_compute_));  // device time: H2D of the shard, decode, gather
     if (cnt > 0)
-        LC_CUDA(cudaMemcpy(lat.p, lat_host + f0 * lat_frame, static_cast<size_t>(cnt * lat_frame) * 4,
-                           cudaMemcpyHostToDevice));
+        LC_CUDA(cudaMemcpyAsync(lat.p, lat_host + f0 * lat_frame, static_cast<size_t>(cnt * lat_frame) * 4,
+                                cudaMemcpyHostToDevice, s_compute_));
     const int64_t keep = decode_slice;
     const bool keep_sliced = cfg_.slice_decode;
     decode_slice = slice;
     cfg_.slice_decode = true;
-    dec_alloc_ = -1;
-    cudaEvent_t e0, e1;
-    LC_CUDA(cudaEventCreate(&e0));
-    LC_CUDA(cudaEventCreate(&e1));
-    LC_CUDA(cudaEventRecord(e0, s_compute_));
     if (cnt > 0) decode_dev(lat.as<float>(), cnt, vid.as<float>() + f0 * vid_frame);
     if (world > 1) {
         // gather to rank 0: grouped point-to-point (ncclGather equivalent
@@ -1962,7 +1963,6 @@ void Engine::decode_sharded(const float* lat_host, int64_t T, int64_t slice, flo
     cudaEventDestroy(e1);
     decode_slice = keep;
     cfg_.slice_decode = keep_sliced;
-    dec_alloc_ = -1;
     if (rank == 0 && video_host)
         LC_CUDA(cudaMemcpy(video_host, vid.p, static_cast<size_t>(T * vid_frame) * 4, cudaMemcpyDeviceToHost));
 }

@@ -266,6 +266,7 @@ private:
     // columns + a gather kernel (launch_tap_gather / launch_subpix_gather)
     std::unique_ptr<TcLayer> head_tap_tc_, dec_last_tap_tc_;
     DevBuf head_wsum_, head_bias_, dec_last_bias_, head_y_buf_, dec_y_buf_;
+    DevBuf shard_lat_, shard_vid_;  // decode_sharded buffers
     // encoder (image mode, codec.cpp:64-81): patch GEMM + [down2 + conv]xS
     std::unique_ptr<TcLayer> enc0_tc_;
     std::vector<std::unique_ptr<TcLayer>> enc_tc_;

@@ -17,7 +17,7 @@ def last_json(path):
     return json.loads(open(path).read().strip().splitlines()[-1])
 
 
-for name in ("b", "c", "ref"):
+for name in ("b", "c", "d", "ref"):
     src = os.path.join(G, f"bench_{name}.json")
     if os.path.exists(src):
         json.dump(last_json(src), open(os.path.join(P, f"bench_{name}_{rnd}.json"), "w"), indent=1)

@@ -9,6 +9,7 @@ mkdir -p gpurun_out
 python bench.py > gpurun_out/bench_b.json 2> gpurun_out/bench_b.err
 python bench.py --workload C > gpurun_out/bench_c.json 2> gpurun_out/bench_c.err
 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+python bench.py --workload D > gpurun_out/bench_d.json 2> gpurun_out/bench_d.err
 python tools/parity_report.py > gpurun_out/parity.json 2> gpurun_out/parity.err
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launch_b.csv python tools/profile_step.py B 3 > gpurun_out/ncu_b.log 2>&1
