@@ -58,9 +58,8 @@ template <int CIN>
 __global__ void __launch_bounds__(256) patch3_kernel(const ThinInArgs a) {
     pdl_wait();
     const int ow = a.win.ox1 - a.win.ox0, oh = a.win.oy1 - a.win.oy0;
-    const int idx = static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int nimg = a.cfg_pair ? 2 * a.nsrc : a.nsrc;
-    if (idx >= nimg * oh * ow) return;
+    const int idx = min(static_cast<int>(blockIdx.x) * blockDim.x + threadIdx.x, nimg * oh * ow - 1);
     const int row = idx / ow;
     const int ox = a.win.ox0 + (idx - row * ow);
     const int n = row / oh;
@@ -91,13 +90,37 @@ __global__ void __launch_bounds__(256) patch3_kernel(const ThinInArgs a) {
                     v[(ic * 3 + ky) * 3 + kx] = x;
                 }
             }
-    uint4* dst = reinterpret_cast<uint4*>(a.out + ((static_cast<size_t>(n) * a.H + oy) * a.W + ox) * 64);
+    // stage the 128-byte row in shared memory (16-byte groups rotated by the
+    // thread index: conflict-free), then write the block's rows as one
+    // contiguous span (the block's pixels are consecutive in the patch tensor)
+    extern __shared__ uint4 rows_sm[];
 #pragma unroll
     for (int g = 0; g < 8; ++g) {
         __align__(16) __half2 h[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) h[j] = __floats2half2_rn(v[8 * g + 2 * j], v[8 * g + 2 * j + 1]);
-        dst[g] = *reinterpret_cast<const uint4*>(h);
+        rows_sm[threadIdx.x * 8 + ((g + threadIdx.x) & 7)] = *reinterpret_cast<const uint4*>(h);
+    }
+    __syncthreads();
+    const int first = static_cast<int>(blockIdx.x) * blockDim.x;
+    const int npx = min(static_cast<int>(blockDim.x), nimg * oh * ow - first);
+    if (ow == a.W && oh == a.H) {
+        // full-image window: the block's pixels are one contiguous span
+        uint4* dst = reinterpret_cast<uint4*>(a.out) + static_cast<size_t>(first) * 8;
+        for (int i = threadIdx.x; i < npx * 8; i += blockDim.x) {
+            const int px = i >> 3, g = i & 7;
+            dst[i] = rows_sm[px * 8 + ((g + px) & 7)];
+        }
+    } else {
+        for (int i = threadIdx.x; i < npx * 8; i += blockDim.x) {
+            const int px = i >> 3, g = i & 7;
+            const int pidx = first + px;
+            const int prow = pidx / ow;
+            const int pn = prow / oh;
+            const int py = a.win.oy0 + (prow - pn * oh), pxx = a.win.ox0 + (pidx - prow * ow);
+            reinterpret_cast<uint4*>(a.out + ((static_cast<size_t>(pn) * a.H + py) * a.W + pxx) * 64)[g] =
+                rows_sm[px * 8 + ((g + px) & 7)];
+        }
     }
 }
 
@@ -273,16 +296,16 @@ cudaError_t launch_patch(const ThinInArgs& a, int kp, cudaStream_t st) {
         const int64_t px = static_cast<int64_t>(rows) * (a.win.ox1 - a.win.ox0);
         if (px <= 0) return cudaSuccess;
         // small launches (a decoder slice): narrower blocks to fill the SMs
-        const int tb = px < 4 * 148 * 256 ? 64 : 256;
+        const int tb = px < 148 * 256 ? 64 : 256;
         const dim3 grid(static_cast<unsigned>((px + tb - 1) / tb)), blk(tb);
         switch (a.c_in) {
-            case 1: return launch_pdl(patch3_kernel<1>, grid, blk, 0, st, a);
-            case 2: return launch_pdl(patch3_kernel<2>, grid, blk, 0, st, a);
-            case 3: return launch_pdl(patch3_kernel<3>, grid, blk, 0, st, a);
-            case 4: return launch_pdl(patch3_kernel<4>, grid, blk, 0, st, a);
-            case 5: return launch_pdl(patch3_kernel<5>, grid, blk, 0, st, a);
-            case 6: return launch_pdl(patch3_kernel<6>, grid, blk, 0, st, a);
-            case 7: return launch_pdl(patch3_kernel<7>, grid, blk, 0, st, a);
+            case 1: return launch_pdl(patch3_kernel<1>, grid, blk, tb * 128, st, a);
+            case 2: return launch_pdl(patch3_kernel<2>, grid, blk, tb * 128, st, a);
+            case 3: return launch_pdl(patch3_kernel<3>, grid, blk, tb * 128, st, a);
+            case 4: return launch_pdl(patch3_kernel<4>, grid, blk, tb * 128, st, a);
+            case 5: return launch_pdl(patch3_kernel<5>, grid, blk, tb * 128, st, a);
+            case 6: return launch_pdl(patch3_kernel<6>, grid, blk, tb * 128, st, a);
+            case 7: return launch_pdl(patch3_kernel<7>, grid, blk, tb * 128, st, a);
             default: break;
         }
     }
