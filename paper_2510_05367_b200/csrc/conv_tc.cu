@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // relative to the class window, see ConvParams::tmO)
             constexpr bool kF16 = EPI == kEpiF16 || EPI == kEpiF16Silu;
             constexpr bool kTma = kF16 || EPI == kEpiF32Raw;  // epilogues with a TMA-store form
-            const bool warp_store = kTma && p.tma_out && tc.live && m0_in_tile && !p.debug_nostore;
+            const bool warp_store = kTma && p.tma_out && tc.live && m0_in_tile;
             const int bx = tc.X0 + m0_x - p.lx0[tc.parity];
             const int by = tc.Y0 + m0_y - p.ly0[tc.parity];
             const int bi = tc.I0 + m0_i;
@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 }
                             }
                         }
-                    } else if (p.tma_out || (valid && nb < p.cs_out && !p.debug_nostore)) {
+                    } else if (p.tma_out || (valid && nb < p.cs_out)) {
                         __align__(16) __half2 h[8];
 #pragma unroll
                         for (int j = 0; j < 16; j += 2) {

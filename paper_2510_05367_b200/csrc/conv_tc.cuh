@@ -92,7 +92,6 @@ struct alignas(64) ConvParams {
     int nhwc32;                   // with out32: raw fp32 NHWC (channel stride cs_out), value
                                   // = scale * acc, no offsets/activation (tap-to-N GEMMs whose
                                   // taps are summed by a gather kernel)
-    int debug_nostore;            // timing experiment only: skip the output stores
     // fp16 outputs through TMA tensor stores: per parity class, the output
     // lattice {C, X, Y, img} of that class (window-clipped, so the TMA unit
     // drops out-of-window rows); each epilogue warp stages 32 pixels x 16

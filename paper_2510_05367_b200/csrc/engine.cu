@@ -617,10 +617,6 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
     p.scale = s / L.wscale;
     p.shift = o;
     p.silu = silu ? 1 : 0;
-    {
-        static const int nostore = std::getenv("LC_DEBUG_NOSTORE") ? std::atoi(std::getenv("LC_DEBUG_NOSTORE")) : 0;
-        p.debug_nostore = nostore;
-    }
     ConvProfiler* prof = conv_profiler();
     if (prof) {
         // algorithmic work of the reference op (conv2d over the concat,

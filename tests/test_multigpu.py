@@ -79,3 +79,28 @@ def test_decode_sharded_single_rank_equals_decode(ctx):
     a = ctx.decode(lat, slice_frames=2)
     b, ms = ctx.decode_sharded(lat, slice_frames=2)
     assert np.array_equal(a, b) and ms > 0
+
+
+@pytest.mark.gpu
+def test_decode_sharded_repeated_calls_and_pinned_buffers(ctx):
+    """The shard buffers persist across calls (bench workload D): repeated
+    calls, a shorter latent after a longer one, and pinned host buffers all
+    give the single-device decode bit for bit."""
+    import paper_2510_05367_b200 as lc
+    over = dict(TINY, **{"run.frames": 6})
+    ctx.configure(lc.config_text(over, base=lc.DEFAULT_CONFIG))
+    rng = np.random.default_rng(2)
+    lat6 = rng.standard_normal((1, 6, 4, 8, 8)).astype(np.float32)
+    want6 = ctx.decode(lat6, slice_frames=4)
+    for _ in range(3):
+        got, _ = ctx.decode_sharded(lat6, slice_frames=4)
+        assert np.array_equal(got, want6)
+    lat3 = lat6[:, :3].copy()
+    got3, _ = ctx.decode_sharded(lat3, slice_frames=4)
+    assert np.array_equal(got3, want6[:, :3])
+    lp, vp = lc.PinnedArray(lat6.size), lc.PinnedArray(want6.size)
+    lp.array[:] = lat6.reshape(-1)
+    vid, _ = ctx.decode_sharded(lp, slice_frames=4, out=vp)
+    assert np.array_equal(vid, want6)
+    lp.free()
+    vp.free()
