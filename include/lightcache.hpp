@@ -96,6 +96,32 @@ public:
         r.report_json = rep.data();
         return r;
     }
+    // Throughput form with caller-owned (pinned) buffers: queue runs, then wait().
+    void run_pipeline_async(const float* x0, float* video) { check(lc_run_pipeline_async(ctx_, x0, video)); }
+    std::string wait() {
+        std::vector<char> rep(1 << 22);
+        check(lc_wait(ctx_, rep.data(), static_cast<int64_t>(rep.size())));
+        return rep.data();
+    }
+
+    // video_series(psnr / ssim) (proj/src/metrics.cpp:81-104) of two b=1
+    // videos {t,c,h,w}; host or device pointers.
+    void video_metrics(const float* a, const float* b, int64_t t, int64_t c, int64_t h, int64_t w,
+                       double data_range, std::vector<double>* psnr, std::vector<double>* ssim) {
+        psnr->resize(static_cast<size_t>(t));
+        ssim->resize(static_cast<size_t>(t));
+        check(lc_video_metrics(ctx_, a, b, t, c, h, w, data_range, psnr->data(), ssim->data()));
+    }
+
+    // write_ledger_csv content (proj/src/ledger.cpp:224-242) of this engine.
+    std::string ledger_csv() {
+        int64_t need = 0;
+        check(lc_ledger_csv(ctx_, nullptr, 0, &need));
+        std::vector<char> buf(static_cast<size_t>(need) + 16);
+        check(lc_ledger_csv(ctx_, buf.data(), static_cast<int64_t>(buf.size()), &need));
+        return buf.data();
+    }
+
     lc_ctx* raw() { return ctx_; }
 
 private:
