@@ -48,8 +48,8 @@ void put(char* dst, int64_t cap, const std::string& s) {
 
 std::string report_json(const lc::Engine& e, const lc::RunStats& st) {
     static const char* stages[4] = {"setup", "encode", "denoise", "decode"};
-    static const char* kinds[6] = {"compute_start", "compute_end", "xfer_start",
-                                   "xfer_end",      "await_start", "await_end"};
+    static const char* kinds[9] = {"compute_start", "compute_end", "xfer_start",     "xfer_end",       "await_start",
+                                   "await_end",     "origin",      "await_part_start", "await_part_end"};
     std::ostringstream os;
     os.precision(10);
     os << "{\"device_ms\":{\"denoise\":" << st.ms_denoise << ",\"decode\":" << st.ms_decode

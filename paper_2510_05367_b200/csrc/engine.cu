@@ -658,6 +658,7 @@ Engine::Engine(int device) : device_(device) {
     for (int b = 0; b < 2; ++b) {
         LC_CUDA(cudaEventCreateWithFlags(&ev_evict_[b], cudaEventDisableTiming));
         LC_CUDA(cudaEventCreateWithFlags(&ev_prefetch_[b], cudaEventDisableTiming));
+        LC_CUDA(cudaEventCreateWithFlags(&ev_prefetch_part_[b], cudaEventDisableTiming));
     }
     for (int b = 0; b < 2; ++b) LC_CUDA(cudaEventCreateWithFlags(&ev_cache_ready_[b], cudaEventDisableTiming));
     LC_CUDA(cudaEventCreate(&ev_start_));
@@ -675,6 +676,7 @@ Engine::~Engine() {
     for (int b = 0; b < 2; ++b) {
         cudaEventDestroy(ev_evict_[b]);
         cudaEventDestroy(ev_prefetch_[b]);
+        cudaEventDestroy(ev_prefetch_part_[b]);
     }
     for (int b = 0; b < 2; ++b) cudaEventDestroy(ev_cache_ready_[b]);
     cudaEventDestroy(ev_start_);
@@ -1092,12 +1094,32 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
         cond(j, &s, &o);
         const Act& out_i = i == 0 ? lv_[0].U : U_of(i);
         if (branch_seam && i == m) {
+            // per entry: the first half of its images as soon as their bytes
+            // landed, the second half once the whole entry has (the await
+            // marks bracket the wait that gates the block; the second wait is
+            // marked as a partial await)
+            auto part = [&](const Act& a, int i0, int ni) {
+                Act h = a;
+                h.n = ni;
+                h.p = a.p + static_cast<int64_t>(i0) * a.h * a.w * a.cs;
+                return h;
+            };
+            static const bool parts = !(std::getenv("LC_SEAM_PARTS") && std::atoi(std::getenv("LC_SEAM_PARTS")) == 0);
+            const int ne = out_i.n / 2, n0 = parts ? ne / 2 : 0;
             for (int b = 0; b < 2; ++b) {
+                const int i0 = b * ne;
                 record(4, prefetch_tag_, 0, s_compute_);
-                LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_prefetch_[b], 0));
+                LC_CUDA(cudaStreamWaitEvent(s_compute_, n0 > 0 ? ev_prefetch_part_[b] : ev_prefetch_[b], 0));
                 record(5, prefetch_tag_, 0, s_compute_);
+                if (n0 > 0) {
+                    up_block(i, part(lv_[i].D, i0, n0), part(U_of(i + 1), i0, n0), part(out_i, i0, n0), s, o);
+                    record(7, prefetch_tag_, 0, s_compute_);
+                    LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_prefetch_[b], 0));
+                    record(8, prefetch_tag_, 0, s_compute_);
+                }
                 if (b == 1 && seam == 2) issue_evict(step);
-                up_block(i, half(lv_[i].D, b), half(U_of(i + 1), b), half(out_i, b), s, o);
+                up_block(i, part(lv_[i].D, i0 + n0, ne - n0), part(U_of(i + 1), i0 + n0, ne - n0),
+                         part(out_i, i0 + n0, ne - n0), s, o);
             }
             prefetch_pending_ = false;
         } else {
@@ -1235,9 +1257,14 @@ void Engine::issue_prefetch(int issued, int needed) {
     const bool async = cfg_.swap_mode == SwapMode::Async;
     cudaStream_t st = async ? s_h2d_ : s_compute_;
     const int64_t bytes = cache_.elems();
+    // the first half of an entry's images (its bytes come first) gets its own
+    // event, so the seam block starts on it while the rest is in flight
+    const int64_t img_bytes = static_cast<int64_t>(cache_.h) * cache_.w * cache_.cs * 2;
+    const int64_t part_bytes = (cache_.n / 2 / 2) * img_bytes;
     for (int b = 0; b < 2; ++b) {
         if (async) h2d_used_ = true;
         size_t ci = 0;
+        bool part_done = part_bytes <= 0;
         for (int64_t off = 0; off < bytes; off += swap_chunk(), ++ci) {
             const int64_t len = std::min(swap_chunk(), bytes - off);
             if (async) LC_CUDA(cudaStreamWaitEvent(st, chunk_event(b, ci), 0));
@@ -1245,6 +1272,10 @@ void Engine::issue_prefetch(int issued, int needed) {
             LC_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(cache_.p) + b * bytes + off,
                                     cache_host_.as<char>() + b * bytes + off, static_cast<size_t>(len),
                                     cudaMemcpyHostToDevice, st));
+            if (!part_done && off + len >= part_bytes) {
+                LC_CUDA(cudaEventRecord(ev_prefetch_part_[b], st));
+                part_done = true;
+            }
         }
         record(3, needed, bytes, st);
         LC_CUDA(cudaEventRecord(ev_prefetch_[b], st));
@@ -1810,8 +1841,8 @@ RunStats Engine::finish_run(RunStats st, float* video_host, float* latent_host) 
                                static_cast<double>(mk.bytes), static_cast<double>(t)});
         lo = std::min(lo, static_cast<double>(t));
         hi = std::max(hi, static_cast<double>(t));
-        if (mk.kind == 4) open = t;
-        if (mk.kind == 5) st.stall_ms += t - open;
+        if (mk.kind == 4 || mk.kind == 7) open = t;
+        if (mk.kind == 5 || mk.kind == 8) st.stall_ms += t - open;
     }
     st.makespan_ms = marks_.empty() ? 0.0 : hi - lo;
     st.cache_bytes_planned = cfg_.cache_enabled

@@ -306,6 +306,7 @@ private:
         cudaEvent_t ev;
     };
     std::vector<Mark> marks_;
+    cudaEvent_t ev_prefetch_part_[2] = {nullptr, nullptr};  // first half of an entry's images landed
     cudaEvent_t ev_evict_[2] = {nullptr, nullptr}, ev_prefetch_[2] = {nullptr, nullptr},
                 ev_cache_ready_[2] = {nullptr, nullptr};  // per CFG entry: U_{m+1} half complete
     bool evict_pending_ = false, prefetch_pending_ = false, cache_ready_recorded_ = false;
