@@ -273,7 +273,9 @@ def reference_arm(args, world, rank):
         fps = workers * max(1, args.steps // 10) / wall
         desc = f"1 frame decoded per host process, {workers} processes, {max(1, args.steps // 10)} rounds"
     else:
-        fps, kind, desc = cpu_measure(lc, over, workers, args.steps)
+        # each round = one bounded sample per host process (~10 s); capped so
+        # the arm ends within a few minutes whatever --steps is
+        fps, kind, desc = cpu_measure(lc, over, workers, min(args.steps, 8))
     line = {"metric": "video_frames_per_sec", "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * WORKLOADS_FRAMES(over) / fps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
