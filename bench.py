@@ -287,6 +287,26 @@ def reference_arm(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def swap_summary(rep: dict) -> dict:
+    """Logical / moved bytes, seam stall, host-link GB/s of the transfers
+    that moved bytes, and the fraction of that transfer time hidden behind
+    compute (1 - stall / transfer time)."""
+    open_x, xfer_ms, xfer_bytes = {}, 0.0, 0
+    for kind, step, nbytes, t in rep["timeline"]["events"]:
+        if kind == "xfer_start":
+            open_x.setdefault(step, []).append(t)
+        elif kind == "xfer_end" and open_x.get(step):
+            dt = t - open_x[step].pop(0)
+            if dt > 0.02:  # clean evictions move nothing (~0 ms)
+                xfer_ms += dt
+                xfer_bytes += nbytes
+    stall = rep["timeline"]["stall_ms"]
+    return {"bytes_per_step": rep["swap"]["bytes"], "bytes_moved_per_step": rep["swap"]["bytes_moved"],
+            "stall_ms": stall, "transfer_ms": xfer_ms,
+            "link_gbs": xfer_bytes / (xfer_ms * 1e6) if xfer_ms > 0 else None,
+            "overlap_frac": 1.0 - stall / xfer_ms if xfer_ms > 0 else None}
+
+
 def WORKLOADS_FRAMES(over):
     return int(over.get("run.frames", 8))
 
@@ -388,8 +408,7 @@ def gpu_arm(args, world, rank, local):
             "uncached": uncached,
             "speedup_vs_uncached": value / uncached["value"],
             "denoise_ms": rep["device_ms"]["denoise"], "decode_ms": rep["device_ms"]["decode"],
-            "swap": {"bytes_per_step": rep["swap"]["bytes"], "bytes_moved_per_step": rep["swap"]["bytes_moved"],
-                     "stall_ms": rep["timeline"]["stall_ms"]},
+            "swap": swap_summary(rep),
             "e2e": {"value": e2e, "unit": "frames/s", "h2d_bytes_per_step": n_lat * 4,
                     "d2h_bytes_per_step": n_vid * 4},
             "roofline": {"bound": "tensor", "kernel": "conv_tc_kernel (tcgen05 implicit-GEMM conv)",
