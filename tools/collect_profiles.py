@@ -48,4 +48,13 @@ if os.path.exists(rep):
         "# ncu --set full --clock-control none --import-source on -k regex:conv_tc --launch-skip 115 "
         "--launch-count 1 python tools/profile_step.py B 3\n# (u0 of a full step: cg=2, BN=160, K=5440)\n\n" +
         det + "\n# selected raw metrics\n" + "\n".join(sel) + "\n")
+for name in ("layers_b", "layers_c", "swap_timeline_b"):
+    src = os.path.join(G, f"{name}.txt")
+    if os.path.exists(src):
+        shutil.copy(src, os.path.join(P, f"{name}_{rnd}.txt"))
+src = os.path.join(G, "launch_b.csv")
+if os.path.exists(src):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "membound_report.py"), src, "3"],
+                         capture_output=True, text=True).stdout
+    open(os.path.join(P, f"membound_b_{rnd}.txt"), "w").write(out)
 print("collected into", P)

@@ -17,4 +17,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launch_c.csv python tools/profile_step.py C 2 > gpurun_out/ncu_c.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:conv_tc --launch-skip ${TOPIDX:-115} --launch-count 1 \
     -o gpurun_out/full_top python tools/profile_step.py B 3 > gpurun_out/ncu_full.log 2>&1
+python tools/layer_report.py B gpurun_out/layers_b.json > gpurun_out/layers_b.txt 2>&1
+python tools/layer_report.py C gpurun_out/layers_c.json > gpurun_out/layers_c.txt 2>&1
+python tools/swap_timeline.py B > gpurun_out/swap_timeline_b.txt 2>&1
 ls -la gpurun_out
