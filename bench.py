@@ -465,9 +465,11 @@ def decode_arm(args, world, rank, local):
     barrier(world)
     ctx.timer_start()
     dev_ms = 0.0
+    launches = 0
     for _ in range(args.steps):
         video, ms = ctx.decode_sharded(lat_p, args.decode_slice, out=vid_p)
         dev_ms += ms
+        launches += ctx.kernel_launches()
     ms_e = allmax(world, ctx.timer_stop())
     dev_ms = allmax(world, dev_ms)
     clk = clocks.stop()
@@ -506,7 +508,7 @@ def decode_arm(args, world, rank, local):
             "roofline": {"bound": "tensor", "kernel": "conv_tc_kernel (decoder convs)", "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": None, "peak_source": peak_src},
-            "gpu_launches": None,
+            "gpu_launches": launches,
             "clocks": clk,
             "video_finite": bool(np.isfinite(video).all()) if rank == 0 else None,
         }

@@ -100,6 +100,8 @@ int lc_conv_profile(lc_ctx* ctx, int64_t* launches, double* ms, double* alg_flop
                     double* exec_flops);
 /* Per-launch records of the conv profile: JSON [{ms, alg_flops, exec_flops, desc}]. */
 int lc_conv_profile_records(lc_ctx* ctx, char* buf, int64_t cap);
+/* Kernels this library launched for the last run / decode call. */
+int lc_kernel_launches(lc_ctx* ctx, int64_t* n);
 /* Pinned host buffers for end-to-end copies. */
 void* lc_alloc_pinned(int64_t bytes);
 int lc_free_pinned(void* p);

@@ -97,7 +97,7 @@ EXPORTS = [
     "lc_forward", "lc_decode", "lc_video_metrics", "lc_ledger_csv", "lc_ledger_summary", "lc_conv2d", "lc_up_conv2d", "lc_plan_steps", "lc_split",
     "lc_model_numbers", "lc_derive_seed", "lc_randn", "lc_shard_frames", "lc_nccl_unique_id",
     "lc_nccl_init", "lc_decode_sharded", "lc_timer_start", "lc_timer_stop", "lc_set_conv_profile",
-    "lc_conv_profile", "lc_conv_profile_records", "lc_alloc_pinned", "lc_free_pinned",
+    "lc_conv_profile", "lc_conv_profile_records", "lc_kernel_launches", "lc_alloc_pinned", "lc_free_pinned",
 ]
 
 # ----------------------------------------------------------------- config
@@ -304,6 +304,12 @@ class Context:
         _check(lib().lc_conv_profile(self._h, ctypes.byref(n), ctypes.byref(ms), ctypes.byref(alg),
                                      ctypes.byref(exe)))
         return {"launches": n.value, "ms": ms.value, "alg_flops": alg.value, "exec_flops": exe.value}
+
+    def kernel_launches(self) -> int:
+        """Kernels launched by the last run / decode call."""
+        n = I64()
+        _check(lib().lc_kernel_launches(self._h, ctypes.byref(n)))
+        return n.value
 
     def conv_profile_records(self) -> list:
         buf = ctypes.create_string_buffer(1 << 20)

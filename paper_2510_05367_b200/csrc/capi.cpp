@@ -449,6 +449,9 @@ int lc_nccl_init(lc_ctx* ctx, const uint8_t* id128, int world, int rank) {
     });
 }
 
+int lc_kernel_launches(lc_ctx* ctx, int64_t* n) {
+    return guarded([&] { *n = ctx->engine.launches; });
+}
 int lc_decode_sharded(lc_ctx* ctx, const float* latents, int64_t T, int64_t slice, float* video, float* ms_out) {
     return guarded([&] {
         if (!ctx->comm && ctx->world > 1) lc::throw_config("lc_nccl_init first");

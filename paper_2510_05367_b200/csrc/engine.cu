@@ -1953,6 +1953,7 @@ void Engine::decode_sharded(const float* lat_host, int64_t T, int64_t slice, flo
     LC_CUDA(cudaEventCreate(&e0));
     LC_CUDA(cudaEventCreate(&e1));
     LC_CUDA(cudaEventRecord(e0, s_compute_));  // device time: H2D of the shard, decode, gather
+    launches = 0;
     if (cnt > 0)
         LC_CUDA(cudaMemcpyAsync(lat.p, lat_host + f0 * lat_frame, static_cast<size_t>(cnt * lat_frame) * 4,
                                 cudaMemcpyHostToDevice, s_compute_));
