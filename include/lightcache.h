@@ -149,6 +149,16 @@ int lc_split(int64_t h, int64_t w, int64_t eta, int64_t omega, int halo_kind, in
  * (proj/src/cache.cpp:124-130) in the reference fp32 geometry. */
 int lc_model_numbers(const char* config_text, int64_t* macs_full, int64_t* macs_cached,
                      int64_t* cache_bytes);
+/* The simulated transfer engine (swap.simulate = true,
+ * proj/src/swap.cpp:141-364, driven by pipeline.cpp:119-207 and
+ * cache.cpp:43-122): the virtual-clock timeline of the config's denoising
+ * loop.  Host-only (no device work).  `events` receives n_events rows of
+ * (kind, step, bytes, clock_ns), kind as TimelineEventKind
+ * (proj/include/stagecache/swap.hpp:16-23); makespan and stall as
+ * makespan_ns / stall_total_ns (swap.cpp:59-79).  Pass events = NULL to
+ * query n_events. */
+int lc_simulate_timeline(const char* config_text, int64_t* events, int64_t cap_events,
+                         int64_t* n_events, int64_t* makespan_ns, int64_t* stall_ns);
 /* derive_seed / NormalStream (proj/include/stagecache/rng.hpp:11-45). */
 uint64_t lc_derive_seed(uint64_t seed, uint64_t stream);
 int lc_randn(uint64_t seed, int64_t n, float* out);

@@ -303,6 +303,13 @@ class Reference:
                                             rep, ctypes.c_int64(1 << 20), macs))
         return video, json.loads(rep.value.decode()), list(macs)
 
+    def timeline(self, kv: dict, cap: int = 1 << 14):
+        """run_pipeline's timeline rows (kind, step, bytes, clock_ns), makespan_ns, stall_ns."""
+        ev = np.empty((cap, 4), np.int64)
+        info = (ctypes.c_int64 * 3)()
+        self._chk(self.lib.ref_timeline(to_text(kv).encode(), _p(ev), ctypes.c_int64(cap), info))
+        return ev[:info[0]].copy(), info[1], info[2]
+
     def check_config(self, kv: dict) -> int:
         return self.lib.ref_check_config(to_text(kv).encode())
 

@@ -105,6 +105,29 @@ int ref_run_pipeline(const char* config_text, float* video, int64_t video_cap_el
     });
 }
 
+// run_pipeline's engine timeline (proj/src/pipeline.cpp:209, swap.hpp:26-31)
+// as (kind, step, bytes, clock_ns) rows; `info` (3 int64): event count,
+// makespan_ns, stall_total_ns (swap.cpp:59-79).  With swap.simulate = true
+// the clocks are the simulated engine's virtual nanoseconds.
+int ref_timeline(const char* config_text, int64_t* events, int64_t cap_events, int64_t* info) {
+    return guarded([&] {
+        RunConfig cfg = parse_text(config_text);
+        cfg.out_dir = "";
+        RunResult r = run_pipeline(cfg);
+        const auto& tl = r.timeline;
+        info[0] = static_cast<int64_t>(tl.size());
+        info[1] = makespan_ns(tl);
+        info[2] = stall_total_ns(tl);
+        if (static_cast<int64_t>(tl.size()) > cap_events) throw ShapeError("timeline buffer too small");
+        for (size_t i = 0; i < tl.size(); ++i) {
+            events[4 * i + 0] = static_cast<int64_t>(tl[i].kind);
+            events[4 * i + 1] = tl[i].step;
+            events[4 * i + 2] = tl[i].bytes;
+            events[4 * i + 3] = tl[i].clock_ns;
+        }
+    });
+}
+
 // Config validation only (reference grammar + RunConfig::validate).
 int ref_check_config(const char* config_text) {
     return guarded([&] { parse_text(config_text).validate(); });

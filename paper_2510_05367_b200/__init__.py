@@ -95,7 +95,7 @@ EXPORTS = [
     "lc_upload_latent", "lc_run_resident", "lc_run_resident_async", "lc_run_pipeline_async", "lc_wait", "lc_download_video",
     "lc_set_decode_slice",
     "lc_forward", "lc_decode", "lc_video_metrics", "lc_ledger_csv", "lc_ledger_summary", "lc_conv2d", "lc_up_conv2d", "lc_plan_steps", "lc_split",
-    "lc_model_numbers", "lc_derive_seed", "lc_randn", "lc_shard_frames", "lc_nccl_unique_id",
+    "lc_model_numbers", "lc_simulate_timeline", "lc_derive_seed", "lc_randn", "lc_shard_frames", "lc_nccl_unique_id",
     "lc_nccl_init", "lc_decode_sharded", "lc_timer_start", "lc_timer_stop", "lc_set_conv_profile",
     "lc_conv_profile", "lc_conv_profile_records", "lc_kernel_launches", "lc_alloc_pinned", "lc_free_pinned",
 ]
@@ -166,6 +166,21 @@ def model_numbers(text: str):
     mf, mc, cb = I64(), I64(), I64()
     _check(lib().lc_model_numbers(text.encode(), ctypes.byref(mf), ctypes.byref(mc), ctypes.byref(cb)))
     return mf.value, mc.value, cb.value
+
+
+TIMELINE_KINDS = ("compute_start", "compute_end", "xfer_start", "xfer_end", "await_start", "await_end")
+
+
+def simulate_timeline(text: str):
+    """Virtual-clock timeline of the simulated transfer engine
+    (proj/src/swap.cpp:141-364): (events int64[n, 4] of kind, step, bytes,
+    clock_ns; makespan_ns; stall_ns)."""
+    n, mk, st = I64(), I64(), I64()
+    _check(lib().lc_simulate_timeline(text.encode(), None, I64(0), ctypes.byref(n), None, None))
+    ev = np.empty((max(1, n.value), 4), np.int64)
+    _check(lib().lc_simulate_timeline(text.encode(), _p(ev), I64(n.value), ctypes.byref(n), ctypes.byref(mk),
+                                      ctypes.byref(st)))
+    return ev[:n.value], mk.value, st.value
 
 
 def plan_steps(total: int, n: int):

@@ -66,7 +66,8 @@ std::string report_json(const lc::Engine& e, const lc::RunStats& st) {
        << st.cache_bytes_physical << ",";
     os << "\"swap\":{\"bytes\":" << st.swap_bytes << ",\"bytes_moved\":" << st.swap_bytes_moved
        << ",\"calls\":" << st.swap_calls << "},";
-    os << "\"timeline\":{\"makespan_ms\":" << st.makespan_ms << ",\"stall_ms\":" << st.stall_ms
+    os << "\"timeline\":{\"simulated\":" << (st.simulated ? "true" : "false")
+       << ",\"makespan_ms\":" << st.makespan_ms << ",\"stall_ms\":" << st.stall_ms
        << ",\"events\":[";
     for (size_t i = 0; i < st.timeline.size(); ++i) {
         const auto& t = st.timeline[i];
@@ -261,7 +262,8 @@ int lc_ledger_summary(lc_ctx* ctx, char* buf, int64_t cap) {
         const lc::Ledger& l = ctx->engine.ledger();
         std::ostringstream os;
         int64_t over[2] = {0, 0};
-        os << "{\"clock\":\"monotonic\",\"stages\":{";
+        os << "{\"clock\":\"" << (ctx->engine.config().swap_simulate ? "virtual" : "monotonic")
+           << "\",\"stages\":{";
         for (int s = 0; s < 4; ++s) {
             over[0] = std::max(over[0], l.peak[s][0]);
             over[1] = std::max(over[1], l.peak[s][1]);
@@ -411,6 +413,26 @@ int lc_model_numbers(const char* text, int64_t* macs_full, int64_t* macs_cached,
         if (macs_cached) *macs_cached = lc::flops_estimate(c, 2, c.frames, lh, lw, true);
         if (cache_bytes)
             *cache_bytes = 2 * c.frames * lc::cache_channels(c) * (lh >> c.cache_depth) * (lw >> c.cache_depth) * 4;
+    });
+}
+
+int lc_simulate_timeline(const char* text, int64_t* events, int64_t cap_events, int64_t* n_events,
+                         int64_t* makespan_ns, int64_t* stall_ns) {
+    return guarded([&] {
+        const lc::RunConfig c = lc::parse_config_text(text ? text : "");
+        const auto tl = lc::simulate_timeline(c);
+        if (n_events) *n_events = static_cast<int64_t>(tl.size());
+        if (makespan_ns) *makespan_ns = lc::sim_makespan_ns(tl);
+        if (stall_ns) *stall_ns = lc::sim_stall_ns(tl);
+        if (events) {
+            if (static_cast<int64_t>(tl.size()) > cap_events) lc::throw_shape("timeline buffer too small");
+            for (size_t i = 0; i < tl.size(); ++i) {
+                events[4 * i + 0] = tl[i].kind;
+                events[4 * i + 1] = tl[i].step;
+                events[4 * i + 2] = tl[i].bytes;
+                events[4 * i + 3] = tl[i].clock_ns;
+            }
+        }
     });
 }
 

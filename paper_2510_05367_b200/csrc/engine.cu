@@ -21,7 +21,8 @@ double Ledger::now() {
     return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 void Ledger::record(int kind, int tier, int64_t bytes, uint64_t id) {
-    events.push_back({kind, bytes, tier, stage, id, static_cast<uint64_t>(events.size()), now() - t0});
+    events.push_back(
+        {kind, bytes, tier, stage, id, static_cast<uint64_t>(events.size()), virt >= 0 ? virt : now() - t0});
     ++events_per_stage[stage];
 }
 void Ledger::enter(int s) {
@@ -728,9 +729,23 @@ void Engine::configure(const RunConfig& cfg) {
     const bool same_weights = configured_ && key == cfg_key_;
     const bool same_geom = configured_ && cfg.frames == cfg_.frames && cfg.height == cfg_.height &&
                            cfg.width == cfg_.width && same_weights &&
-                           cfg.cache_enabled == cfg_.cache_enabled;
+                           cfg.cache_enabled == cfg_.cache_enabled &&
+                           // alloc_activations: the pinned slow-tier entry and the
+                           // separate upsample buffers depend on these
+                           (cfg.swap_mode != SwapMode::Off) == (cfg_.swap_mode != SwapMode::Off) &&
+                           cfg.chunk_enabled == cfg_.chunk_enabled && cfg.halo == cfg_.halo;
     cfg_ = cfg;
     ledger_.budget_fast = 0;  // budget applies to runs, see run()
+    sim_tl_.clear();
+    sim_step_s_.assign(static_cast<size_t>(cfg.steps), 0.0);
+    sim_decode_s_ = 0;
+    if (cfg.swap_simulate) {
+        sim_tl_ = simulate_timeline(cfg);
+        for (const SimEvent& e : sim_tl_)
+            if (e.kind == 0) sim_step_s_[static_cast<size_t>(e.step)] = e.clock_ns * 1e-9;
+        sim_decode_s_ = sim_denoise_end_ns(cfg) * 1e-9;
+    }
+    ledger_.virt = cfg.swap_simulate ? 0.0 : -1.0;
     if (!same_weights) {
         ledger_.enter(kSetup);
         uw_ = init_unet(cfg);
@@ -1617,6 +1632,7 @@ void Engine::enqueue_body(RunStats& st) {
         const int64_t j = S - 1 - s;
         const int64_t t_orig = sc.src[j];
         const bool full = plan.is_full(s);
+        if (cfg_.swap_simulate) ledger_.virt = sim_step_s_[static_cast<size_t>(s)];
         record(0, static_cast<int>(s), 0, s_compute_);
         // 3: full step whose store will be evicted (mark the cache-ready point)
         const int seam = swap ? (full ? 3 : (plan.is_last_consumer(s) ? 2 : 1)) : 0;
@@ -1653,6 +1669,7 @@ void Engine::enqueue_body(RunStats& st) {
     }
     x_final_ = xa;
     record_timing(ev_den1_, s_compute_);
+    if (cfg_.swap_simulate) ledger_.virt = sim_decode_s_;
     ledger_.enter(kDecode);
     out_slices_ = true;
     decode_dev(xa, T, video_.as<float>());
@@ -1690,6 +1707,7 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
     if (async_pending_) (void)wait();
     cudaEvent_t t_start = ev_start_;
     LC_CUDA(cudaEventRecord(t_start, s_compute_));
+    ledger_.virt = cfg_.swap_simulate ? 0.0 : -1.0;
     ledger_.enter(kEncode);
     if (image) {
         // the latent comes from the encode stage inside the body
@@ -1748,6 +1766,7 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
         ++eager_runs_;
     }
     if (pinned) enqueue_video_out(pinned);
+    if (cfg_.swap_simulate) ledger_.virt = sim_decode_s_;
     ledger_.enter(kDecode);
     return finish_run(st, video_host, latent_host);
 }
@@ -1797,6 +1816,7 @@ RunStats Engine::wait() {
     video_host_pinned_ = nullptr;
     RunStats st = graph_stats_;
     stats_ = &st;
+    if (cfg_.swap_simulate) ledger_.virt = sim_decode_s_;
     ledger_.enter(kDecode);
     last_async_ = finish_run(st, nullptr, nullptr);
     return last_async_;
@@ -1845,6 +1865,18 @@ RunStats Engine::finish_run(RunStats st, float* video_host, float* latent_host) 
         if (mk.kind == 5 || mk.kind == 8) st.stall_ms += t - open;
     }
     st.makespan_ms = marks_.empty() ? 0.0 : hi - lo;
+    st.simulated = cfg_.swap_simulate;
+    if (st.simulated) {
+        // swap.simulate: the reported timeline is the simulated transfer
+        // engine's virtual one (swap.cpp:141-374, pipeline.cpp:209-212);
+        // the device work above is unchanged.
+        st.timeline.clear();
+        for (const SimEvent& e : sim_tl_)
+            st.timeline.push_back({static_cast<double>(e.kind), static_cast<double>(e.step),
+                                   static_cast<double>(e.bytes), e.clock_ns * 1e-6});
+        st.makespan_ms = sim_makespan_ns(sim_tl_) * 1e-6;
+        st.stall_ms = sim_stall_ns(sim_tl_) * 1e-6;
+    }
     st.cache_bytes_planned = cfg_.cache_enabled
                                  ? 2 * T * cache_channels(cfg_) * (lh >> cfg_.cache_depth) *
                                        (lw >> cfg_.cache_depth) * 4

@@ -52,6 +52,9 @@ struct Ledger {
     std::vector<LedgerEvent> events;
     uint64_t next_id = 1;
     double t0 = now();
+    // swap.simulate: events carry the simulated engine's virtual clock
+    // (pipeline.cpp:79-82) at the enclosing step boundary; < 0 = monotonic.
+    double virt = -1;
     static double now();
     void enter(int s);
     uint64_t alloc(int tier, int64_t bytes);
@@ -170,6 +173,7 @@ struct RunStats {
     int64_t peak[4][2] = {};
     int64_t hbm_peak = 0;
     std::vector<std::array<double, 4>> timeline;  // kind, step, bytes, t_ms
+    bool simulated = false;  // timeline is the swap.simulate virtual clock
     int64_t kernel_launches = 0;
 };
 
@@ -306,6 +310,12 @@ private:
         cudaEvent_t ev;
     };
     std::vector<Mark> marks_;
+    // swap.simulate: virtual timeline of the config (host.cpp
+    // simulate_timeline), each step's virtual compute start and the clock
+    // after the denoising drain, in seconds.
+    std::vector<SimEvent> sim_tl_;
+    std::vector<double> sim_step_s_;
+    double sim_decode_s_ = 0;
     cudaEvent_t ev_prefetch_part_[2] = {nullptr, nullptr};  // first half of an entry's images landed
     cudaEvent_t ev_evict_[2] = {nullptr, nullptr}, ev_prefetch_[2] = {nullptr, nullptr},
                 ev_cache_ready_[2] = {nullptr, nullptr};  // per CFG entry: U_{m+1} half complete

@@ -350,6 +350,241 @@ int64_t cache_channels(const RunConfig& c) {
     return (m + 1 == c.depth) ? (c.base_channels << (c.depth - 1)) : (c.base_channels << (m + 1));
 }
 
+// ------------------------------------------------------------------ simulated swap
+namespace {
+
+// Virtual transfer engine state for the two cache entries (one per CFG
+// branch, cache.cpp:43-60).  Jobs carry their virtual [start, end).
+struct SimJob {
+    int entry;
+    bool to_fast;
+    int64_t step, bytes, start, end;
+    int id;
+};
+struct SimEntry {
+    bool present = false;
+    bool on_fast = true;   // physical tier (Tensor5::tier)
+    int heading = -1;      // swap.cpp heading_: -1 none, 0 fast, 1 slow
+    int ticket = -1;       // job id of the entry's last ticket; -1 = no-op ticket
+};
+
+struct SimEngine {
+    const RunConfig& c;
+    bool swap_on;
+    int64_t now = 0, channel_free = 0;
+    std::vector<SimJob> pending;
+    std::vector<bool> done;      // per job id
+    std::vector<int64_t> ends;   // per job id
+    std::vector<SimEvent> tl;
+    SimEntry entries[2];
+
+    explicit SimEngine(const RunConfig& cfg) : c(cfg), swap_on(cfg.swap_mode != SwapMode::Off) {}
+
+    void rec(int kind, int64_t step, int64_t bytes, int64_t clock) { tl.push_back({kind, step, bytes, clock}); }
+    void macs(int64_t m) {  // mac_hook_tramp, swap.cpp:161-165
+        now += static_cast<int64_t>(std::llround(static_cast<double>(m) / c.swap_mac_rate * 1e9));
+    }
+    int64_t transfer_ns(int64_t bytes) const {  // swap.cpp:149-153
+        const double secs = c.swap_latency + static_cast<double>(bytes) / c.swap_bandwidth;
+        return static_cast<int64_t>(std::llround(secs * 1e9));
+    }
+    void finish(const SimJob& j) {  // finish_move, swap.cpp:195-213
+        rec(2, j.step, j.bytes, j.start);
+        SimEntry& e = entries[j.entry];
+        e.on_fast = j.to_fast;
+        if (e.heading == (j.to_fast ? 0 : 1)) e.heading = -1;
+        rec(3, j.step, j.bytes, j.end);
+        done[static_cast<size_t>(j.id)] = true;
+    }
+    void flush(int64_t up_to) {  // sim_flush, swap.cpp:351-364
+        std::stable_sort(pending.begin(), pending.end(),
+                         [](const SimJob& a, const SimJob& b) { return a.end < b.end; });
+        std::vector<SimJob> kept;
+        for (const SimJob& j : pending) {
+            if (j.end <= up_to) finish(j);
+            else kept.push_back(j);
+        }
+        pending.swap(kept);
+    }
+    int submit(int entry, bool to_fast, int64_t step, int64_t bytes) {  // swap.cpp:215-250
+        SimJob j{entry, to_fast, step, bytes, std::max(now, channel_free), 0, static_cast<int>(done.size())};
+        j.end = j.start + transfer_ns(bytes);
+        channel_free = j.end;
+        done.push_back(false);
+        ends.push_back(j.end);
+        entries[entry].heading = to_fast ? 0 : 1;
+        if (c.swap_mode == SwapMode::Sync) {
+            now = std::max(now, j.end);
+            finish(j);
+        } else {
+            pending.push_back(j);
+        }
+        return j.id;
+    }
+    int heading_tier(int entry) const {  // 0 fast, 1 slow
+        const SimEntry& e = entries[entry];
+        return e.heading >= 0 ? e.heading : (e.on_fast ? 0 : 1);
+    }
+    void await(int entry, int64_t step_of_ticket) {  // await_ready, swap.cpp:306-316
+        const int id = entries[entry].ticket;
+        if (id < 0) return;
+        rec(4, step_of_ticket, 0, now);
+        if (!done[static_cast<size_t>(id)]) {
+            now = std::max(now, ends[static_cast<size_t>(id)]);
+            flush(now);
+        }
+        rec(5, step_of_ticket, 0, now);
+    }
+    void drain() {  // swap.cpp:326-333
+        int64_t horizon = now;
+        for (const SimJob& j : pending) horizon = std::max(horizon, j.end);
+        now = horizon;
+        flush(horizon);
+    }
+};
+
+}  // namespace
+
+namespace {
+
+// Virtual-clock run of the denoising loop; returns the clock after the
+// loop's drain (pipeline.cpp:187).  Decode MACs advance the clock after the
+// last event and never reach the timeline.
+int64_t run_sim(const RunConfig& c, std::vector<SimEvent>* out) {
+    c.validate();
+    if (!(c.swap_bandwidth > 0) || !(c.swap_mac_rate > 0))
+        throw_config("simulated transfer engine needs bandwidth > 0 and a positive MAC rate");
+    SimEngine E(c);
+    const int64_t S = c.steps, T = c.frames, lh = c.latent_h(), lw = c.latent_w();
+    const int64_t M = c.depth, m = c.cache_depth;
+    StepPlan plan;
+    if (c.cache_enabled) plan = plan_steps(S, c.cache_n);
+    else plan.full.assign(static_cast<size_t>(S), true);
+    const auto blocks = block_plans(c);
+    const bool store_on = E.swap_on;  // CacheStore gets the engine only when swapping
+    const int64_t entry_bytes = T * cache_channels(c) * (lh >> m) * (lw >> m) * 4;
+    std::vector<int64_t> job_step;
+
+    // One block's convolution calls (unet.cpp:78-123, chunk.cpp:194-223,
+    // :274-316): a chunked block runs one conv2d_window per tile core.
+    auto block = [&](const std::string& name) {
+        const BlockPlan& bp = blocks[static_cast<size_t>(block_index(c, name))];
+        const int64_t h = lh >> bp.level, w = lw >> bp.level;
+        const int64_t per_px = 2 * T * bp.c_out * c.kernel * c.kernel * bp.c_in;
+        const bool chunked = c.chunk_enabled &&
+                             std::find(c.targets.begin(), c.targets.end(), name) != c.targets.end();
+        if (chunked && (c.eta > 1 || c.omega > 1)) {
+            const auto tiles = split(h, w, c.eta, c.omega, c.halo, c.halo_px, c.kernel);
+            for (const Tile& t : tiles)
+                E.macs(per_px * (t.core.y1 - t.core.y0) * (t.core.x1 - t.core.x0));
+        } else {
+            E.macs(per_px * h * w);
+        }
+    };
+    auto submit = [&](int entry, bool to_fast, int64_t step) {
+        job_step.push_back(step);
+        return E.submit(entry, to_fast, step, entry_bytes);
+    };
+    auto await_entry = [&](int b) {
+        const int id = E.entries[b].ticket;
+        if (id >= 0) E.await(b, job_step[static_cast<size_t>(id)]);
+    };
+    auto pending = [&](int b) {
+        const int id = E.entries[b].ticket;
+        return id >= 0 && !E.done[static_cast<size_t>(id)];
+    };
+    auto evict_all = [&](int64_t s) {  // cache.cpp:92-98, swap.cpp:284-289
+        for (int b = 0; b < 2; ++b) {
+            if (!E.entries[b].present) continue;
+            if (E.heading_tier(b) == 1) throw_invariant("evict: entry already on (or heading to) the Slow tier");
+            E.entries[b].ticket = submit(b, false, s);
+        }
+    };
+    auto prefetch_all = [&](int64_t needed) {  // cache.cpp:100-106, swap.cpp:291-298
+        for (int b = 0; b < 2; ++b) {
+            if (!E.entries[b].present) continue;
+            E.entries[b].ticket = E.heading_tier(b) == 0 ? -1 : submit(b, true, needed);
+        }
+    };
+
+    for (int64_t s = 0; s < S; ++s) {
+        E.rec(0, s, 0, E.now);  // compute_begin (the MAC hook installs here)
+        block("stem");
+        if (plan.is_full(s)) {
+            for (int64_t i = 0; i < M; ++i) block("d" + std::to_string(i));
+            block("mid");
+            for (int64_t i = M - 1; i >= 0; --i) block("u" + std::to_string(i));
+            block("head");
+            E.rec(1, s, 0, E.now);
+            E.flush(E.now);
+            if (c.cache_enabled) {
+                for (int b = 0; b < 2; ++b) {  // CacheStore::store, cache.cpp:43-60
+                    SimEntry& e = E.entries[b];
+                    if (e.present && store_on && pending(b)) await_entry(b);
+                    e.present = true;
+                    e.on_fast = true;
+                    e.ticket = -1;
+                }
+                if (E.swap_on) {
+                    evict_all(s);
+                    if (plan.has_consumers(s)) prefetch_all(s + 1);
+                }
+            }
+        } else {
+            for (int64_t i = 0; i <= m; ++i) block("d" + std::to_string(i));
+            // seam: CacheStore::assemble -> fetch(uncond), fetch(cond) (cache.cpp:62-90)
+            if (store_on) {
+                for (int b = 0; b < 2; ++b) {
+                    await_entry(b);
+                    if (!E.entries[b].on_fast) {  // recall, swap.cpp:300-304
+                        E.entries[b].ticket = E.heading_tier(b) == 0 ? -1 : submit(b, true, s);
+                        await_entry(b);
+                    }
+                }
+                if (plan.is_last_consumer(s)) evict_all(s);
+            }
+            for (int64_t i = m; i >= 0; --i) block("u" + std::to_string(i));
+            block("head");
+            E.rec(1, s, 0, E.now);
+            E.flush(E.now);
+        }
+    }
+    E.drain();
+    // TransferEngine::timeline() returns the log stably sorted by clock
+    // (swap.cpp:366-374).
+    std::stable_sort(E.tl.begin(), E.tl.end(),
+                     [](const SimEvent& a, const SimEvent& b) { return a.clock_ns < b.clock_ns; });
+    if (out) *out = std::move(E.tl);
+    return E.now;
+}
+
+}  // namespace
+
+std::vector<SimEvent> simulate_timeline(const RunConfig& c) {
+    std::vector<SimEvent> tl;
+    run_sim(c, &tl);
+    return tl;
+}
+int64_t sim_denoise_end_ns(const RunConfig& c) { return run_sim(c, nullptr); }
+
+int64_t sim_makespan_ns(const std::vector<SimEvent>& tl) {
+    if (tl.empty()) return 0;
+    int64_t lo = tl.front().clock_ns, hi = lo;
+    for (const SimEvent& e : tl) {
+        lo = std::min(lo, e.clock_ns);
+        hi = std::max(hi, e.clock_ns);
+    }
+    return hi - lo;
+}
+int64_t sim_stall_ns(const std::vector<SimEvent>& tl) {
+    int64_t total = 0, open = 0;
+    for (const SimEvent& e : tl) {
+        if (e.kind == 4) open = e.clock_ns;
+        else if (e.kind == 5) total += e.clock_ns - open;
+    }
+    return total;
+}
+
 // ------------------------------------------------------------------ rng
 uint64_t splitmix64_at(uint64_t seed, uint64_t counter) {
     uint64_t z = seed + (counter + 1) * 0x9e3779b97f4a7c15ull;

@@ -127,6 +127,26 @@ int64_t flops_estimate(const RunConfig& cfg, int64_t b, int64_t t, int64_t h, in
 // cache_feature_shape channel count at the seam (unet.cpp:302-309).
 int64_t cache_channels(const RunConfig& cfg);
 
+// ------------------------------------------------------------------ simulated swap
+// One timeline event (swap.hpp:16-30): kind 0 compute_start, 1 compute_end,
+// 2 xfer_start, 3 xfer_end, 4 await_start, 5 await_end; clock in virtual ns.
+struct SimEvent {
+    int kind;
+    int64_t step, bytes, clock_ns;
+};
+// The reference's simulated transfer engine (swap.simulate = true,
+// proj/src/swap.cpp:141-364) driven by the denoising loop of run_pipeline
+// (pipeline.cpp:119-207) and the cache store (cache.cpp:43-122): a virtual
+// nanosecond clock advanced by every convolution call's MAC count at
+// swap.mac_rate (tensor.cpp:21-24, :194), one transfer channel of
+// latency + bytes / bandwidth per job.  Returns the event list in the
+// reference's recording order; bit-exact with it (tests/test_simulate.py).
+std::vector<SimEvent> simulate_timeline(const RunConfig& cfg);
+int64_t sim_makespan_ns(const std::vector<SimEvent>& tl);  // swap.cpp:59-68
+int64_t sim_stall_ns(const std::vector<SimEvent>& tl);     // swap.cpp:70-79
+// Virtual clock after the denoising loop's drain (pipeline.cpp:187).
+int64_t sim_denoise_end_ns(const RunConfig& cfg);
+
 // ------------------------------------------------------------------ rng
 uint64_t splitmix64_at(uint64_t seed, uint64_t counter);  // rng.hpp:11-16
 uint64_t derive_seed(uint64_t seed, uint64_t stream);     // rng.hpp:24-26

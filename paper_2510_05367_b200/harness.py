@@ -132,7 +132,8 @@ def run_report(res: RunResult) -> dict:
                                            "cached_steps")},
         "cache_bytes": rep["cache_bytes"],
         "timeline": {"makespan_seconds": rep["timeline"]["makespan_ms"] / 1e3,
-                     "stall_seconds": rep["timeline"]["stall_ms"] / 1e3, "simulated": False},
+                     "stall_seconds": rep["timeline"]["stall_ms"] / 1e3,
+                     "simulated": bool(rep["timeline"].get("simulated", False))},
         "video": {"frames": rep["video"]["frames"], "channels": rep["video"]["channels"],
                   "height": rep["video"]["height"], "width": rep["video"]["width"]},
     }

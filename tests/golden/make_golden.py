@@ -8,7 +8,7 @@ too slow for the single-threaded reference and are produced by the
 restatement oracle/lc_oracle.c, which tests/test_oracle.py pins bit-exactly
 to the reference on every smaller case.
 
-Usage:  python tests/golden/make_golden.py [small|b0|c0]...
+Usage:  python tests/golden/make_golden.py [small|b0|c0|metrics|timelines]...
 """
 import json
 import os
@@ -120,6 +120,43 @@ def metrics():
     np.savez_compressed(os.path.join(HERE, "metrics.npz"), **out)
 
 
+SIM_TINY = {"run.frames": 2, "run.height": 32, "run.width": 32, "sampler.steps": 6, "run.seed": 7,
+            "swap.simulate": "true"}
+SIM = {
+    # acceptance C8 (proj/tests/acceptance_main.cpp:384-418): default config
+    "c8_off": {"swap.simulate": "true", "swap.mode": "off"},
+    "c8_async": {"swap.simulate": "true", "swap.mode": "async"},
+    "c8_sync": {"swap.simulate": "true", "swap.mode": "sync"},
+    # test_pipeline.cpp:250-260 tiny_config
+    "tiny_async": dict(SIM_TINY, **{"swap.mode": "async"}),
+    "tiny_sync_n3": dict(SIM_TINY, **{"swap.mode": "sync", "cache.n": 3}),
+    "tiny_async_n1": dict(SIM_TINY, **{"swap.mode": "async", "cache.n": 1}),
+    "slow_link": dict(SIM_TINY, **{"swap.mode": "async", "swap.bandwidth": 1e6}),
+    "slow_link_sync": dict(SIM_TINY, **{"swap.mode": "sync", "swap.bandwidth": 5e6, "swap.latency": 1e-3}),
+    "mid_link_n3": dict(SIM_TINY, **{"swap.mode": "async", "swap.bandwidth": 3e7, "cache.n": 3,
+                                     "sampler.steps": 7}),
+    "image_m1_chunks": dict(SIM_TINY, **{"swap.mode": "async", "run.mode": "image", "swap.bandwidth": 2e7,
+                                         "unet.cache_depth": 1, "chunk.targets": "stem,d1,u0,u1",
+                                         "chunk.eta": 4, "chunk.omega": 2}),
+    "no_cache": dict(SIM_TINY, **{"swap.mode": "async", "cache.enabled": "false"}),
+    "zero_latency": dict(SIM_TINY, **{"swap.mode": "async", "swap.latency": 0, "swap.mac_rate": 3e9}),
+}
+
+
+def timelines():
+    """Simulated transfer-engine timelines (swap.simulate = true,
+    proj/src/swap.cpp:141-374) from the reference's run_pipeline."""
+    ref = lco.Reference()
+    out = {}
+    for name, over in SIM.items():
+        kv = kv_of(over)
+        ev, mk, st = ref.timeline(kv)
+        out[name + "_events"] = ev
+        out[name + "_info"] = np.array([mk, st], np.int64)
+        out[name + "_config"] = np.array(lco.to_text(kv))
+    np.savez_compressed(os.path.join(HERE, "timelines.npz"), **out)
+
+
 if __name__ == "__main__":
     what = sys.argv[1:] or ["small"]
     if "small" in what:
@@ -130,3 +167,5 @@ if __name__ == "__main__":
         slice0("c_frame0", C0)
     if "metrics" in what:
         metrics()
+    if "timelines" in what:
+        timelines()

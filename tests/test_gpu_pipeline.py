@@ -100,6 +100,10 @@ def test_swap_modes_are_bit_identical(ctx):
     for mode in ("off", "sync", "async"):
         v, _, rep = _run(ctx, dict(TINY, **{"swap.mode": mode}))
         vids.append(v)
+        # reconfiguring off -> on at the same geometry must allocate the
+        # slow-tier entry and really swap
+        assert (rep["swap"]["calls"] > 0) == (mode != "off"), mode
+        assert (rep["peaks"]["denoise"]["slow"] > 0) == (mode != "off"), mode
     assert np.array_equal(vids[0], vids[1]) and np.array_equal(vids[0], vids[2])
 
 
@@ -151,6 +155,37 @@ def test_swap_bytes_logical_and_moved(ctx):
     assert rep["swap"]["calls"] == 7  # plan F c c F c c F
     assert rep["swap"]["bytes"] == 7 * pair
     assert rep["swap"]["bytes_moved"] == 5 * pair  # 3 dirty evictions + 2 prefetches
+
+
+@pytest.mark.parametrize("mode,bw", [("async", 1e6), ("sync", 4e9), ("async", 4e9), ("off", 4e9)])
+def test_simulated_swap_reports_the_virtual_timeline(ctx, mode, bw):
+    """swap.simulate = true (proj/src/swap.cpp:141-374): the device work and
+    video are unchanged, the run reports the simulated engine's virtual
+    timeline (pinned to the reference in tests/test_simulate.py) and the
+    ledger clock is labelled virtual (pipeline.cpp:79-82, :212-216)."""
+    from paper_2510_05367_b200 import harness
+    over = dict(TINY, **{"swap.mode": mode, "swap.bandwidth": bw, "run.seed": 7})
+    real, _, rep_real = _run(ctx, over)
+    assert rep_real["timeline"]["simulated"] is False
+    text = lc.config_text(dict(over, **{"swap.simulate": "true"}), base=DEFAULT)
+    res = harness.run_pipeline(ctx, text)
+    assert np.array_equal(res.video, real)
+    tl = res.rep["timeline"]
+    assert tl["simulated"] is True
+    ev, mk, st = lc.simulate_timeline(text)
+    kinds = list(lc.TIMELINE_KINDS)
+    assert [kinds.index(e[0]) for e in tl["events"]] == ev[:, 0].tolist()
+    assert [[e[1], e[2]] for e in tl["events"]] == ev[:, 1:3].tolist()
+    assert np.allclose([e[3] for e in tl["events"]], ev[:, 3] * 1e-6, rtol=1e-9, atol=1e-9)
+    assert abs(tl["makespan_ms"] - mk * 1e-6) <= 1e-6 * max(1.0, mk * 1e-6)
+    assert abs(tl["stall_ms"] - st * 1e-6) <= 1e-6 * max(1.0, st * 1e-6)
+    rj = harness.run_report(res)
+    assert rj["timeline"]["simulated"] is True
+    assert harness.ledger_summary(ctx)["clock"] == "virtual"
+    # the run's last ledger event (decode -> setup) carries the virtual
+    # clock after the denoising drain, the timeline's last event
+    last = float(harness.ledger_csv(ctx).splitlines()[-1].split(",")[1])
+    assert abs(last - mk * 1e-9) <= 1e-5 * mk * 1e-9
 
 
 def test_nonfinite_input_raises_shape_error(ctx):
