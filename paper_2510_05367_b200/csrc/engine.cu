@@ -665,7 +665,22 @@ Engine::Engine(int device) : device_(device) {
     LC_CUDA(cudaEventCreate(&ev_start_));
     for (int b = 0; b < 2; ++b) LC_CUDA(cudaEventCreateWithFlags(&ev_join_[b], cudaEventDisableTiming));
     LC_CUDA(cudaEventCreateWithFlags(&ev_vid_done_, cudaEventDisableTiming));
+    LC_CUDA(cudaStreamCreateWithFlags(&s_vid_, cudaStreamNonBlocking));
+    LC_CUDA(cudaEventCreateWithFlags(&ev_dl_gate_, cudaEventDisableTiming));
+    LC_CUDA(cudaEventCreateWithFlags(&ev_dl_done_, cudaEventDisableTiming));
+    LC_CUDA(cudaEventCreateWithFlags(&ev_dl_src_, cudaEventDisableTiming));
     if (const char* e = std::getenv("LC_NO_GRAPH")) use_graphs = (e[0] == '0');
+    // LC_DL_GATE = "<step>:<stem|d0|up|head>" or "off" (download right
+    // after the decode, per slice, as the synchronous run does)
+    if (const char* e = std::getenv("LC_DL_GATE")) {
+        const std::string g = e;
+        const auto colon = g.find(':');
+        if (g == "off" || colon == std::string::npos) dl_gate_step_ = -1;
+        else {
+            dl_gate_step_ = std::atoi(g.substr(0, colon).c_str());
+            dl_gate_where_ = g.substr(colon + 1);
+        }
+    }
 }
 
 Engine::~Engine() {
@@ -683,7 +698,12 @@ Engine::~Engine() {
     cudaEventDestroy(ev_start_);
     for (int b = 0; b < 2; ++b) cudaEventDestroy(ev_join_[b]);
     cudaEventDestroy(ev_vid_done_);
+    cudaEventDestroy(ev_dl_gate_);
+    cudaEventDestroy(ev_dl_done_);
+    cudaEventDestroy(ev_dl_src_);
     if (graph_exec_) cudaGraphExecDestroy(graph_exec_);
+    if (graph_) cudaGraphDestroy(graph_);
+    cudaStreamDestroy(s_vid_);
     cudaStreamDestroy(s_compute_);
     cudaStreamDestroy(s_d2h_);
     cudaStreamDestroy(s_h2d_);
@@ -725,6 +745,7 @@ static std::string weights_key(const RunConfig& c) {
 
 void Engine::configure(const RunConfig& cfg) {
     cfg.validate();
+    if (async_pending_) (void)wait();
     const std::string key = weights_key(cfg);
     const bool same_weights = configured_ && key == cfg_key_;
     const bool same_geom = configured_ && cfg.frames == cfg_.frames && cfg.height == cfg_.height &&
@@ -988,6 +1009,7 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
     const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
     auto cond = [&](int j, float* s, float* o) { block_conditioning(uw_, j, timestep, s, o); };
     float s, o;
+    dl_gate(step, "stem");
     // stem: CFG pair built on the fly (pipeline.cpp:127-131), affine + conv + SiLU
     {
         const int j = 0;
@@ -1021,6 +1043,7 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
         }
     }
     cond(1, &s, &o);
+    dl_gate(step, "d0");
     conv_block(1, stem_out_, lv_[0].D, s, o, true);
     const int deepest = full ? M - 1 : m;
     for (int i = 1; i <= deepest; ++i) {
@@ -1079,6 +1102,7 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
         return h;
     };
     const int top = full ? M - 1 : m;
+    dl_gate(step, "up");
     // Per-branch store (async swap, full step whose U_{m+1} is evicted): the
     // producing block u_{m+1} runs on the uncond half, then on the cond half,
     // so entry 0's eviction starts half a block earlier and overlaps the
@@ -1144,6 +1168,7 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
         if (writes_cache && i == m + 1 && seam == 3) cache_ready(-1);
     }
     // head: affine + conv, no SiLU -> eps (2,T,C,h,w) fp32
+    dl_gate(step, "head");
     {
         const int j = static_cast<int>(block_index(cfg_, "head"));
         cond(j, &s, &o);
@@ -1347,6 +1372,10 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
         LC_CUDA(cudaStreamIsCapturing(s_compute_, &cs));
         LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_vid_done_,
                                     cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0));
+        if (dl_capture_) {
+            if (!dl_fired_) fire_download();
+            LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_dl_done_, 0));
+        }
         slice_spans_.clear();
     }
     for (int64_t g0 = 0; g0 < n; g0 += G) {
@@ -1453,11 +1482,68 @@ void Engine::ensure_buf(DevBuf* b, int64_t bytes) {
 }
 
 void Engine::invalidate_graph() {
+    if (dl_pending_) {  // the device video may be about to move or be rewritten
+        flush_pending_download();
+        LC_CUDA(cudaStreamSynchronize(s_vid_));
+    }
     if (graph_exec_) {
         cudaGraphExecDestroy(graph_exec_);
         graph_exec_ = nullptr;
     }
+    if (graph_) {
+        cudaGraphDestroy(graph_);
+        graph_ = nullptr;
+    }
+    dl_node_ = nullptr;
     eager_runs_ = 0;
+}
+
+// ------------------------------------------------ deferred video download
+void Engine::dl_gate(int step, const char* where) {
+    if (dl_capture_ && !dl_fired_ && step == dl_gate_step_ && dl_gate_where_ == where) fire_download();
+}
+
+// Inside the capture: the previous run's video (still in video_) leaves for
+// the host on s_vid_ from this point of the body; the decode joins it before
+// overwriting video_.  The node's destination is a placeholder, re-pointed
+// per launch by arm_download_node().
+void Engine::fire_download() {
+    const size_t bytes = static_cast<size_t>(video_elems()) * 4;
+    if (!dl_scratch_.p || dl_scratch_.bytes < static_cast<int64_t>(bytes))
+        throw_invariant("deferred download: placeholder not allocated before capture");
+    LC_CUDA(cudaEventRecord(ev_dl_gate_, s_compute_));
+    LC_CUDA(cudaStreamWaitEvent(s_vid_, ev_dl_gate_, 0));
+    LC_CUDA(cudaMemcpyAsync(dl_scratch_.p, video_.p, bytes, cudaMemcpyDeviceToHost, s_vid_));
+    LC_CUDA(cudaEventRecord(ev_dl_done_, s_vid_));
+    dl_fired_ = true;
+}
+
+// Outside any graph: issue the pending download now (after everything queued
+// on the compute stream); the next body's decode waits on ev_vid_done_.
+void Engine::flush_pending_download() {
+    if (!dl_pending_) return;
+    LC_CUDA(cudaEventRecord(ev_dl_src_, s_compute_));
+    LC_CUDA(cudaStreamWaitEvent(s_vid_, ev_dl_src_, 0));
+    LC_CUDA(cudaMemcpyAsync(dl_pending_, video_.p, static_cast<size_t>(video_elems()) * 4, cudaMemcpyDeviceToHost,
+                            s_vid_));
+    LC_CUDA(cudaEventRecord(ev_vid_done_, s_vid_));
+    dl_pending_ = nullptr;
+}
+
+void Engine::arm_download_node() {
+    if (!dl_node_) {
+        flush_pending_download();
+        return;
+    }
+    if (dl_pending_) {
+        LC_CUDA(cudaGraphExecMemcpyNodeSetParams1D(graph_exec_, dl_node_, dl_pending_, video_.p,
+                                                   static_cast<size_t>(video_elems()) * 4,
+                                                   cudaMemcpyDeviceToHost));
+        LC_CUDA(cudaGraphNodeSetEnabled(graph_exec_, dl_node_, 1));
+        dl_pending_ = nullptr;
+    } else {
+        LC_CUDA(cudaGraphNodeSetEnabled(graph_exec_, dl_node_, 0));
+    }
 }
 
 // Ancestral per-step noise randn(derive_seed(seed, 0x1000 + s))
@@ -1597,6 +1683,12 @@ void Engine::enqueue_body(RunStats& st) {
     const bool swap = cfg_.cache_enabled && cfg_.swap_mode != SwapMode::Off;
     evict_pending_ = prefetch_pending_ = false;
     d2h_used_ = h2d_used_ = false;
+    {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        LC_CUDA(cudaStreamIsCapturing(s_compute_, &cs));
+        dl_capture_ = cs == cudaStreamCaptureStatusActive && dl_gate_step_ >= 0 && dl_gate_step_ < cfg_.steps;
+        dl_fired_ = false;
+    }
     host_valid_ = false;
     marks_.clear();
     ev_next_ = 0;
@@ -1674,6 +1766,7 @@ void Engine::enqueue_body(RunStats& st) {
     out_slices_ = true;
     decode_dev(xa, T, video_.as<float>());
     out_slices_ = false;
+    dl_capture_ = false;
     // join the copy streams that were used (required to close a graph
     // capture; the last eviction stays in flight through decode as in the
     // reference, proj/README.md "Swap schedule")
@@ -1743,11 +1836,18 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
     video_host_pinned_ = pinned;
     graph_slice_ = decode_slice;
     if (can_graph && graph_exec_) {
+        arm_download_node();
         LC_CUDA(cudaGraphLaunch(graph_exec_, s_compute_));
         st = graph_stats_;
         stats_ = &st;
     } else if (can_graph && eager_runs_ > 0) {
         cudaGraph_t g = nullptr;
+        // placeholder destination of the deferred-download node (no
+        // allocation may happen inside the capture); not a ledger buffer:
+        // steady-state launches re-point the node at the caller's memory
+        const int64_t vbytes = video_elems() * 4;
+        if (dl_gate_step_ >= 0 && (!dl_scratch_.p || dl_scratch_.bytes < vbytes))
+            dl_scratch_ = host_alloc(nullptr, vbytes);
         LC_CUDA(cudaStreamBeginCapture(s_compute_, cudaStreamCaptureModeThreadLocal));
         try {
             enqueue_body(st);
@@ -1757,11 +1857,27 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
             throw;
         }
         LC_CUDA(cudaStreamEndCapture(s_compute_, &g));
+        // the deferred-download memcpy node (source: the device video)
+        dl_node_ = nullptr;
+        size_t nn = 0;
+        LC_CUDA(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        if (nn) LC_CUDA(cudaGraphGetNodes(g, nodes.data(), &nn));
+        for (cudaGraphNode_t nd : nodes) {
+            cudaGraphNodeType ty;
+            LC_CUDA(cudaGraphNodeGetType(nd, &ty));
+            if (ty != cudaGraphNodeTypeMemcpy) continue;
+            cudaMemcpy3DParms mp{};
+            LC_CUDA(cudaGraphMemcpyNodeGetParams(nd, &mp));
+            if (mp.srcPtr.ptr == video_.p && dl_scratch_.p && mp.dstPtr.ptr == dl_scratch_.p) dl_node_ = nd;
+        }
         LC_CUDA(cudaGraphInstantiate(&graph_exec_, g, 0));
-        LC_CUDA(cudaGraphDestroy(g));
+        graph_ = g;
         graph_stats_ = st;
+        arm_download_node();
         LC_CUDA(cudaGraphLaunch(graph_exec_, s_compute_));
     } else {
+        flush_pending_download();
         enqueue_body(st);
         ++eager_runs_;
     }
@@ -1785,8 +1901,10 @@ void Engine::run_e2e_async(const float* x0_pinned, float* video_pinned) {
     LC_CUDA(cudaEventRecord(ev_start_, s_compute_));
     LC_CUDA(cudaMemcpyAsync(x_.p, x0_pinned, static_cast<size_t>(latent_elems()) * 4, cudaMemcpyHostToDevice,
                             s_compute_));
+    arm_download_node();  // the previous run's video leaves inside this one
     LC_CUDA(cudaGraphLaunch(graph_exec_, s_compute_));
-    enqueue_video_out(video_pinned);
+    if (dl_node_) dl_pending_ = video_pinned;
+    else enqueue_video_out(video_pinned);
     async_pending_ = true;
 }
 
@@ -1806,6 +1924,7 @@ void Engine::run_resident_async() {
     LC_CUDA(cudaEventRecord(ev_start_, s_compute_));
     LC_CUDA(cudaMemcpyAsync(x_.p, x0_.p, static_cast<size_t>(latent_elems()) * 4, cudaMemcpyDeviceToDevice,
                             s_compute_));
+    arm_download_node();
     LC_CUDA(cudaGraphLaunch(graph_exec_, s_compute_));
     async_pending_ = true;
 }
@@ -1813,6 +1932,7 @@ void Engine::run_resident_async() {
 RunStats Engine::wait() {
     if (!async_pending_) return last_async_;
     async_pending_ = false;
+    flush_pending_download();
     video_host_pinned_ = nullptr;
     RunStats st = graph_stats_;
     stats_ = &st;
@@ -1838,6 +1958,7 @@ RunStats Engine::finish_run(RunStats st, float* video_host, float* latent_host) 
     LC_CUDA(cudaStreamSynchronize(s_compute_));
     LC_CUDA(cudaStreamSynchronize(s_d2h_));
     LC_CUDA(cudaStreamSynchronize(s_h2d_));
+    LC_CUDA(cudaStreamSynchronize(s_vid_));
     stats_ = nullptr;
     video_host_pinned_ = nullptr;  // operator-level decode() must not stream to it
     if (bad) throw_shape("denoiser input contains non-finite values");
@@ -1892,6 +2013,7 @@ RunStats Engine::finish_run(RunStats st, float* video_host, float* latent_host) 
 
 void Engine::forward(const float* x_host, int64_t T, int64_t timestep, const float* deep_in_ref,
                      float* deep_out_ref, float* eps_host) {
+    if (async_pending_) (void)wait();
     RunConfig c = cfg_;
     if (c.frames != T) {
         c.frames = T;
@@ -1940,6 +2062,7 @@ void Engine::forward(const float* x_host, int64_t T, int64_t timestep, const flo
 }
 
 void Engine::decode(const float* lat_host, int64_t n, float* video_host, int64_t slice) {
+    if (async_pending_) (void)wait();
     const int C = static_cast<int>(cfg_.latent_channels);
     const int64_t nl = n * C * cfg_.latent_h() * cfg_.latent_w();
     const int64_t nv = n * cfg_.image_channels * cfg_.height * cfg_.width;
@@ -1966,6 +2089,7 @@ namespace lc {
 
 void Engine::decode_sharded(const float* lat_host, int64_t T, int64_t slice, float* video_host,
                             ncclComm_t comm, int world, int rank, float* ms_out) {
+    if (async_pending_) (void)wait();
     const int C = static_cast<int>(cfg_.latent_channels);
     const int64_t lat_frame = C * cfg_.latent_h() * cfg_.latent_w();
     const int64_t vid_frame = cfg_.image_channels * cfg_.height * cfg_.width;

@@ -328,6 +328,24 @@ private:
     std::vector<std::pair<int64_t, int64_t>> slice_spans_;  // decoded slices (first frame, frames)
     void enqueue_video_out(float* pinned);
     float* x_final_ = nullptr;
+    // Deferred video download (pipelined e2e): run k's video is copied to its
+    // pinned destination by a memcpy node inside run k+1's graph, released at
+    // a gate point of k+1's body (compute-bound blocks, away from the
+    // memory-bound ones the host-link DMA slows down); the node is re-pointed
+    // (or disabled) before each launch, wait() flushes the last one.
+    cudaStream_t s_vid_ = nullptr;
+    cudaEvent_t ev_dl_gate_ = nullptr, ev_dl_done_ = nullptr, ev_dl_src_ = nullptr;
+    bool dl_capture_ = false, dl_fired_ = false;
+    int dl_gate_step_ = 0;
+    std::string dl_gate_where_ = "stem";  // measured: 0:stem ~ 0:d0 > off > later gates (B e2e)
+    DevBuf dl_scratch_;                    // pinned capture placeholder of the node's destination
+    cudaGraph_t graph_ = nullptr;          // kept alive: dl_node_ belongs to it
+    cudaGraphNode_t dl_node_ = nullptr;
+    float* dl_pending_ = nullptr;          // pinned destination of a not yet issued download
+    void dl_gate(int step, const char* where);
+    void fire_download();
+    void flush_pending_download();
+    void arm_download_node();              // before a graph launch
     cudaGraphExec_t graph_exec_ = nullptr;
     RunStats graph_stats_;
     int eager_runs_ = 0;

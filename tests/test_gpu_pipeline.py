@@ -231,16 +231,38 @@ def test_graph_replay_is_bit_identical(ctx, oracle, kind, extra):
         vid.array[:] = -1.0
         ctx.run_e2e(x0, vid)
         assert np.array_equal(vid.array.reshape(outs[0][0].shape), outs[0][0])
-    # queued pinned runs: each download overlaps the next run's compute
-    vid2 = lc.PinnedArray(ctx.video_elems())
-    vid.array[:] = -1.0
-    vid2.array[:] = -1.0
-    for k in range(4):
-        ctx.run_e2e_async(x0, vid if k % 2 == 0 else vid2)
+    # queued pinned runs: run k's video leaves inside run k+1 (deferred
+    # download node) or at wait(); alternate two inputs so a download that
+    # read the wrong run's video is caught
+    x0b = lc.PinnedArray(ctx.latent_elems())
+    x0b.array[:] = lc.randn(12345, ctx.latent_elems())
+    ctx.run_e2e(x0b, vid)
+    want_b = vid.array.copy()
+    want_a = outs[0][0].reshape(-1)
+    assert not np.array_equal(want_a, want_b)
+    vids = [lc.PinnedArray(ctx.video_elems()) for _ in range(5)]
+    for v in vids:
+        v.array[:] = -1.0
+    for k in range(5):
+        ctx.run_e2e_async(x0 if k % 2 == 0 else x0b, vids[k])
     ctx.wait()
-    assert np.array_equal(vid.array.reshape(outs[0][0].shape), outs[0][0])
-    assert np.array_equal(vid2.array.reshape(outs[0][0].shape), outs[0][0])
-    vid2.free()
+    for k in range(5):
+        assert np.array_equal(vids[k].array, want_a if k % 2 == 0 else want_b), k
+    # a pending download survives a different kind of launch in between
+    vids[0].array[:] = -1.0
+    ctx.run_e2e_async(x0b, vids[0])
+    ctx.run_resident_async()
+    ctx.wait()
+    assert np.array_equal(vids[0].array, want_b)
+    assert np.array_equal(ctx.download_video().reshape(-1), want_a)
+    vids[1].array[:] = -1.0
+    ctx.run_e2e_async(x0b, vids[1])
+    v_sync, _, _ = ctx.run_pipeline()  # synchronous run after a queued one
+    assert np.array_equal(vids[1].array, want_b)
+    assert np.array_equal(v_sync.reshape(-1), want_a)
+    for v in vids:
+        v.free()
+    x0b.free()
     x0.free()
     vid.free()
 
