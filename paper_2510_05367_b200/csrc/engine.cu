@@ -138,6 +138,12 @@ bool tap_gather_enabled() {
     return on;
 }
 
+// LC_SUBPIX_FUSED=0 runs the decoder's last stage as tap-to-N conv + gather (A/B)
+bool subpix_fused_enabled() {
+    static const bool on = !(std::getenv("LC_SUBPIX_FUSED") && std::atoi(std::getenv("LC_SUBPIX_FUSED")) == 0);
+    return on;
+}
+
 // LC_TMA_STORE=0 turns the TMA-store epilogue off (A/B timing)
 bool tma_store_enabled() {
     static const bool on = !(std::getenv("LC_TMA_STORE") && std::atoi(std::getenv("LC_TMA_STORE")) == 0);
@@ -818,8 +824,22 @@ void Engine::configure(const RunConfig& cfg) {
             }
             const Bank& db = cw_.dec[static_cast<size_t>(cfg.stages)];
             dec_last_tap_tc_.reset();
+            dec_last_w16_.reset();
+            dec_last_kb_ = 0;
             if (db.k == 3 && db.c_out <= 4) {
-                dec_last_tap_tc_ = pack_tc_layer(&ledger_, subpix_tap_bank(db), static_cast<int>(db.c_in), 0);
+                const Bank tb = subpix_tap_bank(db);
+                dec_last_tap_tc_ = pack_tc_layer(&ledger_, tb, static_cast<int>(db.c_in), 0);
+                dec_last_kb_ = static_cast<int>((tb.c_in + 63) / 64);
+                if (dec_last_kb_ <= 4) {
+                    const int kp = 64 * dec_last_kb_;
+                    std::vector<__half> w16(static_cast<size_t>(tb.c_out * kp), __float2half_rn(0.0f));
+                    for (int64_t r = 0; r < tb.c_out; ++r)
+                        for (int64_t ic = 0; ic < tb.c_in; ++ic)
+                            w16[static_cast<size_t>(r * kp + ic)] =
+                                __float2half_rn(tb.taps[static_cast<size_t>(r * tb.c_in + ic)]);
+                    dec_last_w16_ = dev_alloc(&ledger_, static_cast<int64_t>(w16.size() * 2), false);
+                    LC_CUDA(cudaMemcpy(dec_last_w16_.p, w16.data(), w16.size() * 2, cudaMemcpyHostToDevice));
+                }
                 dec_last_bias_ = dev_alloc(&ledger_, static_cast<int64_t>(db.bias.size() * 4), false);
                 LC_CUDA(cudaMemcpy(dec_last_bias_.p, db.bias.data(), db.bias.size() * 4, cudaMemcpyHostToDevice));
             }
@@ -1422,7 +1442,31 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
         vid.h = H;
         vid.w = W;
         vid.c = IC;
-        if (dec_last_tap_tc_ && tap_gather_enabled()) {
+        if (dec_last_w16_.p && subpix_fused_enabled()) {
+            // K8: upsample + conv + bias + depth-to-space in one kernel
+            const Act& a = e[S - 1];
+            SubpixTcParams q{};
+            const uint64_t dims[4] = {static_cast<uint64_t>(a.cs), static_cast<uint64_t>(wl), static_cast<uint64_t>(hl),
+                                      static_cast<uint64_t>(gs)};
+            const uint64_t strides[3] = {static_cast<uint64_t>(a.cs) * 2, static_cast<uint64_t>(wl) * a.cs * 2,
+                                         static_cast<uint64_t>(hl) * wl * a.cs * 2};
+            const uint32_t box[4] = {64, kSubpixSX, kSubpixSY, 1};
+            const uint32_t estr[4] = {1, 1, 1, 1};
+            encode_map(&q.tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, a.p, dims, strides, box, estr);
+            q.w = dec_last_w16_.as<__half>();
+            q.bias = dec_last_bias_.as<float>();
+            q.out = video_dev + g0 * IC * H * W;
+            q.n = gs;
+            q.H = hl;
+            q.W = wl;
+            q.C = IC;
+            q.kb = dec_last_kb_;
+            q.tiles_x = (wl + kSubpixTX - 1) / kSubpixTX;
+            q.tiles_y = (hl + kSubpixTY - 1) / kSubpixTY;
+            q.num_tiles = gs * q.tiles_x * q.tiles_y;
+            LC_CUDA(launch_subpix_tc(q, s_compute_));
+            ++launches;
+        } else if (dec_last_tap_tc_ && tap_gather_enabled()) {
             Act yv;
             yv.n = gs;
             yv.h = hl;

@@ -54,6 +54,10 @@ def _run(ctx, over, **kw):
     dict(TINY, **{"run.mode": "image"}),
     dict(TINY, **{"run.mode": "image", "sampler.kind": "ancestral", "codec.stages": 3, "run.height": 64,
                   "run.width": 64}),
+    # K8 (fused last decoder stage): partial tiles in x and y, one and three
+    # 64-channel K blocks
+    dict(TINY, **{"run.frames": 3, "run.height": 96, "run.width": 160, "sampler.steps": 3, "codec.width": 64}),
+    dict(TINY, **{"run.height": 64, "run.width": 64, "sampler.steps": 2, "codec.width": 192}),
 ])
 def test_pipeline_matches_oracle(ctx, oracle, over):
     video, lat, rep = _run(ctx, over)
