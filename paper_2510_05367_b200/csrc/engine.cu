@@ -423,6 +423,22 @@ Bank tap_bank(const Bank& b) {
     return t;
 }
 
+// K8 operand: a tap bank's rows as fp16 [round_up(rows, 16)][kb * 64], zero padded.
+DevBuf pack_tap_w16(Ledger* l, const Bank& tb, int* kb_out, int* n_out) {
+    const int kb = static_cast<int>((tb.c_in + 63) / 64);
+    const int n = static_cast<int>((tb.c_out + 15) / 16 * 16);
+    const int kp = 64 * kb;
+    std::vector<__half> w16(static_cast<size_t>(n) * kp, __float2half_rn(0.0f));
+    for (int64_t r = 0; r < tb.c_out; ++r)
+        for (int64_t ic = 0; ic < tb.c_in; ++ic)
+            w16[static_cast<size_t>(r * kp + ic)] = __float2half_rn(tb.taps[static_cast<size_t>(r * tb.c_in + ic)]);
+    DevBuf b = dev_alloc(l, static_cast<int64_t>(w16.size() * 2), false);
+    LC_CUDA(cudaMemcpy(b.p, w16.data(), w16.size() * 2, cudaMemcpyHostToDevice));
+    *kb_out = kb;
+    *n_out = n;
+    return b;
+}
+
 // Sub-pixel tap-to-N bank of nearest-upsample + 3x3 (the last decoder conv):
 // output channel (p*4 + t)*C + c = merged weights of parity p = (py, px) and
 // low-res tap t = (dy, dx) (see launch_subpix_gather; written channel-planar).
@@ -807,8 +823,15 @@ void Engine::configure(const RunConfig& cfg) {
         {
             const Bank& hb = uw_.banks.back();
             head_tap_tc_.reset();
+            head_w16_.reset();
+            head_kb_ = head_n_ = 0;
             if (hb.c_out <= 4 && hb.k * hb.k * hb.c_out <= 256) {
-                head_tap_tc_ = pack_tc_layer(&ledger_, tap_bank(hb), static_cast<int>(hb.c_in), 0);
+                const Bank tb = tap_bank(hb);
+                head_tap_tc_ = pack_tc_layer(&ledger_, tb, static_cast<int>(hb.c_in), 0);
+                if (hb.k == 3 && tap_tc_supported(kTapConv3, static_cast<int>(hb.c_out),
+                                                  static_cast<int>((tb.c_in + 63) / 64),
+                                                  static_cast<int>((tb.c_out + 15) / 16 * 16)))
+                    head_w16_ = pack_tap_w16(&ledger_, tb, &head_kb_, &head_n_);
                 const int64_t kk = hb.k * hb.k;
                 std::vector<float> ws(static_cast<size_t>(kk * hb.c_out));
                 for (int64_t tp = 0; tp < kk; ++tp)
@@ -829,16 +852,10 @@ void Engine::configure(const RunConfig& cfg) {
             if (db.k == 3 && db.c_out <= 4) {
                 const Bank tb = subpix_tap_bank(db);
                 dec_last_tap_tc_ = pack_tc_layer(&ledger_, tb, static_cast<int>(db.c_in), 0);
-                dec_last_kb_ = static_cast<int>((tb.c_in + 63) / 64);
-                if (dec_last_kb_ <= 4) {
-                    const int kp = 64 * dec_last_kb_;
-                    std::vector<__half> w16(static_cast<size_t>(tb.c_out * kp), __float2half_rn(0.0f));
-                    for (int64_t r = 0; r < tb.c_out; ++r)
-                        for (int64_t ic = 0; ic < tb.c_in; ++ic)
-                            w16[static_cast<size_t>(r * kp + ic)] =
-                                __float2half_rn(tb.taps[static_cast<size_t>(r * tb.c_in + ic)]);
-                    dec_last_w16_ = dev_alloc(&ledger_, static_cast<int64_t>(w16.size() * 2), false);
-                    LC_CUDA(cudaMemcpy(dec_last_w16_.p, w16.data(), w16.size() * 2, cudaMemcpyHostToDevice));
+                if (tap_tc_supported(kTapSubpix, static_cast<int>(db.c_out), static_cast<int>((tb.c_in + 63) / 64),
+                                     static_cast<int>((tb.c_out + 15) / 16 * 16))) {
+                    int nn = 0;
+                    dec_last_w16_ = pack_tap_w16(&ledger_, tb, &dec_last_kb_, &nn);
                 }
                 dec_last_bias_ = dev_alloc(&ledger_, static_cast<int64_t>(db.bias.size() * 4), false);
                 LC_CUDA(cudaMemcpy(dec_last_bias_.p, db.bias.data(), db.bias.size() * 4, cudaMemcpyHostToDevice));
@@ -1197,7 +1214,38 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
         eps_view.h = lh;
         eps_view.w = lw;
         eps_view.c = head_tc_->c_out;
-        if (head_tap_tc_ && tap_gather_enabled()) {
+        if (head_w16_.p && subpix_fused_enabled()) {
+            // K8: tap-to-N GEMM over a halo window + in-window tap sums, fused
+            const Act& a = lv_[0].U;
+            const uint64_t dims[4] = {static_cast<uint64_t>(a.cs), static_cast<uint64_t>(lw), static_cast<uint64_t>(lh),
+                                      static_cast<uint64_t>(a.n)};
+            const uint64_t strides[3] = {static_cast<uint64_t>(a.cs) * 2, static_cast<uint64_t>(lw) * a.cs * 2,
+                                         static_cast<uint64_t>(lh) * lw * a.cs * 2};
+            const uint32_t box[4] = {64, kTapSX, static_cast<uint32_t>(tap_stage_sy(kTapConv3)), 1};
+            const uint32_t estr[4] = {1, 1, 1, 1};
+            TapTcParams q{};
+            encode_map(&q.tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, a.p, dims, strides, box, estr);
+            q.w = head_w16_.as<__half>();
+            q.bias = head_bias_.as<float>();
+            q.wsum = head_wsum_.as<float>();
+            q.scale = s;
+            q.shift = o;
+            q.out = eps2_dev;
+            q.n = a.n;
+            q.H = lh;
+            q.W = lw;
+            q.C = static_cast<int>(head_tc_->c_out);
+            q.N = head_n_;
+            q.kb = head_kb_;
+            for (const Window& wd : block_windows(cfg_, "head", lh, lw)) {
+                q.win = wd;
+                q.tiles_x = (wd.ox1 - wd.ox0 + kTapTX - 1) / kTapTX;
+                q.tiles_y = (wd.oy1 - wd.oy0 + tap_tile_ty(kTapConv3) - 1) / tap_tile_ty(kTapConv3);
+                q.num_tiles = a.n * q.tiles_x * q.tiles_y;
+                LC_CUDA(launch_tap_tc(kTapConv3, q, s_compute_));
+                ++launches;
+            }
+        } else if (head_tap_tc_ && tap_gather_enabled()) {
             // tap-to-N: one K = c_in GEMM over the materialised window into
             // y[px][tap*C + c], then the tap gather adds the in-window taps
             Act yv;
@@ -1445,12 +1493,12 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
         if (dec_last_w16_.p && subpix_fused_enabled()) {
             // K8: upsample + conv + bias + depth-to-space in one kernel
             const Act& a = e[S - 1];
-            SubpixTcParams q{};
+            TapTcParams q{};
             const uint64_t dims[4] = {static_cast<uint64_t>(a.cs), static_cast<uint64_t>(wl), static_cast<uint64_t>(hl),
                                       static_cast<uint64_t>(gs)};
             const uint64_t strides[3] = {static_cast<uint64_t>(a.cs) * 2, static_cast<uint64_t>(wl) * a.cs * 2,
                                          static_cast<uint64_t>(hl) * wl * a.cs * 2};
-            const uint32_t box[4] = {64, kSubpixSX, kSubpixSY, 1};
+            const uint32_t box[4] = {64, kTapSX, static_cast<uint32_t>(tap_stage_sy(kTapSubpix)), 1};
             const uint32_t estr[4] = {1, 1, 1, 1};
             encode_map(&q.tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, a.p, dims, strides, box, estr);
             q.w = dec_last_w16_.as<__half>();
@@ -1460,11 +1508,13 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
             q.H = hl;
             q.W = wl;
             q.C = IC;
+            q.N = 16 * IC;
             q.kb = dec_last_kb_;
-            q.tiles_x = (wl + kSubpixTX - 1) / kSubpixTX;
-            q.tiles_y = (hl + kSubpixTY - 1) / kSubpixTY;
+            q.win = Window{0, hl, 0, wl, 0, hl, 0, wl};
+            q.tiles_x = (wl + kTapTX - 1) / kTapTX;
+            q.tiles_y = (hl + tap_tile_ty(kTapSubpix) - 1) / tap_tile_ty(kTapSubpix);
             q.num_tiles = gs * q.tiles_x * q.tiles_y;
-            LC_CUDA(launch_subpix_tc(q, s_compute_));
+            LC_CUDA(launch_tap_tc(kTapSubpix, q, s_compute_));
             ++launches;
         } else if (dec_last_tap_tc_ && tap_gather_enabled()) {
             Act yv;

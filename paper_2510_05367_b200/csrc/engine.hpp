@@ -271,8 +271,8 @@ private:
     // columns + a gather kernel (launch_tap_gather / launch_subpix_gather)
     std::unique_ptr<TcLayer> head_tap_tc_, dec_last_tap_tc_;
     DevBuf head_wsum_, head_bias_, dec_last_bias_, head_y_buf_, dec_y_buf_;
-    DevBuf dec_last_w16_;  // K8 tap bank, fp16 [16*C][kb*64]
-    int dec_last_kb_ = 0;
+    DevBuf dec_last_w16_, head_w16_;  // K8 tap banks, fp16 [N][kb*64]
+    int dec_last_kb_ = 0, head_kb_ = 0, head_n_ = 0;
     DevBuf shard_lat_, shard_vid_;  // decode_sharded buffers
     // encoder (image mode, codec.cpp:64-81): patch GEMM + [down2 + conv]xS
     std::unique_ptr<TcLayer> enc0_tc_;

@@ -1,19 +1,25 @@
-// K8: fused last decoder stage (see subpix_tc.cuh).
+// K8: fused tap-to-N convolutions (see subpix_tc.cuh).
 //
-// Tile: kSubpixTY x kSubpixTX low-res pixels of one frame.  The TMA box
-// stages the (TY+2) x (TX+2) window around it (out-of-image pixels are
-// zero-filled, which is the conv's zero padding); its pixels, flattened
-// row-major, are the M rows of the GEMM y = window x tapbank^T (N = 16*C,
-// K = c_in), 4 M-tiles of 128 (462 staged pixels), fp32 in TMEM.  Output
-// pixel (2Y+py, 2X+px) = bias + sum over its 2x2 source taps t = (dy,dx) of
-// y[pixel (Y+dy-1+py, X+dx-1+px)][(p*4+t)*C + c] -- the same sums, in the
-// same order, as the tap-to-N GEMM + subpix_gather_kernel pair it replaces.
+// Tile: 5 x 64 pixels of one image (low-res pixels for the decoder).  The
+// TMA box stages the 7 x 66 window around it (out-of-image pixels are
+// zero-filled); its 462 pixels, flattened row-major, are the M rows (4
+// M-tiles of 128) of the GEMM y = window x tapbank^T, fp32 in TMEM.  Then
+//   decoder: out(2Y+py, 2X+px) = bias + sum_{t=(dy,dx)} y[(Y+dy-1+py, X+dx-1+px)][(p*4+t)*C + c]
+//   head:    out(Y, X) = sum_{in-window taps} s*y[(Y+ky-1, X+kx-1)][t*C + c]
+//                        + o * sum_{in-window taps} wsum[t][c] + bias[c]
+// -- the sums, in the order, of the tap-to-N GEMM + gather kernel pairs
+// these replace (kernels.cu tap_gather_kernel / subpix_gather_kernel).
 //
 // Warps: 0 TMA producer, 1 MMA issuer (+ TMEM owner), 2..9 epilogue.  Two
 // A stages (one 64-channel K block each) and two TMEM accumulators, so the
 // loads and MMAs of tile i+1 run under the epilogue of tile i.  Epilogue per
-// output parity: TMEM -> shared (the parity's 4*C columns of every staged
-// pixel), barrier, gather + coalesced planar stores, barrier.
+// tile: all tap columns of every staged pixel TMEM -> shared (the
+// accumulator is released right after), barrier, gather + coalesced planar
+// stores (decoder: both column parities of an output row as one float2),
+// barrier.  A first version with one epilogue pass per output parity (four
+// barrier pairs per tile, bias/wsum re-read per output) ran the decoder
+// stage at 6.9 us per tile, 22 % of HBM bandwidth; a third A stage did not
+// change that.
 #include "subpix_tc.cuh"
 
 #include "pdl.cuh"
@@ -23,20 +29,33 @@ namespace lc {
 
 namespace {
 
-constexpr int kNPix = kSubpixSX * kSubpixSY;     // 462 staged pixels
-constexpr int kMT = (kNPix + 127) / 128;         // 4 M-tiles
-constexpr int kABytes = kMT * 128 * 128;         // one A stage (64 channels x 512 rows)
+// Per mode: staged pixels, M-tiles of 128, A stage stride.  The MMA of the
+// last M-tile reads past the staged rows into the next stage (or the tap
+// bank): those rows only feed accumulator rows that are never read.
+template <int MODE> struct Geo {
+    static constexpr int TY = tap_tile_ty(MODE), SY = tap_stage_sy(MODE);
+    static constexpr int NPix = kTapSX * SY;                   // decoder 462, head 330
+    static constexpr int MT = (NPix + 127) / 128;              // 4, 3
+    static constexpr int ABytes = (NPix * 128 + 1023) / 1024 * 1024;
+};
 constexpr int kStages = 2;
+constexpr int kMaxPC = 48;  // tap columns per staged pixel (decoder 16*3, head 9*4)
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 32 * (2 + kEpiWarps);
-constexpr int kMaxKb = 4;
 constexpr int kAccCols = 256;                    // TMEM columns per accumulator buffer
+constexpr int kSmemMax = 232448;
 
-__host__ __device__ constexpr int y_stride(int C) { return C == 1 ? 4 : C == 4 ? 20 : 12; }
-
-constexpr int kWBytesMax = kMaxKb * 64 * 128;
-constexpr int kYBytesMax = kNPix * 20 * 4;
-constexpr int kSmem = 1024 + kStages * kABytes + kWBytesMax + kYBytesMax + 256;
+// shared-memory row stride (floats) of one staged pixel's pass columns:
+// a multiple of 4 whose lane stride spreads 8 consecutive lanes' 16-byte
+// stores over distinct bank quads
+__host__ __device__ constexpr int y_stride(int mode, int C) {
+    return mode == kTapSubpix ? (C == 1 ? 20 : C == 2 ? 36 : 52) : (C == 1 ? 12 : C == 2 ? 20 : C == 3 ? 28 : 36);
+}
+__host__ __device__ constexpr int pass_cols(int mode, int C) { return mode == kTapSubpix ? 16 * C : 9 * C; }
+template <int MODE>
+int smem_bytes(const TapTcParams& p) {
+    return 1024 + kStages * Geo<MODE>::ABytes + p.kb * p.N * 128 + Geo<MODE>::NPix * y_stride(MODE, p.C) * 4 + 512;
+}
 
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&v)[4]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
@@ -44,22 +63,27 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&v)[4]) {
                  : "r"(taddr));
 }
 
-__global__ void __launch_bounds__(kThreads, 1) subpix_tc_kernel(const __grid_constant__ SubpixTcParams p) {
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_constant__ TapTcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
+    constexpr int kNPix = Geo<MODE>::NPix, kMT = Geo<MODE>::MT, kABytes = Geo<MODE>::ABytes;
+    constexpr int kTapTY = Geo<MODE>::TY;
+    const int C = p.C, N = p.N, YS = y_stride(MODE, C), PC = pass_cols(MODE, C);
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* smA = smem;
     uint8_t* smW = smA + kStages * kABytes;
-    float* smY = reinterpret_cast<float*>(smW + kWBytesMax);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(smY) + kYBytesMax);
-    uint64_t* full_bar = bars;            // [kStages]
-    uint64_t* empty_bar = bars + 2;       // [kStages]
-    uint64_t* tfull = bars + 4;           // [2]
-    uint64_t* tempty = bars + 6;          // [2]
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 8);
+    float* smY = reinterpret_cast<float*>(smW + p.kb * N * 128);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(smY) + kNPix * YS * 4);
+    uint64_t* full_bar = bars;                  // [kStages]
+    uint64_t* empty_bar = bars + kStages;       // [kStages]
+    uint64_t* tfull = bars + 2 * kStages;       // [2]
+    uint64_t* tempty = bars + 2 * kStages + 2;  // [2]
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+    float* sm_bias = reinterpret_cast<float*>(bars + 2 * kStages + 6);  // [4]
+    float* sm_wsum = sm_bias + 4;                                       // [9][C]
 
     const int warp = __shfl_sync(0xffffffff, static_cast<int>(threadIdx.x) / 32, 0);
     const int lane = static_cast<int>(threadIdx.x) & 31;
-    const int C = p.C, N = 16 * C, YS = y_stride(C);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -84,6 +108,8 @@ __global__ void __launch_bounds__(kThreads, 1) subpix_tc_kernel(const __grid_con
             sts128u(smem_u32(smW + k * N * 128 + r * 128 + ((j ^ (r & 7)) << 4)), v);
         }
         fence_proxy_async_smem();
+        if (threadIdx.x < 4) sm_bias[threadIdx.x] = static_cast<int>(threadIdx.x) < C ? p.bias[threadIdx.x] : 0.f;
+        if (MODE == kTapConv3 && static_cast<int>(threadIdx.x) < 9 * C) sm_wsum[threadIdx.x] = p.wsum[threadIdx.x];
     }
     tc_fence_before();
     __syncthreads();
@@ -97,8 +123,8 @@ __global__ void __launch_bounds__(kThreads, 1) subpix_tc_kernel(const __grid_con
         n = tile / tiles_per_img;
         const int r = tile - n * tiles_per_img;
         const int ty = r / p.tiles_x;
-        Y0 = ty * kSubpixTY;
-        X0 = (r - ty * p.tiles_x) * kSubpixTX;
+        Y0 = p.win.oy0 + ty * kTapTY;
+        X0 = p.win.ox0 + (r - ty * p.tiles_x) * kTapTX;
     };
 
     if (warp == 0) {
@@ -152,11 +178,11 @@ __global__ void __launch_bounds__(kThreads, 1) subpix_tc_kernel(const __grid_con
         const int g = e >> 2;                   // M-tiles g, g+2
         const int et = static_cast<int>(threadIdx.x) - 64;
         const uint32_t ybase = smem_u32(smY);
-        float bias[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) bias[c] = c < C ? __ldg(p.bias + c) : 0.f;
-        const int H2 = 2 * p.H, W2 = 2 * p.W;
-        const size_t plane = static_cast<size_t>(H2) * W2;
+        const float yscale = MODE == kTapConv3 ? p.scale : 1.0f;
+        const int nld = (PC + 3) / 4;
+        const int OH = MODE == kTapSubpix ? 2 * p.H : p.H, OW = MODE == kTapSubpix ? 2 * p.W : p.W;
+        const size_t plane = static_cast<size_t>(OH) * OW;
+        constexpr int kTilePx = kTapTY * kTapTX;
         int lt = 0;
         for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++lt) {
             const int buf = lt & 1;
@@ -164,53 +190,82 @@ __global__ void __launch_bounds__(kThreads, 1) subpix_tc_kernel(const __grid_con
             tile_origin(tile, n, Y0, X0);
             mbar_wait(&tfull[buf], (lt >> 1) & 1);
             tc_fence_after();
-            for (int par = 0; par < 4; ++par) {
-                const int py = par >> 1, px = par & 1;
-                // this parity's 4*C columns of every staged pixel -> shared
-                for (int mt = g; mt < kMT; mt += 2) {
-                    const int q = mt * 128 + qd * 32 + lane;
-                    const uint32_t ta = tmem_base + (static_cast<uint32_t>(qd * 32) << 16) +
-                                        static_cast<uint32_t>(buf * kAccCols + mt * N + par * 4 * C);
-                    uint32_t v[16];
+            // every staged pixel's tap columns -> shared (all loads in flight, one wait)
+            for (int mt = g; mt < kMT; mt += 2) {
+                const int q = mt * 128 + qd * 32 + lane;
+                const uint32_t ta = tmem_base + (static_cast<uint32_t>(qd * 32) << 16) +
+                                    static_cast<uint32_t>(buf * kAccCols + mt * N);
+                uint32_t v[kMaxPC];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        if (j < C) tmem_ld4(ta + 4 * j, *reinterpret_cast<uint32_t(*)[4]>(&v[4 * j]));
-                    tmem_ld_wait();
-                    if (q < kNPix) {
+                for (int j = 0; j < kMaxPC / 4; ++j)
+                    if (j < nld) tmem_ld4(ta + 4 * j, *reinterpret_cast<uint32_t(*)[4]>(&v[4 * j]));
+                tmem_ld_wait();
+                if (q < kNPix) {
 #pragma unroll
-                        for (int j = 0; j < 4; ++j)
-                            if (j < C)
-                                sts128u(ybase + static_cast<uint32_t>((q * YS + 4 * j) * 4),
-                                        make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-                    }
+                    for (int j = 0; j < kMaxPC / 4; ++j)
+                        if (j < nld)
+                            sts128(ybase + static_cast<uint32_t>((q * YS + 4 * j) * 4),
+                                   make_float4(__uint_as_float(v[4 * j]) * yscale, __uint_as_float(v[4 * j + 1]) * yscale,
+                                               __uint_as_float(v[4 * j + 2]) * yscale,
+                                               __uint_as_float(v[4 * j + 3]) * yscale));
                 }
-                named_bar_sync(1, 32 * kEpiWarps);
-                // gather: out(2Y+py, 2X+px) = bias + sum_t y[src(t)][t*C + c]
-                for (int i = et; i < kSubpixTY * kSubpixTX; i += 32 * kEpiWarps) {
-                    const int ry = i / kSubpixTX, rx = i - ry * kSubpixTX;
-                    const int Y = Y0 + ry, X = X0 + rx;
-                    if (Y >= p.H || X >= p.W) continue;
-                    float acc[4];
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) acc[c] = bias[c];
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        const int q = (ry + (t >> 1) + py) * kSubpixSX + rx + (t & 1) + px;
-                        const float* yp = smY + q * YS + t * C;
-#pragma unroll
-                        for (int c = 0; c < 4; ++c)
-                            if (c < C) acc[c] += yp[c];
-                    }
-                    float* o = p.out + static_cast<size_t>(n) * C * plane + static_cast<size_t>(2 * Y + py) * W2 + 2 * X + px;
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        if (c < C) o[c * plane] = acc[c];
-                }
-                named_bar_sync(1, 32 * kEpiWarps);
             }
+            // the accumulator is in shared memory now: release it to the MMA warp
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
+            named_bar_sync(1, 32 * kEpiWarps);
+            if (MODE == kTapSubpix) {
+                // task (c, py, ry, rx): out(2Y+py, 2X+{0,1}) = bias + sum_t y[src(t)][((py*2+px)*4+t)*C + c]
+                for (int i = et; i < kTilePx * 2 * C; i += 32 * kEpiWarps) {
+                    const int c = i / (2 * kTilePx);
+                    const int r = i - c * 2 * kTilePx;
+                    const int py = r / kTilePx, r2 = r - py * kTilePx;
+                    const int ry = r2 / kTapTX, rx = r2 - ry * kTapTX;
+                    const int Y = Y0 + ry, X = X0 + rx;
+                    if (Y >= p.win.oy1 || X >= p.win.ox1) continue;
+                    float o2[2];
+#pragma unroll
+                    for (int px = 0; px < 2; ++px) {
+                        float acc = sm_bias[c];
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            const int q = (ry + (t >> 1) + py) * kTapSX + rx + (t & 1) + px;
+                            acc += smY[q * YS + ((py * 2 + px) * 4 + t) * C + c];
+                        }
+                        o2[px] = acc;
+                    }
+                    *reinterpret_cast<float2*>(p.out + (static_cast<size_t>(n) * C + c) * plane +
+                                               static_cast<size_t>(2 * Y + py) * OW + 2 * X) = make_float2(o2[0], o2[1]);
+                }
+            } else {
+                // task (c, ry, rx): out(Y, X) = sum_in s*y + (o * sum_in wsum + bias)
+                for (int i = et; i < kTilePx * C; i += 32 * kEpiWarps) {
+                    const int c = i / kTilePx;
+                    const int r = i - c * kTilePx;
+                    const int ry = r / kTapTX, rx = r - ry * kTapTX;
+                    const int Y = Y0 + ry, X = X0 + rx;
+                    if (Y >= p.win.oy1 || X >= p.win.ox1) continue;
+                    float acc = 0.f, ws = 0.f;
+#pragma unroll
+                    for (int ky = 0; ky < 3; ++ky) {
+                        const int sy = Y + ky - 1;
+                        const bool rin = sy >= p.win.vy0 && sy < p.win.vy1;
+#pragma unroll
+                        for (int kx = 0; kx < 3; ++kx) {
+                            const int sx = X + kx - 1;
+                            const bool in = rin && sx >= p.win.vx0 && sx < p.win.vx1;
+                            const int t = ky * 3 + kx;
+                            const float v = smY[((ry + ky) * kTapSX + rx + kx) * YS + t * C + c];
+                            acc += in ? v : 0.f;
+                            ws += in ? sm_wsum[t * C + c] : 0.f;
+                        }
+                    }
+                    p.out[(static_cast<size_t>(n) * C + c) * plane + static_cast<size_t>(Y) * OW + X] =
+                        acc + fmaf(p.shift, ws, sm_bias[c]);
+                }
+            }
+            named_bar_sync(1, 32 * kEpiWarps);  // shared y is rewritten by the next tile
         }
     }
     tc_fence_before();
@@ -221,13 +276,11 @@ __global__ void __launch_bounds__(kThreads, 1) subpix_tc_kernel(const __grid_con
     }
 }
 
-}  // namespace
-
-cudaError_t launch_subpix_tc(const SubpixTcParams& p, cudaStream_t st) {
-    if (p.C < 1 || p.C > 4 || p.kb < 1 || p.kb > kMaxKb) return cudaErrorInvalidValue;
+template <int MODE>
+cudaError_t launch_mode(const TapTcParams& p, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        const cudaError_t e = cudaFuncSetAttribute(subpix_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        const cudaError_t e = cudaFuncSetAttribute(tap_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
         if (e != cudaSuccess) return e;
         attr = true;
     }
@@ -238,7 +291,26 @@ cudaError_t launch_subpix_tc(const SubpixTcParams& p, cudaStream_t st) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const int grid = p.num_tiles < sms ? p.num_tiles : sms;
-    return launch_pdl(subpix_tc_kernel, dim3(grid), dim3(kThreads), kSmem, st, p);
+    return launch_pdl(tap_tc_kernel<MODE>, dim3(grid), dim3(kThreads), static_cast<size_t>(smem_bytes<MODE>(p)), st, p);
+}
+
+}  // namespace
+
+bool tap_tc_supported(int mode, int C, int kb, int N) {
+    TapTcParams p{};
+    p.C = C;
+    p.kb = kb;
+    p.N = N;
+    const int mt = mode == kTapSubpix ? Geo<kTapSubpix>::MT : Geo<kTapConv3>::MT;
+    const int smem = mode == kTapSubpix ? smem_bytes<kTapSubpix>(p) : smem_bytes<kTapConv3>(p);
+    return C >= 1 && C <= 4 && kb >= 1 && kb <= kTapMaxKb && N % 16 == 0 && N >= pass_cols(mode, C) &&
+           pass_cols(mode, C) <= kMaxPC && mt * N <= kAccCols && smem <= kSmemMax;
+}
+
+cudaError_t launch_tap_tc(int mode, const TapTcParams& p, cudaStream_t st) {
+    if (!tap_tc_supported(mode, p.C, p.kb, p.N)) return cudaErrorInvalidValue;
+    if (p.num_tiles <= 0) return cudaSuccess;
+    return mode == kTapSubpix ? launch_mode<kTapSubpix>(p, st) : launch_mode<kTapConv3>(p, st);
 }
 
 }  // namespace lc

@@ -1,32 +1,52 @@
-// K8: the decoder's last stage -- nearest 2x upsample + 3x3 conv (c_in ->
-// C <= 4 image channels) + bias, written straight into the fp32 planar video
-// (codec.cpp:96-124 decode_batch's last block; tensor.cpp:160-196 conv2d,
-// :232-248 upsample2).  One persistent tcgen05 kernel: a TMA-staged window of
-// low-res pixels (with a one-pixel halo) times the 16*C-column tap bank
-// (engine.cu subpix_tap_bank: every (output parity, 2x2 source tap) pair's
-// merged 3x3 weights) into TMEM, then per output parity the four taps of
-// each output pixel are summed from shared memory.  Replaces the tap-to-N
-// conv + subpix_gather_kernel pair: no fp32 intermediate in HBM.
+// K8: fused tap-to-N convolutions with a tiny output channel count, the
+// U-Net head (3x3 conv c_in -> C <= 4, conditioning affine, bias;
+// unet.cpp:76-97 run_conv_block for "head") and the decoder's last stage
+// (nearest 2x upsample + 3x3 conv + bias; codec.cpp:96-124, tensor.cpp:
+// 160-196, :232-248).  One persistent tcgen05 kernel: a TMA-staged window of
+// pixels with a one-pixel halo times the tap bank (N = taps x C columns:
+// for the head the 9 taps of the 3x3 kernel, engine.cu tap_bank; for the
+// decoder every (output parity, 2x2 source tap) pair's merged weights,
+// engine.cu subpix_tap_bank) into TMEM; then each output pixel sums its taps
+// from shared memory and is stored straight into the fp32 planar output.
+// Replaces the tap-to-N conv + tap/subpix gather kernel pairs: no fp32
+// intermediate in HBM.
 #pragma once
 
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include "kernels.cuh"
+
 namespace lc {
 
-struct SubpixTcParams {
-    CUtensorMap tmA;      // low-res activation (cs, W, H, n) fp16, box (64, kSX, kSY, 1), SW128
-    const __half* w;      // [N = 16*C][kb*64] fp16, row (p*4+t)*C + c
+enum TapMode : int {
+    kTapSubpix = 0,  // decoder: 4 output parities x 2x2 taps, output (n, C, 2H, 2W)
+    kTapConv3 = 1,   // head: 3x3 taps, output (n, C, H, W), scale/offset affine
+};
+
+struct TapTcParams {
+    CUtensorMap tmA;      // input (cs, W, H, n) fp16, box (64, kTapSX, kTapSY, 1), SW128
+    const __half* w;      // [N][kb*64] fp16, row t*C + c (head) or (p*4+t)*C + c (decoder)
     const float* bias;    // [C]
-    float* out;           // planar (n, C, 2H, 2W) fp32
-    int n, H, W, C, kb;   // low-res extents, image channels, 64-channel K blocks
+    const float* wsum;    // head: [9][C] per-tap weight sums (offset correction)
+    float scale, shift;   // head: conditioning affine s*x + o
+    float* out;           // planar fp32
+    int n, H, W, C, N, kb;
+    Window win;           // head: v* zero-padding window, o* output window (engine.hpp)
     int tiles_x, tiles_y, num_tiles;
 };
 
-constexpr int kSubpixTX = 64, kSubpixTY = 5;                        // core tile (low-res pixels)
-constexpr int kSubpixSX = kSubpixTX + 2, kSubpixSY = kSubpixTY + 2;  // staged window with halo
+// Core tile kTapTX x tap_tile_ty(mode) pixels; the staged window adds a
+// one-pixel halo on every side (TMA box kTapSX x tap_stage_sy(mode)).
+constexpr int kTapTX = 64, kTapSX = kTapTX + 2;
+__host__ __device__ constexpr int tap_tile_ty(int mode) { return mode == kTapSubpix ? 5 : 5; }
+__host__ __device__ constexpr int tap_stage_sy(int mode) { return tap_tile_ty(mode) + 2; }
+constexpr int kTapMaxKb = 5;  // c_in <= 320
 
-cudaError_t launch_subpix_tc(const SubpixTcParams& p, cudaStream_t st);
+cudaError_t launch_tap_tc(int mode, const TapTcParams& p, cudaStream_t st);
+// Whether launch_tap_tc accepts this geometry (output channels, K blocks,
+// tap columns; shared-memory fit).
+bool tap_tc_supported(int mode, int C, int kb, int N);
 
 }  // namespace lc

@@ -14,6 +14,9 @@ CFGS = {
     "tiny": {"run.frames": 2, "run.height": 32, "run.width": 32, "sampler.steps": 6},
     "odd": {"run.frames": 3, "run.height": 96, "run.width": 160, "sampler.steps": 3, "codec.width": 64},
     "w192": {"run.frames": 2, "run.height": 64, "run.width": 64, "sampler.steps": 2, "codec.width": 192},
+    "k5": {"run.frames": 2, "run.height": 32, "run.width": 32, "sampler.steps": 3, "unet.kernel": 5},
+    "headchunk": {"run.frames": 2, "run.height": 64, "run.width": 96, "sampler.steps": 3, "chunk.halo": "none",
+                  "chunk.targets": "stem,u0,head", "chunk.eta": 2, "chunk.omega": 3},
     "B1": {"run.frames": 1, "run.height": 512, "run.width": 512, "codec.stages": 3, "codec.width": 128,
            "unet.base_channels": 320, "unet.depth": 3, "sampler.steps": 4, "cache.n": 2},
 }
