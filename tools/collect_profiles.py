@@ -45,9 +45,16 @@ if os.path.exists(rep):
             "smsp__average_warps_issue_stalled_", "l1tex__m_xbar2l1tex_read_bytes.sum")
     sel = [f"{h} = {v}" for h, v in zip(rows[0], rows[2]) if h.startswith(keep) and not h.endswith("pct_of_peak_sustained_elapsed")]
     open(os.path.join(P, f"ncu_full_conv_b_{rnd}.txt"), "w").write(
-        "# ncu --set full --clock-control none --import-source on -k regex:conv_tc --launch-skip 115 "
+        "# ncu --set full --clock-control none --import-source on -k regex:conv_tc --launch-skip 92 "
         "--launch-count 1 python tools/profile_step.py B 3\n# (u0 of a full step: cg=2, BN=160, K=5440)\n\n" +
         det + "\n# selected raw metrics\n" + "\n".join(sel) + "\n")
+rep = os.path.join(G, "full_tap.ncu-rep")
+if os.path.exists(rep):
+    det = subprocess.run(["ncu", "-i", rep, "--page", "details"], capture_output=True, text=True).stdout
+    open(os.path.join(P, f"ncu_full_tap_b_{rnd}.txt"), "w").write(
+        "# ncu --set full --clock-control none --import-source on -k regex:tap_tc --launch-skip 4 "
+        "--launch-count 1 python tools/profile_step.py B 1\n# (K8, the decoder's fused last stage of the "
+        "first 4-frame slice)\n\n" + det)
 for name in ("layers_b", "layers_c", "swap_timeline_b"):
     src = os.path.join(G, f"{name}.txt")
     if os.path.exists(src):
