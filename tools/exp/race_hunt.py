@@ -26,7 +26,7 @@ kv = lco.parse_text(lc.DEFAULT_CONFIG)
 kv.update({k: str(v) for k, v in CFG.items()})
 want, _ = lco.Restatement().run_pipeline(kv)
 for fused in ("1", "0"):
-    for rep in range(4):
+    for rep in range(int(os.environ.get("RH_PROCS", "4"))):
         env = dict(os.environ, LC_SUBPIX_FUSED=fused)
         r = subprocess.run([sys.executable, __file__, "/tmp/rh", "4"], env=env, capture_output=True, text=True)
         if r.returncode:
