@@ -423,15 +423,22 @@ Bank tap_bank(const Bank& b) {
     return t;
 }
 
-// K8 operand: a tap bank's rows as fp16 [round_up(rows, 16)][kb * 64], zero padded.
-DevBuf pack_tap_w16(Ledger* l, const Bank& tb, int* kb_out, int* n_out) {
+// K8 operand: a tap bank's rows as fp16 [round_up(rows, 16)][kb * 64], zero
+// padded, times the power-of-two scale pack_tc_layer gives the same bank
+// (fan_in = c_in for a 1x1 tap bank), so K8 rounds the weights and the
+// accumulator exactly as the tap-to-N GEMM it replaces; the epilogue
+// multiplies by scale / wscale.
+DevBuf pack_tap_w16(Ledger* l, const Bank& tb, int* kb_out, int* n_out, float* wscale_out) {
     const int kb = static_cast<int>((tb.c_in + 63) / 64);
     const int n = static_cast<int>((tb.c_out + 15) / 16 * 16);
     const int kp = 64 * kb;
+    const float wscale = std::ldexp(1.0f, static_cast<int>(std::lround(0.5 * std::log2(static_cast<double>(tb.c_in)))));
     std::vector<__half> w16(static_cast<size_t>(n) * kp, __float2half_rn(0.0f));
     for (int64_t r = 0; r < tb.c_out; ++r)
         for (int64_t ic = 0; ic < tb.c_in; ++ic)
-            w16[static_cast<size_t>(r * kp + ic)] = __float2half_rn(tb.taps[static_cast<size_t>(r * tb.c_in + ic)]);
+            w16[static_cast<size_t>(r * kp + ic)] =
+                __float2half_rn(tb.taps[static_cast<size_t>(r * tb.c_in + ic)] * wscale);
+    *wscale_out = wscale;
     DevBuf b = dev_alloc(l, static_cast<int64_t>(w16.size() * 2), false);
     LC_CUDA(cudaMemcpy(b.p, w16.data(), w16.size() * 2, cudaMemcpyHostToDevice));
     *kb_out = kb;
@@ -831,7 +838,7 @@ void Engine::configure(const RunConfig& cfg) {
                 if (hb.k == 3 && tap_tc_supported(kTapConv3, static_cast<int>(hb.c_out),
                                                   static_cast<int>((tb.c_in + 63) / 64),
                                                   static_cast<int>((tb.c_out + 15) / 16 * 16)))
-                    head_w16_ = pack_tap_w16(&ledger_, tb, &head_kb_, &head_n_);
+                    head_w16_ = pack_tap_w16(&ledger_, tb, &head_kb_, &head_n_, &head_wscale_);
                 const int64_t kk = hb.k * hb.k;
                 std::vector<float> ws(static_cast<size_t>(kk * hb.c_out));
                 for (int64_t tp = 0; tp < kk; ++tp)
@@ -855,7 +862,7 @@ void Engine::configure(const RunConfig& cfg) {
                 if (tap_tc_supported(kTapSubpix, static_cast<int>(db.c_out), static_cast<int>((tb.c_in + 63) / 64),
                                      static_cast<int>((tb.c_out + 15) / 16 * 16))) {
                     int nn = 0;
-                    dec_last_w16_ = pack_tap_w16(&ledger_, tb, &dec_last_kb_, &nn);
+                    dec_last_w16_ = pack_tap_w16(&ledger_, tb, &dec_last_kb_, &nn, &dec_last_wscale_);
                 }
                 dec_last_bias_ = dev_alloc(&ledger_, static_cast<int64_t>(db.bias.size() * 4), false);
                 LC_CUDA(cudaMemcpy(dec_last_bias_.p, db.bias.data(), db.bias.size() * 4, cudaMemcpyHostToDevice));
@@ -1228,7 +1235,7 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
             q.w = head_w16_.as<__half>();
             q.bias = head_bias_.as<float>();
             q.wsum = head_wsum_.as<float>();
-            q.scale = s;
+            q.scale = s / head_wscale_;
             q.shift = o;
             q.out = eps2_dev;
             q.n = a.n;
@@ -1502,6 +1509,7 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
             const uint32_t estr[4] = {1, 1, 1, 1};
             encode_map(&q.tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, a.p, dims, strides, box, estr);
             q.w = dec_last_w16_.as<__half>();
+            q.scale = 1.0f / dec_last_wscale_;
             q.bias = dec_last_bias_.as<float>();
             q.out = video_dev + g0 * IC * H * W;
             q.n = gs;

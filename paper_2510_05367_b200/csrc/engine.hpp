@@ -273,6 +273,7 @@ private:
     DevBuf head_wsum_, head_bias_, dec_last_bias_, head_y_buf_, dec_y_buf_;
     DevBuf dec_last_w16_, head_w16_;  // K8 tap banks, fp16 [N][kb*64]
     int dec_last_kb_ = 0, head_kb_ = 0, head_n_ = 0;
+    float dec_last_wscale_ = 1.0f, head_wscale_ = 1.0f;
     DevBuf shard_lat_, shard_vid_;  // decode_sharded buffers
     // encoder (image mode, codec.cpp:64-81): patch GEMM + [down2 + conv]xS
     std::unique_ptr<TcLayer> enc0_tc_;

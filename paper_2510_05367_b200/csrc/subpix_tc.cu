@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_consta
         const int g = e >> 2;                   // M-tiles g, g+2
         const int et = static_cast<int>(threadIdx.x) - 64;
         const uint32_t ybase = smem_u32(smY);
-        const float yscale = MODE == kTapConv3 ? p.scale : 1.0f;
+        const float yscale = p.scale;
         const int nld = (PC + 3) / 4;
         const int OH = MODE == kTapSubpix ? 2 * p.H : p.H, OW = MODE == kTapSubpix ? 2 * p.W : p.W;
         const size_t plane = static_cast<size_t>(OH) * OW;

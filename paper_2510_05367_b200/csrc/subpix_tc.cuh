@@ -30,7 +30,8 @@ struct TapTcParams {
     const __half* w;      // [N][kb*64] fp16, row t*C + c (head) or (p*4+t)*C + c (decoder)
     const float* bias;    // [C]
     const float* wsum;    // head: [9][C] per-tap weight sums (offset correction)
-    float scale, shift;   // head: conditioning affine s*x + o
+    float scale;          // y = scale * acc (head: s / wscale; decoder: 1 / wscale)
+    float shift;          // head: conditioning offset o
     float* out;           // planar fp32
     int n, H, W, C, N, kb;
     Window win;           // head: v* zero-padding window, o* output window (engine.hpp)

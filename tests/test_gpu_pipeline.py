@@ -405,3 +405,39 @@ def test_random_configs_match_oracle(ctx, oracle, over):
     want_v, want_l = oracle.run_pipeline(_kv(over))
     assert lc.rel_l2(lat, want_l) < TOL
     assert lc.rel_l2(video, want_v) < TOL
+
+
+_K8_CHILD = r"""
+import sys, numpy as np
+import paper_2510_05367_b200 as lc
+over = eval(sys.argv[1])
+ctx = lc.Context(0)
+ctx.configure(lc.config_text(over, base=lc.DEFAULT_CONFIG))
+v, lat, _ = ctx.run_pipeline(want_latent=True)
+np.savez(sys.argv[2], v=v, lat=lat)
+"""
+
+
+@pytest.mark.parametrize("over", [
+    TINY,
+    dict(TINY, **{"run.height": 64, "run.width": 96, "sampler.steps": 3, "chunk.halo": "none",
+                  "chunk.targets": "stem,u0,head", "chunk.eta": 2, "chunk.omega": 3}),
+    dict(TINY, **{"run.height": 64, "run.width": 64, "sampler.steps": 2, "codec.width": 192}),
+])
+def test_fused_tap_kernel_matches_gemm_plus_gather(tmp_path, over):
+    """K8 (csrc/subpix_tc.cu) sums the same tap products in the same order
+    as the tap-to-N GEMM + gather pair it replaces (LC_SUBPIX_FUSED=0):
+    bit-identical latents and videos, head chunk windows included."""
+    import os
+    import subprocess
+    import sys
+    outs = []
+    for fused in ("1", "0"):
+        path = str(tmp_path / f"k8_{fused}.npz")
+        env = dict(os.environ, LC_SUBPIX_FUSED=fused)
+        r = subprocess.run([sys.executable, "-c", _K8_CHILD, repr(over), path], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0]["lat"], outs[1]["lat"])
+    assert np.array_equal(outs[0]["v"], outs[1]["v"])
