@@ -85,10 +85,17 @@ __host__ __device__ inline int epi_smem_bytes(int tabf, int tma_out, int wide, i
 
 // ring stages: A + B per stage, or A only with a resident weight panel of
 // total_kb K blocks (b_res)
+// A-operand bytes of one ring stage: one 128-pixel box, or (halo staging)
+// one hh x hw box rounded up to the 1024 B swizzle atom
+__host__ __device__ inline int a_stage_bytes(const ConvParams& p) {
+    return p.halo ? (p.hw * p.hh * kBK * 2 + 1023) & ~1023 : static_cast<int>(kABytes);
+}
+
 template <int CG>
-__host__ __device__ inline int num_stages(int bn, int tabf, int tma_out, int b_res, int total_kb, int wide) {
+__host__ __device__ inline int num_stages(int bn, int tabf, int tma_out, int b_res, int total_kb, int wide,
+                                          int a_stage) {
     const int bblk = (bn / CG) * kBK * 2;
-    const int per = static_cast<int>(kABytes) + (b_res ? 0 : bblk);
+    const int per = a_stage + (b_res ? 0 : bblk);
     int s = (kSmemMax - kSmemFixed - epi_smem_bytes(tabf, tma_out, wide, b_res) - (b_res ? total_kb * bblk : 0)) / per;
     return s > 8 ? 8 : (s < 2 ? 2 : s);
 }
@@ -168,7 +175,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < p.nseg; ++s) total_kb += p.seg[s].ntaps * p.seg[s].ncb;
     const bool b_res = CG == 1 && p.b_res;
     const int tabf = tab_floats(p.rc, p.BN);
-    const int stages = num_stages<CG>(p.BN, tabf, p.tma_out, b_res, total_kb, p.nhwc32);
+    const bool halo = CG == 1 && p.halo;
+    const int a_stage = a_stage_bytes(p);
+    const int stages = num_stages<CG>(p.BN, tabf, p.tma_out, b_res, total_kb, p.nhwc32, a_stage);
     // fp32 raw (tap-to-N) epilogues need no offset registers: two chunks per wait
     constexpr int kCh = EPI == kEpiF32Raw ? 2 : kChunks;
     const int schunk = stage_chunk(p.nhwc32);
@@ -177,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int bn_cta = p.BN / CG;  // B rows staged by this CTA
     const uint32_t b_bytes = static_cast<uint32_t>(bn_cta) * kBK * 2;
     uint8_t* smA = smem;
-    uint8_t* smB = smem + stages * kABytes;
+    uint8_t* smB = smem + stages * a_stage;
     const int b_blocks = b_res ? total_kb : stages;  // resident panel or ring
     uint64_t* full_bar = reinterpret_cast<uint64_t*>(smB + b_blocks * b_bytes);
     uint64_t* empty_bar = full_bar + stages;
@@ -271,10 +280,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
         if (elect_one()) {
-            const uint32_t a_bytes = static_cast<uint32_t>(p.TI * p.TH * p.TW) * kBK * 2;
+            const uint32_t a_bytes = halo ? static_cast<uint32_t>(p.hw * p.hh) * kBK * 2
+                                          : static_cast<uint32_t>(p.TI * p.TH * p.TW) * kBK * 2;
             const uint32_t tx_bytes = b_res ? a_bytes : CG * (a_bytes + b_bytes);  // both CTAs complete on the leader
             if (b_res && unit0 < total_units) {
-                // the slab's whole weight panel, once
+                // the slab's whole weight panel, once (slot = K block of the weight row)
                 mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(total_kb) * b_bytes);
                 int s = 0, tap = 0, cb = 0, kcoord = p.seg[0].kbase;
                 for (int kb = 0; kb < total_kb; ++kb) {
@@ -292,40 +302,52 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             int stage = 0;
             uint32_t phase = 0;
+            auto advance = [&]() {
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            };
             for (int u = unit0; u < total_units; u += unit_step) {
                 const TileCoord tc = coord(u);
-                int s = 0, tap = 0, cb = 0;
-                int kcoord = p.seg[0].kbase;
+                if (halo) {
+                    // one box per channel block serves every tap (see ConvParams::halo)
+                    const ConvSegDev& sg = p.seg[0];
+                    const int cx = tc.X0 + p.hox[tc.parity] - sg.wx0;
+                    const int cy = tc.Y0 + p.hoy[tc.parity] - sg.wy0;
+                    for (int cb = 0; cb < sg.ncb; ++cb) {
+                        mbar_wait(&empty_bar[stage], phase ^ 1);
+                        mbar_arrive_expect_tx(&full_bar[stage], a_bytes);
+                        tma_load_4d(smA + stage * a_stage, &p.tmA[0], &full_bar[stage], cb * kBK, cx, cy, tc.I0);
+                        advance();
+                    }
+                    continue;
+                }
                 const int nrow = tc.n_tile * p.BN + static_cast<int>(rank) * bn_cta;
-                for (int kb = 0; kb < total_kb; ++kb) {
-                    mbar_wait(&empty_bar[stage], phase ^ 1);
+                // K blocks in (segment, channel block, tap) order
+                for (int s = 0; s < p.nseg; ++s) {
                     const ConvSegDev& sg = p.seg[s];
-                    const int cx = tc.X0 * sg.mx + sg.ox[tc.parity][tap] - sg.wx0;
-                    const int cy = tc.Y0 * sg.my + sg.oy[tc.parity][tap] - sg.wy0;
-                    if (CG == 1) {
-                        mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
-                        tma_load_4d(smA + stage * kABytes, &p.tmA[s], &full_bar[stage], cb * kBK, cx, cy, tc.I0);
-                        if (!b_res)
-                            tma_load_3d(smB + stage * b_bytes, &p.tmB, &full_bar[stage], kcoord, nrow, tc.parity);
-                    } else {
-                        if (leader) mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
-                        const uint32_t bar = mapa_shared(smem_u32(&full_bar[stage]), 0);
-                        tma_load_4d_cg2(smA + stage * kABytes, &p.tmA[s], bar, cb * kBK, cx, cy, tc.I0);
-                        tma_load_3d_cg2(smB + stage * b_bytes, &p.tmB, bar, kcoord, nrow, tc.parity);
-                    }
-                    kcoord += kBK;
-                    if (++cb == sg.ncb) {
-                        cb = 0;
-                        if (++tap == sg.ntaps) {
-                            tap = 0;
-                            ++s;
-                            if (s < p.nseg) kcoord = p.seg[s].kbase;
+                    for (int cb = 0; cb < sg.ncb; ++cb)
+                        for (int tap = 0; tap < sg.ntaps; ++tap) {
+                            mbar_wait(&empty_bar[stage], phase ^ 1);
+                            const int cx = tc.X0 * sg.mx + sg.ox[tc.parity][tap] - sg.wx0;
+                            const int cy = tc.Y0 * sg.my + sg.oy[tc.parity][tap] - sg.wy0;
+                            const int kcoord = sg.kbase + (tap * sg.ncb + cb) * kBK;
+                            if (CG == 1) {
+                                mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
+                                tma_load_4d(smA + stage * a_stage, &p.tmA[s], &full_bar[stage], cb * kBK, cx, cy,
+                                            tc.I0);
+                                if (!b_res)
+                                    tma_load_3d(smB + stage * b_bytes, &p.tmB, &full_bar[stage], kcoord, nrow,
+                                                tc.parity);
+                            } else {
+                                if (leader) mbar_arrive_expect_tx(&full_bar[stage], tx_bytes);
+                                const uint32_t bar = mapa_shared(smem_u32(&full_bar[stage]), 0);
+                                tma_load_4d_cg2(smA + stage * a_stage, &p.tmA[s], bar, cb * kBK, cx, cy, tc.I0);
+                                tma_load_3d_cg2(smB + stage * b_bytes, &p.tmB, bar, kcoord, nrow, tc.parity);
+                            }
+                            advance();
                         }
-                    }
-                    if (++stage == stages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
                 }
             }
         }
@@ -337,37 +359,74 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
+            auto advance = [&]() {
+                if (++stage == stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            };
+            // 128 x BN x 64 from one A stage address and one B panel/ring address
+            auto mma_kblock = [&](uint32_t d_tmem, uint32_t a_addr, uint32_t b_addr, bool first) {
+                const uint64_t adesc = umma_desc_sw128(a_addr);
+                const uint64_t bdesc = umma_desc_sw128(b_addr);
+#pragma unroll
+                for (int k = 0; k < kBK / 16; ++k) {
+                    // +32 bytes per K=16 step inside the 128 B swizzle row
+                    const uint32_t accum = (!first || k != 0) ? 1u : 0u;
+                    if (CG == 1)
+                        umma_f16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, accum);
+                    else
+                        umma_f16_cg2(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, accum);
+                }
+            };
+            auto commit = [&](uint64_t* bar) {
+                if (CG == 1) umma_commit(bar);
+                else umma_commit_cg2(bar);
+            };
             if (b_res && unit0 < total_units) mbar_wait(bfull, 0);
             for (int u = unit0; u < total_units; u += unit_step) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * acc_stride;
-                for (int kb = 0; kb < total_kb; ++kb) {
-                    mbar_wait(&full_bar[stage], phase);
-                    tc_fence_after();
-                    if (elect_one()) {
-                        const uint64_t adesc = umma_desc_sw128(smem_u32(smA + stage * kABytes));
-                        const uint64_t bdesc = umma_desc_sw128(smem_u32(smB + (b_res ? kb : stage) * b_bytes));
-#pragma unroll
-                        for (int k = 0; k < kBK / 16; ++k) {
-                            // +32 bytes per K=16 step inside the 128 B swizzle row
-                            if (CG == 1)
-                                umma_f16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
-                            else
-                                umma_f16_cg2(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+                if (halo) {
+                    // b_res: every unit of this CTA is its slab's parity
+                    const ConvSegDev& sg = p.seg[0];
+                    const int par = slab_par;
+                    for (int cb = 0; cb < sg.ncb; ++cb) {
+                        mbar_wait(&full_bar[stage], phase);
+                        tc_fence_after();
+                        if (elect_one()) {
+                            const uint32_t a0 = smem_u32(smA + stage * a_stage);
+                            for (int tap = 0; tap < sg.ntaps; ++tap) {
+                                const int row = (sg.oy[par][tap] - p.hoy[par]) * p.hw + (sg.ox[par][tap] - p.hox[par]);
+                                mma_kblock(d_tmem, a0 + static_cast<uint32_t>(row) * 128u,
+                                           smem_u32(smB + (tap * sg.ncb + cb) * b_bytes), (cb | tap) == 0);
+                            }
+                            commit(&empty_bar[stage]);
+                            if (cb == sg.ncb - 1) commit(&tfull[acc]);
                         }
-                        if (CG == 1) {
-                            umma_commit(&empty_bar[stage]);
-                            if (kb == total_kb - 1) umma_commit(&tfull[acc]);
-                        } else {
-                            umma_commit_cg2(&empty_bar[stage]);
-                            if (kb == total_kb - 1) umma_commit_cg2(&tfull[acc]);
-                        }
+                        __syncwarp();
+                        advance();
                     }
-                    __syncwarp();
-                    if (++stage == stages) {
-                        stage = 0;
-                        phase ^= 1;
+                } else {
+                    int kb = 0, seg_kb0 = 0;
+                    for (int s = 0; s < p.nseg; ++s) {
+                        const ConvSegDev& sg = p.seg[s];
+                        for (int cb = 0; cb < sg.ncb; ++cb)
+                            for (int tap = 0; tap < sg.ntaps; ++tap, ++kb) {
+                                mbar_wait(&full_bar[stage], phase);
+                                tc_fence_after();
+                                if (elect_one()) {
+                                    const int bslot = b_res ? seg_kb0 + tap * sg.ncb + cb : stage;
+                                    mma_kblock(d_tmem, smem_u32(smA + stage * a_stage), smem_u32(smB + bslot * b_bytes),
+                                               kb == 0);
+                                    commit(&empty_bar[stage]);
+                                    if (kb == total_kb - 1) commit(&tfull[acc]);
+                                }
+                                __syncwarp();
+                                advance();
+                            }
+                        seg_kb0 += sg.ntaps * sg.ncb;
                     }
                 }
                 if (++acc == 2) {
@@ -680,9 +739,10 @@ size_t smem_bytes_for(const ConvParams& p) {
     int total_kb = 0;
     for (int s = 0; s < p.nseg; ++s) total_kb += p.seg[s].ntaps * p.seg[s].ncb;
     const int b_res = CG == 1 && p.b_res;
-    const int st = num_stages<CG>(p.BN, tabf, p.tma_out, b_res, total_kb, p.nhwc32);
+    const int a_stage = a_stage_bytes(p);
+    const int st = num_stages<CG>(p.BN, tabf, p.tma_out, b_res, total_kb, p.nhwc32, a_stage);
     const size_t bblk = static_cast<size_t>(p.BN / CG) * kBK * 2;
-    return kSmemFixed + static_cast<size_t>(st) * (kABytes + (b_res ? 0 : bblk)) + (b_res ? total_kb * bblk : 0) +
+    return kSmemFixed + static_cast<size_t>(st) * (a_stage + (b_res ? 0 : bblk)) + (b_res ? total_kb * bblk : 0) +
            epi_smem_bytes(tabf, p.tma_out, p.nhwc32, b_res);
 }
 
@@ -781,13 +841,26 @@ static bool want_b_res(const ConvParams& p, int parities) {
     if (m_tiles < 2 * cps) return false;
     int total_kb = 0;
     for (int s = 0; s < p.nseg; ++s) total_kb += p.seg[s].ntaps * p.seg[s].ncb;
-    return num_stages<1>(p.BN, tab_floats(p.rc, p.BN), p.tma_out, 1, total_kb, p.nhwc32) >= 3 &&
+    // >= 3 activation stages; >= 2 halo stages (each carries every tap of a channel block)
+    const int a_stage = a_stage_bytes(p), min_stages = p.halo ? 2 : 3;
+    return num_stages<1>(p.BN, tab_floats(p.rc, p.BN), p.tma_out, 1, total_kb, p.nhwc32, a_stage) >= min_stages &&
            (kSmemMax - kSmemFixed - epi_smem_bytes(tab_floats(p.rc, p.BN), p.tma_out, p.nhwc32, 1) -
-            total_kb * p.BN * kBK * 2) >= 3 * static_cast<int>(kABytes);
+            total_kb * p.BN * kBK * 2) >= min_stages * a_stage;
+}
+
+bool conv_tc_halo_fits(const ConvParams& p, int parities) {
+    return p.halo && p.cg == 1 && p.nseg == 1 && want_b_res(p, parities);
 }
 
 cudaError_t launch_conv_tc(const ConvParams& p, int parities, cudaStream_t stream) {
-    if (p.cg == 2) return launch_cg<2>(p, parities, stream);
+    if (p.cg == 2) return p.halo ? cudaErrorInvalidValue : launch_cg<2>(p, parities, stream);
+    if (p.halo) {
+        // halo staging runs only on the weight-stationary schedule
+        if (!conv_tc_halo_fits(p, parities)) return cudaErrorInvalidValue;
+        ConvParams q = p;
+        q.b_res = 1;
+        return launch_cg<1>(q, parities, stream);
+    }
     if (want_b_res(p, parities)) {
         ConvParams q = p;
         q.b_res = 1;

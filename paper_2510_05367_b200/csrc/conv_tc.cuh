@@ -13,7 +13,10 @@
 //   * bias, conditioning shift and SiLU run in the TMEM->register epilogue.
 //
 // GEMM view: M = output pixels (a TI x TH x TW spatial tile of <=128 pixels),
-// N = output channels (BN <= 256 per CTA), K = segment x tap x channel.
+// N = output channels (BN <= 256 per CTA), K = segment x tap x channel in
+// the weight rows; the MMAs accumulate in (segment, 64-channel block, tap)
+// order, the order the halo staging (below) consumes its boxes in, so every
+// staging variant of a layer produces bit-identical sums.
 // Activations are fp16 NHWC ("channels-last"), channel stride a multiple of
 // 64 so one K block is one 128-byte SW128 row per pixel.
 #pragma once
@@ -104,6 +107,15 @@ struct alignas(64) ConvParams {
     // tiles (small-K, small-N layers whose per-tile weight re-reads would
     // otherwise make them L2-bandwidth bound)
     int b_res;
+    // halo operand staging (b_res, one segment, one-row tiles of 128 pixels
+    // at source scale 1): per 64-channel block ONE box of hh rows x hw
+    // pixels covering every tap's shifted tile is loaded (origin hox/hoy per
+    // parity), and each tap's MMA reads its 128 rows at a row offset of that
+    // box (a start-address shift of the SW128 descriptor, 128 B per pixel)
+    // instead of a box of its own: hh*hw instead of ntaps*128 pixel rows
+    int halo;
+    int hw, hh;
+    int hox[4], hoy[4];
     FastDiv fd_units, fd_ntiles, fd_par, fd_tx, fd_ty;  // launch-side divisors of tile_coord
 };
 
@@ -120,5 +132,8 @@ struct ConvTcConfig {
 // Host launcher (conv_tc.cu).
 cudaError_t launch_conv_tc(const ConvParams& p, int parities, cudaStream_t stream);
 size_t conv_tc_smem_bytes(const ConvParams& p);
+// Whether a layer with p.halo set (and hw/hh filled in) can run halo-staged:
+// one segment, single CTAs, weight-stationary with >= 2 halo stages.
+bool conv_tc_halo_fits(const ConvParams& p, int parities);
 
 }  // namespace lc

@@ -504,6 +504,42 @@ Bank subpixel_shuffle_bank(const Bank& b) {
     return s;
 }
 
+// Halo operand staging (ConvParams::halo) for layers that qualify: one
+// segment at source scale 1, several taps, one-row tiles of 128 pixels, the
+// weight-stationary schedule with >= 2 halo stages.  The activation map is
+// re-encoded with the halo box {64, hw, hh, 1}; LC_HALO=0 disables it.
+void plan_halo(const TcLayer& L, ConvParams* p, const __half* base, const uint64_t* dims, const uint64_t* strides) {
+    static const int env = std::getenv("LC_HALO") ? std::atoi(std::getenv("LC_HALO")) : 1;
+    p->halo = 0;
+    if (!env || L.nseg != 1 || L.seg_m[0] != 1 || L.seg_ntaps[0] < 2 || p->cg != 1) return;
+    if (p->TW != 128 || p->TH != 1 || p->TI != 1) return;
+    int dxr = 0, dyr = 0;
+    for (int q = 0; q < L.P; ++q) {
+        int x0 = 127, x1 = -128, y0 = 127, y1 = -128;
+        for (int t = 0; t < L.seg_ntaps[0]; ++t) {
+            x0 = std::min(x0, static_cast<int>(L.ox[0][q][t]));
+            x1 = std::max(x1, static_cast<int>(L.ox[0][q][t]));
+            y0 = std::min(y0, static_cast<int>(L.oy[0][q][t]));
+            y1 = std::max(y1, static_cast<int>(L.oy[0][q][t]));
+        }
+        p->hox[q] = x0;
+        p->hoy[q] = y0;
+        dxr = std::max(dxr, x1 - x0);
+        dyr = std::max(dyr, y1 - y0);
+    }
+    p->hw = p->TW + dxr;
+    p->hh = 1 + dyr;
+    if (p->hw > 256 || p->hh > 8) return;
+    p->halo = 1;
+    if (!conv_tc_halo_fits(*p, L.P)) {
+        p->halo = 0;
+        return;
+    }
+    const uint32_t box[4] = {64, static_cast<uint32_t>(p->hw), static_cast<uint32_t>(p->hh), 1};
+    const uint32_t estr[4] = {1, 1, 1, 1};
+    encode_map(&p->tmA[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, base, dims, strides, box, estr);
+}
+
 void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window& win, float s,
                  float o, bool silu, cudaStream_t st, float* out32, int shuffle_c, bool nhwc32, bool planar) {
     ConvParams p{};
@@ -529,6 +565,8 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
     p.tiles_y = (Lh + p.TH - 1) / p.TH;
     p.tiles_i = (out.n + p.TI - 1) / p.TI;
     p.nseg = L.nseg;
+    const __half* seg0_base = nullptr;
+    uint64_t seg0_dims[4] = {}, seg0_strides[3] = {};
     for (int sgi = 0; sgi < L.nseg; ++sgi) {
         const Act& a = srcs[sgi];
         const int m = L.seg_m[sgi];
@@ -548,6 +586,11 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
                                  static_cast<uint32_t>(p.TI)};
         const uint32_t estr[4] = {1, static_cast<uint32_t>(m), static_cast<uint32_t>(m), 1};
         encode_map(&p.tmA[sgi], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, base, dims, strides, box, estr);
+        if (sgi == 0) {
+            seg0_base = base;
+            std::memcpy(seg0_dims, dims, sizeof(dims));
+            std::memcpy(seg0_strides, strides, sizeof(strides));
+        }
         ConvSegDev& sd = p.seg[sgi];
         sd.ntaps = L.seg_ntaps[sgi];
         sd.ncb = L.seg_cpad[sgi] / 64;
@@ -647,6 +690,7 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
     p.scale = s / L.wscale;
     p.shift = o;
     p.silu = silu ? 1 : 0;
+    plan_halo(L, &p, seg0_base, seg0_dims, seg0_strides);
     ConvProfiler* prof = conv_profiler();
     if (prof) {
         // algorithmic work of the reference op (conv2d over the concat,
@@ -665,7 +709,8 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
             r.desc = "P" + std::to_string(L.P) + " M" + std::to_string(mt) + "x128 tile " + std::to_string(p.TI) +
                      "x" + std::to_string(p.TH) + "x" + std::to_string(p.TW) + " N" + std::to_string(L.n_pad) +
                      "/BN" + std::to_string(L.BN) + " K" + std::to_string(L.k_total) + " cg" + std::to_string(p.cg) +
-                     (out32 ? (nhwc32 ? " raw32" : " f32") : (silu ? " silu" : "")) + (p.tma_out ? " tma" : "");
+                     (out32 ? (nhwc32 ? " raw32" : " f32") : (silu ? " silu" : "")) + (p.tma_out ? " tma" : "") +
+                     (p.halo ? " halo" : "");
         }
         LC_CUDA(cudaEventCreate(&r.e0));
         LC_CUDA(cudaEventCreate(&r.e1));
