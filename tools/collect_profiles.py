@@ -55,6 +55,21 @@ if os.path.exists(rep):
         "# ncu --set full --clock-control none --import-source on -k regex:tap_tc --launch-skip 4 "
         "--launch-count 1 python tools/profile_step.py B 1\n# (K8, the decoder's fused last stage of the "
         "first 4-frame slice)\n\n" + det)
+rep = os.path.join(G, "full_halo.ncu-rep")
+if os.path.exists(rep):
+    det = subprocess.run(["ncu", "-i", rep, "--page", "details"], capture_output=True, text=True).stdout
+    open(os.path.join(P, f"ncu_full_halo_b_{rnd}.txt"), "w").write(
+        "# ncu --set full --clock-control none --import-source on -k regex:conv_tc --launch-skip 116 "
+        "--launch-count 1 python tools/profile_step.py B 3\n# (decoder dec2: P4 sub-pixel up-conv 128->128 at "
+        "256x256, halo-staged, weight-stationary, first 4-frame slice of run 3)\n\n" + det)
+src = os.path.join(G, "launch_d.csv")
+if os.path.exists(src):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), src, "4", "-v"],
+                         capture_output=True, text=True).stdout
+    open(os.path.join(P, f"ncu_launches_d_{rnd}.txt"), "w").write(
+        "# ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none "
+        "python bench.py --workload D --steps 1 --warmup 3\n# (last of 4 decodes; serialized: per-launch SHARES "
+        "are meaningful, absolute sums are not)\n" + out)
 for name in ("layers_b", "layers_c", "swap_timeline_b"):
     src = os.path.join(G, f"{name}.txt")
     if os.path.exists(src):
