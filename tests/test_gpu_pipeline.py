@@ -441,3 +441,48 @@ def test_fused_tap_kernel_matches_gemm_plus_gather(tmp_path, over):
         outs.append(np.load(path))
     assert np.array_equal(outs[0]["lat"], outs[1]["lat"])
     assert np.array_equal(outs[0]["v"], outs[1]["v"])
+
+
+_HALO_CHILD = r"""
+import sys, numpy as np
+import paper_2510_05367_b200 as lc
+over = eval(sys.argv[1])
+ctx = lc.Context(0)
+ctx.configure(lc.config_text(over, base=lc.DEFAULT_CONFIG))
+v, lat, _ = ctx.run_pipeline(want_latent=True)
+ctx.set_conv_profile(True)
+ctx.run_resident()
+halo = sum(" halo" in r["desc"] for r in ctx.conv_profile_records())
+np.savez(sys.argv[2], v=v, lat=lat, halo=halo)
+"""
+
+
+@pytest.mark.parametrize("over", [
+    # 1024x576 video, 2 frames: decoder up-convs on 128- and 256-wide
+    # lattices and the base-32 U-Net's level-0 3x3 convs (128 wide) run
+    # halo-staged
+    {"run.frames": 2, "run.height": 576, "run.width": 1024, "codec.stages": 3, "codec.width": 128,
+     "unet.base_channels": 32, "unet.depth": 3, "sampler.steps": 2, "cache.n": 2},
+    # B's frame-0 slice: dec2 (128 wide) halo-staged
+    dict(B_SHAPE, **{"run.frames": 1, "sampler.steps": 2}),
+])
+def test_halo_staging_is_bit_identical(tmp_path, over):
+    """Halo operand staging (one TMA box per channel block feeding every tap
+    through row-shifted descriptors, conv_tc.cu) accumulates in the same
+    (segment, channel block, tap) order as per-tap staging (LC_HALO=0):
+    bit-identical latents and videos."""
+    import os
+    import subprocess
+    import sys
+    outs = []
+    for halo in ("1", "0"):
+        path = str(tmp_path / f"halo_{halo}.npz")
+        env = dict(os.environ, LC_HALO=halo)
+        r = subprocess.run([sys.executable, "-c", _HALO_CHILD, repr(over), path], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+    assert int(outs[0]["halo"]) > 0 and int(outs[1]["halo"]) == 0  # the switch really changed the staging
+    assert np.isfinite(outs[0]["v"]).all()
+    assert np.array_equal(outs[0]["lat"], outs[1]["lat"])
+    assert np.array_equal(outs[0]["v"], outs[1]["v"])
