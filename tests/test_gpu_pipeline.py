@@ -450,6 +450,8 @@ over = eval(sys.argv[1])
 ctx = lc.Context(0)
 ctx.configure(lc.config_text(over, base=lc.DEFAULT_CONFIG))
 v, lat, _ = ctx.run_pipeline(want_latent=True)
+kv = lc.parse_config(lc.config_text(over, base=lc.DEFAULT_CONFIG))
+ctx.upload_latent(lc.randn(lc.derive_seed(int(kv["run.seed"]), 1), ctx.latent_elems()))
 ctx.set_conv_profile(True)
 ctx.run_resident()
 halo = sum(" halo" in r["desc"] for r in ctx.conv_profile_records())
