@@ -100,6 +100,19 @@ __host__ __device__ inline int num_stages(int bn, int tabf, int tma_out, int b_r
     return s > 8 ? 8 : (s < 2 ? 2 : s);
 }
 
+// Halo staging without a resident weight panel: separate rings, kHaloAStages
+// halo boxes (one per channel block, serving every tap) and up to
+// 8 - kHaloAStages weight boxes (one per (channel block, tap)); 0 if fewer
+// than 3 weight stages fit.
+constexpr int kHaloAStages = 2;
+template <int CG>
+__host__ __device__ inline int halo_ring_bstages(int bn, int tabf, int tma_out, int wide, int a_stage) {
+    const int bblk = (bn / CG) * kBK * 2;
+    int s = (kSmemMax - kSmemFixed - epi_smem_bytes(tabf, tma_out, wide, 0) - kHaloAStages * a_stage) / bblk;
+    s = s > 8 - kHaloAStages ? 8 - kHaloAStages : s;
+    return s < 3 ? 0 : s;
+}
+
 __host__ __device__ inline uint32_t tmem_cols_for(int bn) {
     // two accumulator buffers of bn fp32 columns, power of two >= 32
     const int need = 2 * bn;
@@ -175,9 +188,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < p.nseg; ++s) total_kb += p.seg[s].ntaps * p.seg[s].ncb;
     const bool b_res = CG == 1 && p.b_res;
     const int tabf = tab_floats(p.rc, p.BN);
-    const bool halo = CG == 1 && p.halo;
+    const bool halo = p.halo;
+    const bool halo_ring = halo && !b_res;  // halo boxes + a separate weight ring
     const int a_stage = a_stage_bytes(p);
-    const int stages = num_stages<CG>(p.BN, tabf, p.tma_out, b_res, total_kb, p.nhwc32, a_stage);
+    const int bstages = halo_ring ? halo_ring_bstages<CG>(p.BN, tabf, p.tma_out, p.nhwc32, a_stage) : 0;
+    // ring slots: A+B stages, or kHaloAStages halo stages then bstages weight stages
+    const int stages = halo_ring ? kHaloAStages + bstages
+                                 : num_stages<CG>(p.BN, tabf, p.tma_out, b_res, total_kb, p.nhwc32, a_stage);
     // fp32 raw (tap-to-N) epilogues need no offset registers: two chunks per wait
     constexpr int kCh = EPI == kEpiF32Raw ? 2 : kChunks;
     const int schunk = stage_chunk(p.nhwc32);
@@ -186,8 +203,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int bn_cta = p.BN / CG;  // B rows staged by this CTA
     const uint32_t b_bytes = static_cast<uint32_t>(bn_cta) * kBK * 2;
     uint8_t* smA = smem;
-    uint8_t* smB = smem + stages * a_stage;
-    const int b_blocks = b_res ? total_kb : stages;  // resident panel or ring
+    uint8_t* smB = smem + (halo_ring ? kHaloAStages : stages) * a_stage;
+    const int b_blocks = b_res ? total_kb : (halo_ring ? bstages : stages);  // resident panel or ring
     uint64_t* full_bar = reinterpret_cast<uint64_t*>(smB + b_blocks * b_bytes);
     uint64_t* empty_bar = full_bar + stages;
     uint64_t* tfull = empty_bar + stages;  // [2] accumulator ready
@@ -308,7 +325,52 @@ __global__ void __launch_bounds__(kThreads, 1)
                     phase ^= 1;
                 }
             };
-            for (int u = unit0; u < total_units; u += unit_step) {
+            if (halo_ring) {
+                // halo box per channel block into slots [0, kHaloAStages), then that
+                // block's per-tap weight boxes into slots [kHaloAStages, stages)
+                const ConvSegDev& sg = p.seg[0];
+                int as = 0, bs = 0;
+                uint32_t aph = 0, bph = 0;
+                for (int u = unit0; u < total_units; u += unit_step) {
+                    const TileCoord tc = coord(u);
+                    const int nrow = tc.n_tile * p.BN + static_cast<int>(rank) * bn_cta;
+                    const int cx = tc.X0 + p.hox[tc.parity] - sg.wx0;
+                    const int cy = tc.Y0 + p.hoy[tc.parity] - sg.wy0;
+                    for (int cb = 0; cb < sg.ncb; ++cb) {
+                        mbar_wait(&empty_bar[as], aph ^ 1);
+                        if (CG == 1) {
+                            mbar_arrive_expect_tx(&full_bar[as], a_bytes);
+                            tma_load_4d(smA + as * a_stage, &p.tmA[0], &full_bar[as], cb * kBK, cx, cy, tc.I0);
+                        } else {
+                            if (leader) mbar_arrive_expect_tx(&full_bar[as], CG * a_bytes);
+                            tma_load_4d_cg2(smA + as * a_stage, &p.tmA[0], mapa_shared(smem_u32(&full_bar[as]), 0),
+                                            cb * kBK, cx, cy, tc.I0);
+                        }
+                        if (++as == kHaloAStages) {
+                            as = 0;
+                            aph ^= 1;
+                        }
+                        for (int tap = 0; tap < sg.ntaps; ++tap) {
+                            const int slot = kHaloAStages + bs;
+                            mbar_wait(&empty_bar[slot], bph ^ 1);
+                            const int kcoord = sg.kbase + (tap * sg.ncb + cb) * kBK;
+                            if (CG == 1) {
+                                mbar_arrive_expect_tx(&full_bar[slot], b_bytes);
+                                tma_load_3d(smB + bs * b_bytes, &p.tmB, &full_bar[slot], kcoord, nrow, tc.parity);
+                            } else {
+                                if (leader) mbar_arrive_expect_tx(&full_bar[slot], CG * b_bytes);
+                                tma_load_3d_cg2(smB + bs * b_bytes, &p.tmB, mapa_shared(smem_u32(&full_bar[slot]), 0),
+                                                kcoord, nrow, tc.parity);
+                            }
+                            if (++bs == bstages) {
+                                bs = 0;
+                                bph ^= 1;
+                            }
+                        }
+                    }
+                }
+            }
+            for (int u = unit0; u < total_units && !halo_ring; u += unit_step) {
                 const TileCoord tc = coord(u);
                 if (halo) {
                     // one box per channel block serves every tap (see ConvParams::halo)
@@ -383,12 +445,46 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (CG == 1) umma_commit(bar);
                 else umma_commit_cg2(bar);
             };
+            int ras = 0, rbs = 0;  // halo_ring slots
+            uint32_t raph = 0, rbph = 0;
             if (b_res && unit0 < total_units) mbar_wait(bfull, 0);
             for (int u = unit0; u < total_units; u += unit_step) {
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * acc_stride;
-                if (halo) {
+                if (halo_ring) {
+                    const ConvSegDev& sg = p.seg[0];
+                    const int par = coord(u).parity;
+                    for (int cb = 0; cb < sg.ncb; ++cb) {
+                        mbar_wait(&full_bar[ras], raph);
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(smA + ras * a_stage);
+                        for (int tap = 0; tap < sg.ntaps; ++tap) {
+                            const int slot = kHaloAStages + rbs;
+                            mbar_wait(&full_bar[slot], rbph);
+                            tc_fence_after();
+                            if (elect_one()) {
+                                const int row = (sg.oy[par][tap] - p.hoy[par]) * p.hw + (sg.ox[par][tap] - p.hox[par]);
+                                mma_kblock(d_tmem, a0 + static_cast<uint32_t>(row) * 128u, smem_u32(smB + rbs * b_bytes),
+                                           (cb | tap) == 0);
+                                commit(&empty_bar[slot]);
+                                if (tap == sg.ntaps - 1) {
+                                    commit(&empty_bar[ras]);
+                                    if (cb == sg.ncb - 1) commit(&tfull[acc]);
+                                }
+                            }
+                            __syncwarp();
+                            if (++rbs == bstages) {
+                                rbs = 0;
+                                rbph ^= 1;
+                            }
+                        }
+                        if (++ras == kHaloAStages) {
+                            ras = 0;
+                            raph ^= 1;
+                        }
+                    }
+                } else if (halo) {
                     // b_res: every unit of this CTA is its slab's parity
                     const ConvSegDev& sg = p.seg[0];
                     const int par = slab_par;
@@ -740,8 +836,12 @@ size_t smem_bytes_for(const ConvParams& p) {
     for (int s = 0; s < p.nseg; ++s) total_kb += p.seg[s].ntaps * p.seg[s].ncb;
     const int b_res = CG == 1 && p.b_res;
     const int a_stage = a_stage_bytes(p);
-    const int st = num_stages<CG>(p.BN, tabf, p.tma_out, b_res, total_kb, p.nhwc32, a_stage);
     const size_t bblk = static_cast<size_t>(p.BN / CG) * kBK * 2;
+    if (p.halo && !b_res)
+        return kSmemFixed + static_cast<size_t>(kHaloAStages) * a_stage +
+               static_cast<size_t>(halo_ring_bstages<CG>(p.BN, tabf, p.tma_out, p.nhwc32, a_stage)) * bblk +
+               epi_smem_bytes(tabf, p.tma_out, p.nhwc32, 0);
+    const int st = num_stages<CG>(p.BN, tabf, p.tma_out, b_res, total_kb, p.nhwc32, a_stage);
     return kSmemFixed + static_cast<size_t>(st) * (a_stage + (b_res ? 0 : bblk)) + (b_res ? total_kb * bblk : 0) +
            epi_smem_bytes(tabf, p.tma_out, p.nhwc32, b_res);
 }
@@ -848,19 +948,28 @@ static bool want_b_res(const ConvParams& p, int parities) {
             total_kb * p.BN * kBK * 2) >= min_stages * a_stage;
 }
 
+static bool halo_ring_fits(const ConvParams& p) {
+    const int tabf = tab_floats(p.rc, p.BN), a_stage = a_stage_bytes(p);
+    return (p.cg == 2 ? halo_ring_bstages<2>(p.BN, tabf, p.tma_out, p.nhwc32, a_stage)
+                      : halo_ring_bstages<1>(p.BN, tabf, p.tma_out, p.nhwc32, a_stage)) > 0;
+}
+
 bool conv_tc_halo_fits(const ConvParams& p, int parities) {
-    return p.halo && p.cg == 1 && p.nseg == 1 && want_b_res(p, parities);
+    if (!p.halo || p.nseg != 1) return false;
+    if (p.cg == 1 && want_b_res(p, parities)) return true;
+    static const int ring = std::getenv("LC_HALO_RING") ? std::atoi(std::getenv("LC_HALO_RING")) : 1;
+    return ring && halo_ring_fits(p);
 }
 
 cudaError_t launch_conv_tc(const ConvParams& p, int parities, cudaStream_t stream) {
-    if (p.cg == 2) return p.halo ? cudaErrorInvalidValue : launch_cg<2>(p, parities, stream);
     if (p.halo) {
-        // halo staging runs only on the weight-stationary schedule
+        // weight-stationary when it pays (as below), else halo + weight rings
         if (!conv_tc_halo_fits(p, parities)) return cudaErrorInvalidValue;
         ConvParams q = p;
-        q.b_res = 1;
-        return launch_cg<1>(q, parities, stream);
+        q.b_res = p.cg == 1 && want_b_res(p, parities) ? 1 : 0;
+        return p.cg == 2 ? launch_cg<2>(q, parities, stream) : launch_cg<1>(q, parities, stream);
     }
+    if (p.cg == 2) return launch_cg<2>(p, parities, stream);
     if (want_b_res(p, parities)) {
         ConvParams q = p;
         q.b_res = 1;

@@ -505,13 +505,14 @@ Bank subpixel_shuffle_bank(const Bank& b) {
 }
 
 // Halo operand staging (ConvParams::halo) for layers that qualify: one
-// segment at source scale 1, several taps, one-row tiles of 128 pixels, the
-// weight-stationary schedule with >= 2 halo stages.  The activation map is
+// segment at source scale 1, several taps, one-row tiles of 128 pixels, and
+// either the weight-stationary schedule with >= 2 halo stages or (any CTA
+// group) 2 halo stages beside a ring of >= 3 weight stages.  The activation map is
 // re-encoded with the halo box {64, hw, hh, 1}; LC_HALO=0 disables it.
 void plan_halo(const TcLayer& L, ConvParams* p, const __half* base, const uint64_t* dims, const uint64_t* strides) {
     static const int env = std::getenv("LC_HALO") ? std::atoi(std::getenv("LC_HALO")) : 1;
     p->halo = 0;
-    if (!env || L.nseg != 1 || L.seg_m[0] != 1 || L.seg_ntaps[0] < 2 || p->cg != 1) return;
+    if (!env || L.nseg != 1 || L.seg_m[0] != 1 || L.seg_ntaps[0] < 2) return;
     if (p->TW != 128 || p->TH != 1 || p->TI != 1) return;
     int dxr = 0, dyr = 0;
     for (int q = 0; q < L.P; ++q) {

@@ -467,6 +467,9 @@ np.savez(sys.argv[2], v=v, lat=lat, halo=halo)
      "unet.base_channels": 32, "unet.depth": 3, "sampler.steps": 2, "cache.n": 2},
     # B's frame-0 slice: dec2 (128 wide) halo-staged
     dict(B_SHAPE, **{"run.frames": 1, "sampler.steps": 2}),
+    # C's frame-0 slice: d0 (320 -> 320 on the 128-wide level 0) halo-staged
+    # with a streamed weight ring (no resident panel)
+    dict(C_SHAPE, **{"run.frames": 1, "sampler.steps": 2}),
 ])
 def test_halo_staging_is_bit_identical(tmp_path, over):
     """Halo operand staging (one TMA box per channel block feeding every tap
