@@ -921,8 +921,15 @@ int conv_tc_cta_group(int BN, int m_tiles, int n_tiles, int parities, int k_bloc
     // long enough for the smem saving to matter (measured on B200: a win
     // from K = 45 blocks up, a loss at K <= 18 blocks) and there are enough
     // tiles to keep every pair busy.
+    // A long K loop (>= 64 blocks) also takes pairs when they fill >= 3/4 of
+    // the pair slots in one wave: single CTAs are ~35 % slower per tile there
+    // (B's mid block: 144 single CTAs of BN 144 -> 64 pairs of BN 160).
     const bool ok = BN % 32 == 0 && m_tiles >= 2;
-    int cg = (ok && k_blocks >= 32 && m_tiles * n_tiles * parities >= 2 * sm_count()) ? 2 : 1;
+    const int pair_units = (m_tiles + 1) / 2 * n_tiles * parities;
+    int cg = (ok && k_blocks >= 32 &&
+              (m_tiles * n_tiles * parities >= 2 * sm_count() || (k_blocks >= 64 && 4 * pair_units >= 3 * (sm_count() / 2))))
+                 ? 2
+                 : 1;
     if (g_cta_group_override == 1) cg = 1;
     if (g_cta_group_override == 2 && ok) cg = 2;
     return cg;

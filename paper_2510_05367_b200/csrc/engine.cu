@@ -283,8 +283,12 @@ std::unique_ptr<TcLayer> pack_tc_layer(Ledger* l, const Bank& b, int c_split, in
             if (n_t * bn - L->c_out >= bn) continue;  // an empty N tile
             if (static_cast<double>(n_t) * bn > 1.125 * round_up(L->c_out, 16)) continue;  // > 12.5% padding
             const int64_t tiles = static_cast<int64_t>(m_tiles_hint) * n_t * L->P;
-            const bool pair = bn % 32 == 0 && m_tiles_hint >= 2 && kb >= 32 && tiles >= 2 * 148;
-            const int64_t units = pair ? static_cast<int64_t>((m_tiles_hint + 1) / 2) * n_t * L->P : tiles;
+            const int64_t pair_units = static_cast<int64_t>((m_tiles_hint + 1) / 2) * n_t * L->P;
+            // pairs as conv_tc_cta_group picks them (>= 2 waves, or a long K
+            // loop filling >= 3/4 of the pair slots)
+            const bool pair = bn % 32 == 0 && m_tiles_hint >= 2 && kb >= 32 &&
+                              (tiles >= 2 * 148 || (kb >= 64 && 4 * pair_units >= 3 * 74));
+            const int64_t units = pair ? pair_units : tiles;
             const int slots = pair ? 74 : 148;
             const double cost = static_cast<double>((units + slots - 1) / slots) *
                                 (pair ? 0.95 : (kb >= 32 ? 1.35 : 1.0)) * (bn + 32);
