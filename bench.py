@@ -51,7 +51,7 @@ DESCR = {
     "C": "SVD-XT-shaped U-Net: 25 frames, latent 4x72x128 (1024x576 video), 25 Euler steps, cache N=2, "
          "async swap, chunk u0 2x2, sliced decode, base 320, depth 3, codec W=128 S=3",
     "A": "tiny desk config: 8 frames, latent 4x32x32, 25 steps, N=3, chunk u0 2x1",
-    "D": "SVD-XT VAE decode: latent 25x4x72x128 -> 25 frames 1024x576, codec W=128 S=3, 4-frame slices, "
+    "D": "SVD-XT VAE decode: latent 25x4x72x128 -> 25 frames 1024x576, codec W=128 S=3, 5-frame slices, "
          "contiguous frame blocks per GPU, NCCL gather of the decoded frames to rank 0",
 }
 
@@ -527,9 +527,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="lightcache", choices=["lightcache", "reference"])
     ap.add_argument("--workload", default="B", choices=sorted(WORKLOADS))
-    ap.add_argument("--decode-slice", type=int, default=4)
+    ap.add_argument("--decode-slice", type=int, default=None,
+                    help="frames per decoder slice (default: config A's 4 slices of 2 frames; otherwise the "
+                         "largest divisor of the frame count <= 5: B 4, C/D 5 -- even slices, no 1-frame tail)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.decode_slice is None:
+        T = int(WORKLOADS[args.workload].get("run.frames", 8))
+        args.decode_slice = 2 if args.workload == "A" else max(d for d in range(1, 6) if T % d == 0)
     if args.warmup < 3 and args.impl != "reference":
         args.warmup = 3
     world, rank, local = dist_init()
