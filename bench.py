@@ -5,13 +5,20 @@ Metric (BASELINE.json): end-to-end video frames/sec (+ peak HBM GB) against
 the uncached GPU run and the CPU reference.  One "step" is one whole video
 generation -- run_pipeline (proj/src/pipeline.cpp:64): the denoise loop with
 the feature cache / async swap / chunked execution, then sliced decode --
-on the workload BASELINE.json quotes at one GPU (configs[1], config B):
-AnimateDiff-Lightning-shaped U-Net, 16 frames, latent 4x64x64, 4 Euler
-steps, N=2, base 320, synthetic latent and random-init weights.
+on the LARGEST single-GPU configuration of BASELINE.json (configs[2],
+config C): SVD-XT-shaped U-Net, 25 frames, latent 4x72x128 (1024x576
+video), 25 Euler steps, cache N=2 with the async swap, base 320, synthetic
+latent and random-init weights (B, A and the decode workload D on request).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload B|C|A]
-  python bench.py --impl reference ...     (CPU reference arm)
-  torchrun --nproc-per-node N bench.py --gpus N   (N replicas, weak scaling)
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C|B|A|D]
+  python bench.py --impl reference ...     (CPU reference arm: oracle/_ref)
+  python bench.py --gpus N ...             (spawns N local ranks itself)
+  torchrun --nproc-per-node N bench.py --gpus N   (same, launched by torchrun)
+
+At N > 1 every rank runs one replica of the workload (denoising does not
+shard: batch 1 per GPU) and the line adds
+`decode_sharded`: workload D's sliced decode sharded over the N GPUs with
+the NCCL gather of the decoded slices (strong scaling).
 
 Rank 0 prints ONE JSON line.
 """
@@ -29,6 +36,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+# default_config() (proj/src/config.cpp:90-98): the workloads override it
+DEFAULT_TEXT = ""
 
 WORKLOADS = {
     # configs[1] of BASELINE.json
@@ -48,8 +58,9 @@ DESCR = {
     "B": "AnimateDiff-Lightning-shaped U-Net: 16 frames, latent 4x64x64 (512x512 video), 4 Euler steps, "
          "cache N=2 at seam m=0, async swap, chunk u0 2x2 exact halo, sliced decode (4 frames/slice), "
          "base 320, depth 3, codec W=128 S=3",
-    "C": "SVD-XT-shaped U-Net: 25 frames, latent 4x72x128 (1024x576 video), 25 Euler steps, cache N=2, "
-         "async swap, chunk u0 2x2, sliced decode, base 320, depth 3, codec W=128 S=3",
+    "C": "SVD-XT-shaped U-Net: 25 frames, latent 4x72x128 (1024x576 video), 25 Euler steps, cache N=2 at "
+         "seam m=0 (13 full + 12 cached steps), async swap, chunk u0 2x2 exact halo, sliced decode, base 320, "
+         "depth 3, codec W=128 S=3",
     "A": "tiny desk config: 8 frames, latent 4x32x32, 25 steps, N=3, chunk u0 2x1",
     "D": "SVD-XT VAE decode: latent 25x4x72x128 -> 25 frames 1024x576, codec W=128 S=3, 5-frame slices, "
          "contiguous frame blocks per GPU, NCCL gather of the decoded frames to rank 0",
@@ -68,8 +79,31 @@ def dist_init():
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # host-side plumbing only (barriers, max over ranks, the NCCL id);
+        # the data path's collective is the library's own NCCL gather
         dist.init_process_group("gloo", rank=rank, world_size=world)
     return world, rank, local
+
+
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` without torchrun: start N local ranks of this script (one
+    per GPU, RANK/LOCAL_RANK/WORLD_SIZE/MASTER_* set as torchrun sets them)
+    and wait; rank 0's stdout is the JSON line."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable] + sys.argv, env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    rc = 0
+    for p in procs:
+        rc = rc or p.wait()
+    return rc
 
 
 def barrier(world):
@@ -163,125 +197,146 @@ def decode_macs(kv: dict, frames: int) -> int:
     return 9 * tot * frames
 
 
-def run_macs(lc, text: str, kv: dict) -> int:
-    mf, mc, _ = lc.model_numbers(text)
+def _plan_counts(kv: dict):
+    """(full, cached) step counts of plan_steps (proj/src/cache.cpp:25-33)."""
     S, N = int(kv["sampler.steps"]), int(kv["cache.n"])
     enabled = kv["cache.enabled"] in ("true", "on", "1")
     nf = sum(1 for s in range(S) if (not enabled) or s % N == 0)
-    return nf * mf + (S - nf) * mc + decode_macs(kv, int(kv["run.frames"]))
+    return nf, S - nf
+
+
+def ref_run_macs(lib, kv: dict) -> int:
+    """MACs of one whole run_pipeline of `kv` from the REFERENCE's own
+    closed forms: flops_estimate per Full / Cached step
+    (proj/src/unet.cpp:287-300, via oracle/_ref or the restatement) over the
+    plan, plus the decoder's convs (proj/src/codec.cpp:103-113)."""
+    import lco
+    if isinstance(lib, lco.Reference):
+        nums = lib.model_numbers(kv)
+        mf, mc = nums[0], nums[1]
+    else:
+        mf, mc = lib.flops_estimate(kv, False), lib.flops_estimate(kv, True)
+    nf, nc = _plan_counts(kv)
+    return nf * mf + nc * mc + decode_macs(kv, int(kv["run.frames"]))
 
 
 # ---------------------------------------------------------------- CPU arm
-def cpu_sample_config(over: dict) -> dict:
-    """Bounded sample of the workload: one frame at 1/16 of the latent area
-    (latent 16x16 for B), same channels/depth/steps/cache plan; the work
-    is linear in frames x pixels, so frames/s is extrapolated by the exact
-    MAC ratio (conv MACs per tensor.cpp:194-195, decode per codec.cpp)."""
-    s = dict(over)
-    s["run.frames"] = 1
-    scale = 1 << int(s.get("codec.stages", 2))
-    depth = 1 << int(s.get("unet.depth", 3))
-    # 16x16 latent (>= 2^depth and divisible by eta/omega of the chunk)
-    s["run.height"] = 16 * scale
-    s["run.width"] = 16 * scale
-    return s
+# Bounded sample of a workload for the reference's CPU path: one frame (the
+# toy model has no cross-frame ops, SURVEY.md P6), the smallest latent the
+# U-Net depth admits with the workload's aspect (C: 8x16 = 1/72 of 72x128),
+# the same channels / depth / kernel / codec, and one refresh period of the
+# cache plan (N steps: 1 Full + N-1 Cached); the swap and chunking settings
+# stay.  The reference's work is linear in frames x pixels and per step, so
+# frames/s of the full workload = sample MACs / full-frame MACs x samples/s,
+# with both MAC counts from the reference's own closed forms.
+SAMPLES = {
+    "C": {"run.frames": 1, "run.height": 64, "run.width": 128, "sampler.steps": 2},
+    "B": {"run.frames": 1, "run.height": 64, "run.width": 64, "sampler.steps": 2},
+    "A": {"run.frames": 1, "run.height": 32, "run.width": 32, "sampler.steps": 3},
+    "D": {"run.frames": 1, "run.height": 64, "run.width": 128},
+}
+
+
+def _kv(over: dict) -> dict:
+    import lco
+    kv = lco.parse_text(DEFAULT_TEXT)
+    kv.update({k: str(v) for k, v in over.items()})
+    return kv
+
+
+def _cpu_lib():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import lco
+    if lco.Reference.available():
+        return lco.Reference(), "reference"
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    return lco.Restatement(), "port"
 
 
 def _cpu_worker(args):
-    text, kind = args
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    """One bounded sample through the reference's public API (run_pipeline,
+    or decode_sliced for workload D); returns its wall seconds."""
+    text, decode_only = args
+    lib, _ = _cpu_lib()
     import lco
     kv = lco.parse_text(text)
     t = time.time()
-    if kind == "reference":
-        lco.Reference().run_pipeline(kv)
+    if decode_only:
+        import numpy as np
+        s = 1 << int(kv["codec.stages"])
+        lat = np.random.default_rng(0).standard_normal(
+            (1, 1, int(kv["codec.latent_channels"]), int(kv["run.height"]) // s,
+             int(kv["run.width"]) // s)).astype(np.float32)
+        lib.decode(kv, lat)
     else:
-        os.environ.setdefault("OMP_NUM_THREADS", "1")
-        lco.Restatement().run_pipeline(kv)
+        lib.run_pipeline(kv)
     return time.time() - t
 
 
-def cpu_measure(lc, over: dict, workers: int, reps: int):
-    """Time the reference CPU path on the bounded sample; returns
-    (frames/s extrapolated to the full workload, kind, sample description)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+def cpu_sample(workload: str):
+    """(sample config kv, sample MACs, full-workload MACs per frame, kind)."""
+    lib, kind = _cpu_lib()
+    full = _kv(WORKLOADS[workload])
+    samp = _kv(dict(WORKLOADS[workload], **SAMPLES[workload]))
+    T = int(full["run.frames"])
+    if workload == "D":
+        return samp, decode_macs(samp, 1), decode_macs(full, T) / T, kind
+    return samp, ref_run_macs(lib, samp), ref_run_macs(lib, full) / T, kind
+
+
+def _sample_desc(workload, samp, macs_s, macs_f, kind):
+    s = 1 << int(samp["codec.stages"])
+    what = "decode of 1 frame" if workload == "D" else (
+        f"run_pipeline of 1 frame, {samp['sampler.steps']} steps (one N={samp['cache.n']} cache period)")
+    return (f"{kind} CPU path ({'oracle/_ref, the unmodified reference' if kind == 'reference' else 'oracle port'}): "
+            f"{what} at latent {int(samp['run.height']) // s}x{int(samp['run.width']) // s}, same channels/depth/codec; "
+            f"{macs_s / 1e9:.2f} GMAC per sample vs {macs_f / 1e9:.1f} GMAC per full-workload frame "
+            f"(reference flops_estimate + decoder MACs); frames/s = sample MACs / frame MACs x samples/s")
+
+
+def cpu_measure(workload: str, reps: int = 1):
+    """Single-core reference sample for the GPU arm's cpu_baseline."""
+    samp, macs_s, macs_f, kind = cpu_sample(workload)
     import lco
-    kind = "reference" if lco.Reference.available() else "port"
-    full_text = lc.config_text(over, base=lc.DEFAULT_CONFIG)
-    samp = cpu_sample_config(over)
-    samp_text = lc.config_text(samp, base=lc.DEFAULT_CONFIG)
-    kv_full = lco.parse_text(full_text)
-    kv_s = lco.parse_text(samp_text)
-    macs_full = run_macs(lc, full_text, kv_full) / int(kv_full["run.frames"])
-    macs_s = run_macs(lc, samp_text, kv_s)
-    times = []
-    if workers <= 1:
-        for _ in range(reps):
-            times.append(_cpu_worker((lco.to_text(kv_s), kind)))
-        per_sample = statistics.median(times)
-        fps_sample = 1.0 / per_sample
-    else:
-        import multiprocessing as mp
-        with mp.get_context("fork").Pool(workers) as pool:
-            t0 = time.time()
-            for _ in range(reps):
-                pool.map(_cpu_worker, [(lco.to_text(kv_s), kind)] * workers)
-            wall = time.time() - t0
-        fps_sample = workers * reps / wall
-        per_sample = wall / reps
-    fps = fps_sample * macs_s / macs_full
-    desc = (f"1 frame at latent {kv_s['run.height']}x{kv_s['run.width']} pixels/{1 << int(kv_s['codec.stages'])} "
-            f"(same channels, depth, {kv_s['sampler.steps']} steps, N={kv_s['cache.n']}), "
-            f"{macs_s / 1e9:.2f} GMAC vs {macs_full / 1e9:.1f} GMAC per full-size frame; "
-            f"{per_sample:.1f} s per sample; frames/s extrapolated by the MAC ratio")
-    return fps, kind, desc
-
-
-def _cpu_decode_worker(text):
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import numpy as np
-
-    import lco
-    kv = lco.parse_text(text)
-    s = 1 << int(kv["codec.stages"])
-    lat = np.random.default_rng(0).standard_normal(
-        (1, 1, 4, int(kv["run.height"]) // s, int(kv["run.width"]) // s)).astype(np.float32)
-    lib = lco.Reference() if lco.Reference.available() else lco.Restatement()
-    t = time.time()
-    lib.decode(kv, lat)
-    return time.time() - t
+    times = [_cpu_worker((lco.to_text(samp), workload == "D")) for _ in range(reps)]
+    per = statistics.median(times)
+    fps = macs_s / macs_f / per
+    return {"value": fps, "unit": "frames/s", "cores": 1, "kind": kind,
+            "sample": _sample_desc(workload, samp, macs_s, macs_f, kind) + f"; {per:.1f} s per sample, 1 core"}
 
 
 def reference_arm(args, world, rank):
-    import paper_2510_05367_b200 as lc
+    """The reference's own CPU implementation of the path (oracle/_ref:
+    the unmodified proj/src compiled in place; run_pipeline,
+    proj/src/pipeline.cpp:64-228) on all host cores: each step runs one
+    bounded sample per core in a persistent process pool.  Nothing of the
+    product (paper_2510_05367_b200) is imported or loaded here."""
     if rank != 0:
         return
-    over = WORKLOADS[args.workload]
-    workers = min(os.cpu_count() or 1, 64)
-    if args.workload == "D":
-        # the reference's decode of one frame per host process (decode is frame-wise)
-        import multiprocessing as mp
-        sys.path.insert(0, os.path.join(ROOT, "oracle"))
-        import lco
-        kind = "reference" if lco.Reference.available() else "port"
-        text = lc.config_text(over, base=lc.DEFAULT_CONFIG)
-        with mp.get_context("fork").Pool(workers) as pool:
+    import multiprocessing as mp
+    import lco
+    samp, macs_s, macs_f, kind = cpu_sample(args.workload)
+    workers = max(1, min(os.cpu_count() or 1, 256))
+    job = (lco.to_text(samp), args.workload == "D")
+    with mp.get_context("spawn").Pool(workers) as pool:
+        for _ in range(args.warmup):
+            pool.map(_cpu_worker, [job] * workers)
+        walls = []
+        for _ in range(args.steps):
             t0 = time.time()
-            for _ in range(max(1, args.steps // 10)):
-                pool.map(_cpu_decode_worker, [text] * workers)
-            wall = time.time() - t0
-        fps = workers * max(1, args.steps // 10) / wall
-        desc = f"1 frame decoded per host process, {workers} processes, {max(1, args.steps // 10)} rounds"
-    else:
-        # each round = one bounded sample per host process (~10 s); capped so
-        # the arm ends within a few minutes whatever --steps is
-        fps, kind, desc = cpu_measure(lc, over, workers, min(args.steps, 8))
+            pool.map(_cpu_worker, [job] * workers)
+            walls.append(time.time() - t0)
+    total = sum(walls)
+    frames = workers * args.steps * macs_s / macs_f  # full-workload frame equivalents
+    fps = frames / total
+    desc = _sample_desc(args.workload, samp, macs_s, macs_f, kind) + (
+        f"; {workers} processes x {args.steps} steps, {total / args.steps:.2f} s per step")
     line = {"metric": "video_frames_per_sec", "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * WORKLOADS_FRAMES(over) / fps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
-            "data": "synthetic (seeded randn latent, random-init weights)",
-            "config": {"workload": DESCR[args.workload], "parallelism": f"{workers} CPU processes"},
-            "impl": "reference",
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak" if args.workload != "D" else "strong",
+            "vs_baseline": None, "dtype": "fp32",
+            "data": "synthetic (seeded randn latent, random-init weights of the reference architecture)",
+            "config": workload_config(args, world), "impl": "reference",
             "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": workers, "kind": kind, "sample": desc},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -307,8 +362,15 @@ def swap_summary(rep: dict) -> dict:
             "overlap_frac": 1.0 - stall / xfer_ms if xfer_ms > 0 else None}
 
 
-def WORKLOADS_FRAMES(over):
-    return int(over.get("run.frames", 8))
+def workload_config(args, world) -> dict:
+    """`config` of the JSON line -- identical for both arms (the reference
+    arm times a bounded sample of this same workload, see SAMPLES)."""
+    T = int(WORKLOADS[args.workload].get("run.frames", 8))
+    return {"workload": DESCR[args.workload], "frames_per_step": T,
+            "parallelism": (f"decode sharded x{world}" if args.workload == "D" else
+                            (f"{world} replicas (one video per GPU)" if world > 1 else "single GPU")),
+            "l2": "working set per step > 126 MB L2 (inputs larger than L2)",
+            "decode_slice_frames": args.decode_slice}
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -321,6 +383,7 @@ def gpu_arm(args, world, rank, local):
     kv = lc.parse_config(text)
     T = int(kv["run.frames"])
     ctx = lc.Context(local)
+    free0, total_mem = ctx.mem_info()
     ctx.configure(text)
     ctx.set_decode_slice(args.decode_slice)
     n_lat, n_vid = ctx.latent_elems(), ctx.video_elems()
@@ -333,9 +396,9 @@ def gpu_arm(args, world, rank, local):
     ctx.upload_latent(x0.array)
     for _ in range(args.warmup):
         rep = ctx.run_resident()
+    free1, _ = ctx.mem_info()
     barrier(world)
     ctx.timer_start()
-    launches = 0
     for _ in range(args.steps):
         ctx.run_resident_async()  # graph replays queued back to back
     rep = ctx.wait()
@@ -387,24 +450,27 @@ def gpu_arm(args, world, rank, local):
     ms_b = allmax(world, ctx.timer_stop())
     uncached = {"value": world * T * nb / (ms_b / 1000.0), "unit": "frames/s",
                 "hbm_peak_gb": rep_b["hbm_peak_bytes"] / 1e9, "denoiser_macs": rep_b["mac"]["denoiser_total"]}
+    x0.free()
+    vid.free()
+    ctx.close()
 
-    line = None
+    sharded = decode_sharded_leg(args, world, rank, local) if world > 1 else None
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            fps, kind, desc = cpu_measure(lc, over, 1, 1)
-            cpu = {"value": fps, "unit": "frames/s", "cores": 1, "kind": kind, "sample": desc}
+            cpu = cpu_measure(args.workload)
         line = {
             "metric": "video_frames_per_sec", "value": value, "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "fp16 (fp32 accumulate; fp32 latent, sampler and video)",
             "data": "synthetic (seeded randn latent, random-init weights of the reference architecture)",
-            "config": {"workload": DESCR[args.workload], "frames_per_step": T,
-                       "parallelism": "replicas" if world > 1 else "single GPU",
-                       "l2": "working set per step ~0.9 GB > 126 MB L2 (inputs larger than L2)",
-                       "decode_slice_frames": args.decode_slice},
+            "config": workload_config(args, world),
             "hbm_peak_gb": rep["hbm_peak_bytes"] / 1e9,
+            "hbm_peaks_by_stage_gb": {k: v["fast"] / 1e9 for k, v in rep["peaks"].items()},
+            "cuda_mem_in_use_gb": (free0 - free1) / 1e9,
+            "cuda_mem_note": "cudaMemGetInfo drop from context creation to after warm-up (ledger buffers + "
+                             "CUDA graph and allocator overhead); hbm_peak_gb is the engine ledger's peak",
             "uncached": uncached,
             "speedup_vs_uncached": value / uncached["value"],
             "denoise_ms": rep["device_ms"]["denoise"], "decode_ms": rep["device_ms"]["decode"],
@@ -425,99 +491,122 @@ def gpu_arm(args, world, rank, local):
             "clocks": clk,
             "video_finite": finite,
         }
+        if sharded:
+            line["decode_sharded"] = sharded
         if cpu:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
-    x0.free()
-    vid.free()
-    ctx.close()
 
 
-def decode_arm(args, world, rank, local):
-    """Workload D (BASELINE.json configs[3]): sliced decode sharded over N
-    GPUs (lc_decode_sharded: contiguous frame blocks, grouped NCCL
-    send/recv to rank 0).  A step decodes the whole 25-frame latent video;
-    value = frames / device time of (latent shard H2D + decode + gather),
-    max over ranks; e2e adds the D2H of the full video on rank 0."""
+def _nccl_ctx(lc, ctx, world, rank):
+    import torch.distributed as dist
+    uid = [lc.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    ctx.nccl_init(uid[0], world, rank)
+
+
+def decode_sharded_leg(args, world, rank, local, steps=None):
+    """Workload D over all ranks: lc_decode_sharded (balanced frame blocks,
+    per-slice NCCL sends to rank 0).  value: frames / device time of (shard
+    H2D + decode + gather), max over ranks; e2e: every rank also downloads
+    its frames into one shared pinned host video (parallel host links)."""
     import numpy as np
 
     import paper_2510_05367_b200 as lc
-    over = WORKLOADS["D"]
-    text = lc.config_text(over, base=lc.DEFAULT_CONFIG)
+    steps = steps or args.steps
+    text = lc.config_text(WORKLOADS["D"], base=lc.DEFAULT_CONFIG)
     kv = lc.parse_config(text)
     T, s = int(kv["run.frames"]), 1 << int(kv["codec.stages"])
     H, W = int(kv["run.height"]), int(kv["run.width"])
     ctx = lc.Context(local)
     ctx.configure(text)
     if world > 1:
+        _nccl_ctx(lc, ctx, world, rank)
+    lat = lc.randn(lc.derive_seed(int(kv["run.seed"]), 1), T * 4 * (H // s) * (W // s))
+    lat_p = lc.PinnedArray(lat.size)
+    lat_p.array[:] = lat
+    name = f"lc_bench_video_{os.environ.get('MASTER_PORT', '0')}"
+    if world > 1:
         import torch.distributed as dist
-        uid = [lc.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ctx.nccl_init(uid[0], world, rank)
-    lat = lc.randn(lc.derive_seed(int(kv["run.seed"]), 1), T * 4 * (H // s) * (W // s)).reshape(
-        1, T, 4, H // s, W // s)
-    lat_p = lc.PinnedArray(lat.size)  # pinned host buffers: the API's fast path
-    lat_p.array[:] = lat.reshape(-1)
-    vid_p = lc.PinnedArray(T * 3 * H * W)
-    clocks = ClockSampler(local).start()
-    for _ in range(args.warmup):
-        ctx.decode_sharded(lat_p, args.decode_slice, out=vid_p)
+        if rank == 0:
+            shared = lc.SharedVideo(name, T * 3 * H * W, create=True)
+        dist.barrier()
+        if rank != 0:
+            shared = lc.SharedVideo(name, T * 3 * H * W, create=False)
+    else:
+        shared = lc.PinnedArray(T * 3 * H * W)
+    sl = max(d for d in range(1, 6) if T % d == 0) if args.workload != "D" else args.decode_slice
+    for _ in range(max(3, args.warmup)):
+        ctx.decode_sharded(lat_p, sl)
     barrier(world)
-    ctx.timer_start()
     dev_ms = 0.0
     launches = 0
-    for _ in range(args.steps):
-        video, ms = ctx.decode_sharded(lat_p, args.decode_slice, out=vid_p)
+    for _ in range(steps):
+        _, ms = ctx.decode_sharded(lat_p, sl)  # device resident: the gathered video stays in rank 0's HBM
         dev_ms += ms
         launches += ctx.kernel_launches()
-    ms_e = allmax(world, ctx.timer_stop())
     dev_ms = allmax(world, dev_ms)
+    for _ in range(2):
+        ctx.decode_sharded(lat_p, sl, out=shared, host_shared=world > 1)
+    barrier(world)
+    e2e_ms = 0.0
+    for _ in range(steps):
+        _, ms = ctx.decode_sharded(lat_p, sl, out=shared, host_shared=world > 1)
+        e2e_ms += ms
+    e2e_ms = allmax(world, e2e_ms)
+    barrier(world)
+    finite = bool(np.isfinite(shared.array).all()) if rank == 0 else None
+    barrier(world)
+    shared.free()
+    lat_p.free()
+    ctx.close()
+    return {"workload": DESCR["D"], "n_gpus": world, "steps": steps, "decode_slice_frames": sl,
+            "value": T * steps / (dev_ms / 1e3), "unit": "frames/s", "ms_per_step": dev_ms / steps,
+            "scaling": "strong",
+            "e2e": {"value": T * steps / (e2e_ms / 1e3), "unit": "frames/s",
+                    "h2d_bytes_per_step": T * 4 * (H // s) * (W // s) * 4, "d2h_bytes_per_step": T * 3 * H * W * 4,
+                    "note": "each rank H2Ds its latent block and D2Hs its own frames into one shared pinned video"},
+            "gpu_launches": launches, "video_finite": finite}
+
+
+def decode_arm(args, world, rank, local):
+    """Workload D (BASELINE.json configs[3]) as the headline workload: the
+    sharded sliced decode over the launch's N GPUs (strong scaling)."""
+    import paper_2510_05367_b200 as lc
+    clocks = ClockSampler(local).start()
+    d = decode_sharded_leg(args, world, rank, local)
     clk = clocks.stop()
-    value = T * args.steps / (dev_ms / 1e3)
-    e2e = T * args.steps / (ms_e / 1e3)
-    # roofline: the decoder convs of one single-GPU decode, event-timed
+    # roofline: the decoder convs of one single-GPU 5-frame decode, event-timed
+    text = lc.config_text(WORKLOADS["D"], base=lc.DEFAULT_CONFIG)
+    kv = lc.parse_config(text)
+    s = 1 << int(kv["codec.stages"])
+    ctx = lc.Context(local)
+    ctx.configure(text)
+    lat = lc.randn(7, 5 * 4 * (int(kv["run.height"]) // s) * (int(kv["run.width"]) // s)).reshape(
+        1, 5, 4, int(kv["run.height"]) // s, int(kv["run.width"]) // s)
     ctx.set_conv_profile(True)
-    ctx.decode(lat[:, :min(T, 4)], args.decode_slice)
+    ctx.decode(lat, args.decode_slice)
     prof = ctx.conv_profile()
     ctx.set_conv_profile(False)
+    ctx.close()
     peak, peak_src = peaks()
     achieved = prof["alg_flops"] / (prof["ms"] / 1e3) / 1e12 if prof["ms"] > 0 else 0.0
     if rank == 0:
-        cpu = None
-        if world == 1 and not args.no_cpu_baseline:
-            sys.path.insert(0, os.path.join(ROOT, "oracle"))
-            import lco
-            kind = "reference" if lco.Reference.available() else "port"
-            lib = lco.Reference() if kind == "reference" else lco.Restatement()
-            t0 = time.time()
-            lib.decode(lco.parse_text(text), lat[:, :1])
-            dt = time.time() - t0
-            cpu = {"value": 1.0 / dt, "unit": "frames/s", "cores": 1, "kind": kind,
-                   "sample": f"1 frame decoded by the {kind} CPU decoder ({dt:.1f} s)"}
         line = {
-            "metric": "video_frames_per_sec", "value": value, "unit": "frames/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
+            "metric": "video_frames_per_sec", "value": d["value"], "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": d["ms_per_step"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "fp16 (fp32 accumulate; fp32 latent and video)",
             "data": "synthetic (seeded randn latent, random-init codec weights of the reference architecture)",
-            "config": {"workload": DESCR["D"], "frames_per_step": T, "parallelism": f"decode sharded x{world}",
-                       "l2": "video 177 MB > 126 MB L2 (outputs larger than L2)",
-                       "decode_slice_frames": args.decode_slice},
-            "e2e": {"value": e2e, "unit": "frames/s", "h2d_bytes_per_step": int(lat.nbytes) // world,
-                    "d2h_bytes_per_step": int(video.nbytes)},
+            "config": workload_config(args, world), "e2e": d["e2e"],
             "roofline": {"bound": "tensor", "kernel": "conv_tc_kernel (decoder convs)", "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                          "traffic": None, "peak_source": peak_src},
-            "gpu_launches": launches,
-            "clocks": clk,
-            "video_finite": bool(np.isfinite(video).all()) if rank == 0 else None,
+            "gpu_launches": d["gpu_launches"], "clocks": clk, "video_finite": d["video_finite"],
         }
-        if cpu:
-            line["cpu_baseline"] = cpu
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_measure("D")
         print(json.dumps(line), flush=True)
-    lat_p.free()
-    vid_p.free()
-    ctx.close()
 
 
 def main():
@@ -526,7 +615,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="lightcache", choices=["lightcache", "reference"])
-    ap.add_argument("--workload", default="B", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="C", choices=sorted(WORKLOADS),
+                    help="C (default): the largest single-GPU configuration of BASELINE.json")
     ap.add_argument("--decode-slice", type=int, default=None,
                     help="frames per decoder slice (default: config A's 4 slices of 2 frames; otherwise the "
                          "largest divisor of the frame count <= 5: B 4, C/D 5 -- even slices, no 1-frame tail)")
@@ -537,6 +627,8 @@ def main():
         args.decode_slice = 2 if args.workload == "A" else max(d for d in range(1, 6) if T % d == 0)
     if args.warmup < 3 and args.impl != "reference":
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        sys.exit(spawn_ranks(args.gpus))
     world, rank, local = dist_init()
     if args.impl == "reference":
         reference_arm(args, world, rank)

@@ -114,8 +114,11 @@ int lc_free_pinned(void* p);
 int lc_forward(lc_ctx* ctx, const float* x, int64_t T, int64_t timestep, const float* deep_in,
                float* deep_out, float* eps);
 /* decode_batch / decode_sliced (proj/src/codec.cpp:117-145) of n latents
- * (n,1,C,h,w) -> (n,1,3,H,W); `slice` frames per launch group. */
-int lc_decode(lc_ctx* ctx, const float* latents, int64_t n, int64_t slice, float* video);
+ * (n,1,c,h,w) -> (n,1,3,H,W); `slice` frames per launch group.  c must be
+ * the codec's latent channel count (ShapeError, as codec.cpp:129-131) and
+ * h x w the configured latent geometry (ShapeError otherwise). */
+int lc_decode(lc_ctx* ctx, const float* latents, int64_t n, int64_t c, int64_t h, int64_t w,
+              int64_t slice, float* video);
 /* Quality metrics: per-frame PSNR (dB, capped at 99) and
  * mean 7x7-window SSIM of two b=1 videos {t,c,h,w} fp32 (host or device
  * pointers), data range L.  Replaces psnr / ssim / video_series
@@ -164,19 +167,39 @@ uint64_t lc_derive_seed(uint64_t seed, uint64_t stream);
 int lc_randn(uint64_t seed, int64_t n, float* out);
 
 /* Multi-GPU sliced decode (one process per GPU) --------------------------- */
-/* Frame shard of rank r out of g for T frames: contiguous blocks of
- * ceil(T/g). */
+/* Frame shard of rank r out of g for T frames: balanced contiguous blocks
+ * (the first T % g ranks take one more frame; 25 on
+ * 8 GPUs = 4,3,3,3,3,3,3,3). */
 int lc_shard_frames(int64_t T, int world, int rank, int64_t* first, int64_t* count);
+/* The gather schedule lc_decode_sharded executes: rows of (round, rank,
+ * first_frame, count); round i moves the i-th decoded slice of every rank
+ * that has one to rank 0.  rows = NULL queries n_rows. */
+int lc_gather_plan(int64_t T, int world, int64_t slice, int64_t* rows, int64_t cap_rows,
+                   int64_t* n_rows);
 /* NCCL communicator for the decode gather.  lc_nccl_unique_id writes
  * 128 bytes; the caller distributes them (e.g. over torch.distributed). */
 int lc_nccl_unique_id(uint8_t* id128);
 int lc_nccl_init(lc_ctx* ctx, const uint8_t* id128, int world, int rank);
-/* Decode this rank's shard of `latents` (T,1,C,h,w, replicated) and gather
- * every frame on rank 0 over NVLink (ncclGather emulated with grouped
- * send/recv); video (T,1,3,H,W) is written on rank 0 only (may be NULL
- * elsewhere).  ms_out (nullable) receives the device time of decode+gather. */
-int lc_decode_sharded(lc_ctx* ctx, const float* latents, int64_t T, int64_t slice, float* video,
-                      float* ms_out);
+/* Decode this rank's shard of `latents` (T,1,c,h,w, replicated on every
+ * rank) slice by slice (decode_sliced, proj/src/codec.cpp:126-145) and
+ * gather every frame into rank 0's HBM over NVLink: each slice is sent with
+ * ncclSend as soon as it is decoded, rank 0 receives round by round
+ * (lc_gather_plan) while its own slices decode.  video (T,1,3,H,W host,
+ * nullable): without flags rank 0 writes the whole video (other ranks may
+ * pass NULL); with LC_SHARD_HOST_SHARED `video` is ONE host buffer mapped by
+ * every rank (e.g. a shared-memory segment registered with
+ * lc_host_register) and each rank downloads its own frames into it over its
+ * own host link.  ms_out (nullable): device time of H2D + decode + gather
+ * (+ download) on this rank. */
+#define LC_SHARD_HOST_SHARED 1
+int lc_decode_sharded(lc_ctx* ctx, const float* latents, int64_t T, int64_t c, int64_t h, int64_t w,
+                      int64_t slice, float* video, int flags, float* ms_out);
+/* cudaMemGetInfo of the context's device (cross-check of the ledger's
+ * physical HBM peak). */
+int lc_mem_info(lc_ctx* ctx, int64_t* free_bytes, int64_t* total_bytes);
+/* Page-lock caller memory (cudaHostRegister, portable) for fast copies. */
+int lc_host_register(void* p, int64_t bytes);
+int lc_host_unregister(void* p);
 
 #ifdef __cplusplus
 }

@@ -96,7 +96,8 @@ EXPORTS = [
     "lc_set_decode_slice",
     "lc_forward", "lc_decode", "lc_video_metrics", "lc_ledger_csv", "lc_ledger_summary", "lc_conv2d", "lc_up_conv2d", "lc_plan_steps", "lc_split",
     "lc_model_numbers", "lc_simulate_timeline", "lc_derive_seed", "lc_randn", "lc_shard_frames", "lc_nccl_unique_id",
-    "lc_nccl_init", "lc_decode_sharded", "lc_timer_start", "lc_timer_stop", "lc_set_conv_profile",
+    "lc_nccl_init", "lc_decode_sharded", "lc_gather_plan", "lc_host_register", "lc_host_unregister", "lc_mem_info",
+    "lc_timer_start", "lc_timer_stop", "lc_set_conv_profile",
     "lc_conv_profile", "lc_conv_profile_records", "lc_kernel_launches", "lc_alloc_pinned", "lc_free_pinned",
 ]
 
@@ -218,6 +219,20 @@ def shard_frames(T: int, world: int, rank: int):
     return f0.value, cnt.value
 
 
+def gather_plan(T: int, world: int, slice_frames: int) -> np.ndarray:
+    """The slice-by-slice gather schedule of lc_decode_sharded: int64 rows of
+    (round, rank, first_frame, count)."""
+    n = I64()
+    _check(lib().lc_gather_plan(I64(T), ctypes.c_int(world), I64(slice_frames), None, I64(0), ctypes.byref(n)))
+    rows = np.empty((max(1, n.value), 4), np.int64)
+    _check(lib().lc_gather_plan(I64(T), ctypes.c_int(world), I64(slice_frames), _p(rows), I64(n.value),
+                                ctypes.byref(n)))
+    return rows[:n.value]
+
+
+SHARD_HOST_SHARED = 1
+
+
 # ----------------------------------------------------------------- context
 class Context:
     """One GPU: streams, packed weights and device buffers (lc_ctx)."""
@@ -250,6 +265,12 @@ class Context:
 
     def video_elems(self) -> int:
         return lib().lc_video_elems(self._h)
+
+    def mem_info(self):
+        """(free, total) device bytes (cudaMemGetInfo)."""
+        f, t = I64(), I64()
+        _check(lib().lc_mem_info(self._h, ctypes.byref(f), ctypes.byref(t)))
+        return f.value, t.value
 
     def set_decode_slice(self, frames: int):
         _check(lib().lc_set_decode_slice(self._h, I64(frames)))
@@ -350,12 +371,17 @@ class Context:
         return eps, deep_out
 
     def decode(self, latents: np.ndarray, slice_frames: int = 1) -> np.ndarray:
+        """decode_sliced (proj/src/codec.cpp:126-145) of latents (b,t,c,h,w)."""
         lat = _f32(latents)
+        if lat.ndim != 5:
+            raise ShapeError("decode: latents must be (b, t, c, h, w)")
         cfg = parse_config(self._text)
         s = 1 << int(cfg["codec.stages"])
-        n = lat.shape[0] * lat.shape[1]
-        out = np.empty((lat.shape[0], lat.shape[1], 3, lat.shape[3] * s, lat.shape[4] * s), np.float32)
-        _check(lib().lc_decode(self._h, _p(lat), I64(n), I64(slice_frames), _p(out)))
+        ic = int(cfg.get("codec.image_channels", 3))
+        b, t, c, h, w = lat.shape
+        out = np.empty((b, t, ic, h * s, w * s), np.float32)
+        # c / h / w are validated by the library against the configured codec
+        _check(lib().lc_decode(self._h, _p(lat), I64(b * t), I64(c), I64(h), I64(w), I64(slice_frames), _p(out)))
         return out
 
     def video_metrics(self, a, b, data_range: float = 1.0):
@@ -395,25 +421,40 @@ class Context:
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
         _check(lib().lc_nccl_init(self._h, buf, ctypes.c_int(world), ctypes.c_int(rank)))
 
-    def decode_sharded(self, latents, slice_frames: int = 4, out=None):
-        """lc_decode_sharded; `latents` / `out` may be PinnedArray (fast host
-        copies) or numpy arrays.  Returns (video, device ms)."""
+    def decode_sharded(self, latents, slice_frames: int = 4, out=None, host_shared: bool = False):
+        """lc_decode_sharded; `latents` may be a PinnedArray (the whole
+        (1,T,C,h,w) latent video of the config) or a numpy array (b,t,c,h,w);
+        `out` a PinnedArray / SharedVideo / numpy array or None (device
+        only: the gathered video stays in rank 0's HBM).  Returns (video or
+        None, device ms)."""
         cfg = parse_config(self._text)
         s = 1 << int(cfg["codec.stages"])
+        C = int(cfg["codec.latent_channels"])
         if isinstance(latents, PinnedArray):
-            lat_ptr, T = latents.ptr, int(cfg["run.frames"])
+            T = int(cfg["run.frames"])
             h, w = int(cfg["run.height"]) // s, int(cfg["run.width"]) // s
+            if latents.n != T * C * h * w:
+                raise ShapeError("decode_sharded: pinned latent size does not match the config")
+            lat_ptr, c = latents.ptr, C
         else:
             lat = _f32(latents)
-            lat_ptr, T = _p(lat), lat.shape[0] * lat.shape[1]
-            h, w = lat.shape[3], lat.shape[4]
-        if out is None:
-            out = np.empty((1, T, 3, h * s, w * s), np.float32)
-        out_ptr = out.ptr if isinstance(out, PinnedArray) else _p(out)
+            if lat.ndim != 5:
+                raise ShapeError("decode_sharded: latents must be (b, t, c, h, w)")
+            lat_ptr, T, c, h, w = _p(lat), lat.shape[0] * lat.shape[1], lat.shape[2], lat.shape[3], lat.shape[4]
+        nvid = T * 3 * h * s * w * s
+        out_ptr = None
+        if out is not None:
+            n_out = out.n if hasattr(out, "n") else out.size
+            if n_out < nvid:
+                raise ShapeError("decode_sharded: output buffer too small")
+            out_ptr = out.ptr if hasattr(out, "ptr") else _p(out)
         ms = ctypes.c_float()
-        _check(lib().lc_decode_sharded(self._h, lat_ptr, I64(T), I64(slice_frames), out_ptr, ctypes.byref(ms)))
-        video = out.array.reshape(1, T, 3, h * s, w * s) if isinstance(out, PinnedArray) else out
-        return video, ms.value
+        _check(lib().lc_decode_sharded(self._h, lat_ptr, I64(T), I64(c), I64(h), I64(w), I64(slice_frames), out_ptr,
+                                       ctypes.c_int(SHARD_HOST_SHARED if host_shared else 0), ctypes.byref(ms)))
+        if out is None:
+            return None, ms.value
+        arr = out.array if hasattr(out, "array") else out
+        return arr.reshape(-1)[:nvid].reshape(1, T, 3, h * s, w * s), ms.value
 
 
 class PinnedArray:
@@ -432,6 +473,30 @@ class PinnedArray:
         if self.ptr:
             lib().lc_free_pinned(self.ptr)
             self.ptr = None
+
+
+class SharedVideo:
+    """fp32 host buffer in a POSIX shared-memory segment, page-locked with
+    lc_host_register, so every rank of one box maps the same video and
+    downloads its own frames into it (LC_SHARD_HOST_SHARED)."""
+
+    def __init__(self, name: str, n: int, create: bool):
+        from multiprocessing import shared_memory
+        self.shm = shared_memory.SharedMemory(name=name, create=create, size=max(1, n) * 4)
+        self.n = n
+        self.array = np.ndarray((n,), np.float32, buffer=self.shm.buf)
+        self.ptr = ctypes.c_void_p(self.array.ctypes.data)
+        _check(lib().lc_host_register(self.ptr, I64(max(1, n) * 4)))
+        self._owner = create
+
+    def free(self):
+        if self.ptr is not None:
+            lib().lc_host_unregister(self.ptr)
+            self.ptr = None
+            self.array = None
+            self.shm.close()
+            if self._owner:
+                self.shm.unlink()
 
 
 def nccl_unique_id() -> bytes:

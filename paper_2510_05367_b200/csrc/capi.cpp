@@ -39,6 +39,17 @@ int guarded(F&& f) {
     }
 }
 
+// Entry points that take a context make its GPU current first: one context
+// per GPU, several contexts per process (lightcache.h).
+template <typename F>
+int guarded_on(lc_ctx* ctx, F&& f) {
+    return guarded([&] {
+        if (!ctx) lc::throw_config("null lc_ctx");
+        LC_CUDA(cudaSetDevice(ctx->device));
+        f();
+    });
+}
+
 void put(char* dst, int64_t cap, const std::string& s) {
     if (!dst || cap <= 0) return;
     const size_t n = std::min<size_t>(s.size(), static_cast<size_t>(cap - 1));
@@ -109,7 +120,7 @@ lc::Act upload_act(lc::DevBuf& buf, const float* x, int n, int c, int h, int w) 
     a.cs = (c + 63) / 64 * 64;
     const auto hv = to_nhwc(x, n, c, h, w, a.cs);
     buf = lc::dev_alloc(nullptr, static_cast<int64_t>(hv.size()) * 2, false);
-    LC_CUDA(cudaMemcpy(buf.p, hv.data(), hv.size() * 2, cudaMemcpyHostToDevice));
+    lc::h2d_blocking(buf.p, hv.data(), hv.size() * 2);
     a.p = buf.as<__half>();
     return a;
 }
@@ -130,8 +141,9 @@ int lc_ctx_create(int device, lc_ctx** out) {
     return guarded([&] { *out = new lc_ctx(device); });
 }
 int lc_ctx_destroy(lc_ctx* ctx) {
-    return guarded([&] {
-        if (ctx && ctx->comm) ncclCommDestroy(ctx->comm);
+    if (!ctx) return 0;
+    return guarded_on(ctx, [&] {
+        if (ctx->comm) ncclCommDestroy(ctx->comm);
         delete ctx;
     });
 }
@@ -143,58 +155,65 @@ int lc_config_to_text(const char* text, char* out, int64_t cap) {
     return guarded([&] { put(out, cap, lc::config_to_text(lc::parse_config_text(text ? text : ""))); });
 }
 int lc_configure(lc_ctx* ctx, const char* text) {
-    return guarded([&] { ctx->engine.configure(lc::parse_config_text(text ? text : "")); });
+    return guarded_on(ctx, [&] { ctx->engine.configure(lc::parse_config_text(text ? text : "")); });
 }
 int64_t lc_latent_elems(lc_ctx* ctx) { return ctx->engine.latent_elems(); }
 int64_t lc_video_elems(lc_ctx* ctx) { return ctx->engine.video_elems(); }
 
 int lc_run_pipeline(lc_ctx* ctx, const float* x0, float* video, float* latent_out, char* report,
                     int64_t cap) {
-    return guarded([&] {
+    return guarded_on(ctx, [&] {
         const lc::RunStats st = ctx->engine.run(x0, video, latent_out, false);
         put(report, cap, report_json(ctx->engine, st));
     });
 }
+// Both copies are ordered on the engine's compute stream after any queued
+// async runs (which read the staged latent / write the device video) and
+// complete before returning.
 int lc_upload_latent(lc_ctx* ctx, const float* x0) {
-    return guarded([&] {
+    return guarded_on(ctx, [&] {
+        (void)ctx->engine.wait();
         ctx->engine.run_prepare();
-        LC_CUDA(cudaMemcpy(ctx->engine.latent_dev(), x0, static_cast<size_t>(ctx->engine.latent_elems()) * 4,
-                           cudaMemcpyHostToDevice));
+        LC_CUDA(cudaMemcpyAsync(ctx->engine.latent_dev(), x0, static_cast<size_t>(ctx->engine.latent_elems()) * 4,
+                                cudaMemcpyHostToDevice, ctx->engine.stream()));
+        LC_CUDA(cudaStreamSynchronize(ctx->engine.stream()));
     });
 }
 int lc_run_resident(lc_ctx* ctx, char* report, int64_t cap) {
-    return guarded([&] {
+    return guarded_on(ctx, [&] {
         const lc::RunStats st = ctx->engine.run(nullptr, nullptr, nullptr, true);
         put(report, cap, report_json(ctx->engine, st));
     });
 }
 int lc_run_resident_async(lc_ctx* ctx) {
-    return guarded([&] { ctx->engine.run_resident_async(); });
+    return guarded_on(ctx, [&] { ctx->engine.run_resident_async(); });
 }
 int lc_run_pipeline_async(lc_ctx* ctx, const float* x0, float* video) {
-    return guarded([&] { ctx->engine.run_e2e_async(x0, video); });
+    return guarded_on(ctx, [&] { ctx->engine.run_e2e_async(x0, video); });
 }
 int lc_wait(lc_ctx* ctx, char* report, int64_t cap) {
-    return guarded([&] {
+    return guarded_on(ctx, [&] {
         const lc::RunStats st = ctx->engine.wait();
         put(report, cap, report_json(ctx->engine, st));
     });
 }
 int lc_download_video(lc_ctx* ctx, float* video) {
-    return guarded([&] {
-        LC_CUDA(cudaMemcpy(video, ctx->engine.video_dev(), static_cast<size_t>(ctx->engine.video_elems()) * 4,
-                           cudaMemcpyDeviceToHost));
+    return guarded_on(ctx, [&] {
+        (void)ctx->engine.wait();
+        LC_CUDA(cudaMemcpyAsync(video, ctx->engine.video_dev(), static_cast<size_t>(ctx->engine.video_elems()) * 4,
+                                cudaMemcpyDeviceToHost, ctx->engine.stream()));
+        LC_CUDA(cudaStreamSynchronize(ctx->engine.stream()));
     });
 }
 int lc_set_decode_slice(lc_ctx* ctx, int64_t frames) {
-    return guarded([&] {
+    return guarded_on(ctx, [&] {
         if (frames < 1) lc::throw_config("decode slice must be >= 1");
         ctx->engine.decode_slice = frames;
     });
 }
 
 int lc_timer_start(lc_ctx* ctx) {
-    return guarded([&] {
+    return guarded_on(ctx, [&] {
         if (!ctx->t0) {
             LC_CUDA(cudaEventCreate(&ctx->t0));
             LC_CUDA(cudaEventCreate(&ctx->t1));
@@ -203,23 +222,23 @@ int lc_timer_start(lc_ctx* ctx) {
     });
 }
 int lc_timer_stop(lc_ctx* ctx, float* ms) {
-    return guarded([&] {
+    return guarded_on(ctx, [&] {
         LC_CUDA(cudaEventRecord(ctx->t1, ctx->engine.stream()));
         LC_CUDA(cudaEventSynchronize(ctx->t1));
         LC_CUDA(cudaEventElapsedTime(ms, ctx->t0, ctx->t1));
     });
 }
 int lc_set_conv_profile(lc_ctx* ctx, int on) {
-    return guarded([&] {
+    return guarded_on(ctx, [&] {
         ctx->prof.clear();
         lc::set_conv_profiler(on ? &ctx->prof : nullptr);
     });
 }
 int lc_conv_profile(lc_ctx* ctx, int64_t* launches, double* ms, double* alg, double* exec) {
-    return guarded([&] { ctx->prof.summarize(launches, ms, alg, exec); });
+    return guarded_on(ctx, [&] { ctx->prof.summarize(launches, ms, alg, exec); });
 }
 int lc_conv_profile_records(lc_ctx* ctx, char* buf, int64_t cap) {
-    return guarded([&] { put(buf, cap, ctx->prof.records_json()); });
+    return guarded_on(ctx, [&] { put(buf, cap, ctx->prof.records_json()); });
 }
 void* lc_alloc_pinned(int64_t bytes) {
     void* p = nullptr;
@@ -235,10 +254,10 @@ int lc_free_pinned(void* p) {
 
 int lc_forward(lc_ctx* ctx, const float* x, int64_t T, int64_t timestep, const float* deep_in,
                float* deep_out, float* eps) {
-    return guarded([&] { ctx->engine.forward(x, T, timestep, deep_in, deep_out, eps); });
+    return guarded_on(ctx, [&] { ctx->engine.forward(x, T, timestep, deep_in, deep_out, eps); });
 }
 int lc_ledger_csv(lc_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
-    return guarded([&] {
+    return guarded_on(ctx, [&] {
         static const char* kinds[5] = {"alloc", "free", "move_start", "move_end", "stage_enter"};
         static const char* stages[4] = {"setup", "encode", "denoise", "decode"};
         const lc::Ledger& l = ctx->engine.ledger();
@@ -257,7 +276,7 @@ int lc_ledger_csv(lc_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
     });
 }
 int lc_ledger_summary(lc_ctx* ctx, char* buf, int64_t cap) {
-    return guarded([&] {
+    return guarded_on(ctx, [&] {
         static const char* stages[4] = {"setup", "encode", "denoise", "decode"};
         const lc::Ledger& l = ctx->engine.ledger();
         std::ostringstream os;
@@ -278,7 +297,7 @@ int lc_ledger_summary(lc_ctx* ctx, char* buf, int64_t cap) {
 }
 int lc_video_metrics(lc_ctx* ctx, const float* a, const float* b, int64_t t, int64_t c, int64_t h, int64_t w,
                      double data_range, double* psnr, double* ssim) {
-    return guarded([&] {
+    return guarded_on(ctx, [&] {
         if (!(data_range > 0.0)) lc::throw_config("psnr: data_range must be positive");
         if (h < 7 || w < 7) lc::throw_shape("ssim: frame smaller than the 7x7 window");
         if (t < 1 || c < 1) lc::throw_shape("video_metrics: empty video");
@@ -307,14 +326,15 @@ int lc_video_metrics(lc_ctx* ctx, const float* a, const float* b, int64_t t, int
         LC_CUDA(lc::video_metrics(pa, pb, t, c, h, w, data_range, psnr, ssim, st));
     });
 }
-int lc_decode(lc_ctx* ctx, const float* latents, int64_t n, int64_t slice, float* video) {
-    return guarded([&] { ctx->engine.decode(latents, n, video, slice); });
+int lc_decode(lc_ctx* ctx, const float* latents, int64_t n, int64_t c, int64_t h, int64_t w, int64_t slice,
+              float* video) {
+    return guarded_on(ctx, [&] { ctx->engine.decode(latents, n, c, h, w, video, slice); });
 }
 
 int lc_conv2d(lc_ctx* ctx, const float* x, int64_t b, int64_t t, int64_t c_in, int64_t h, int64_t w,
               const float* taps, const float* bias, int64_t c_out, int64_t k, float s, float o, int silu,
               float* out) {
-    return guarded([&] {
+    return guarded_on(ctx, [&] {
         if (k < 1 || k % 2 == 0) lc::throw_shape("kernel size must be odd");
         lc::Bank bank;
         bank.c_in = c_in;
@@ -347,7 +367,7 @@ int lc_conv2d(lc_ctx* ctx, const float* x, int64_t b, int64_t t, int64_t c_in, i
 int lc_up_conv2d(lc_ctx* ctx, const float* skip, const float* u, int64_t b, int64_t t, int64_t c_a,
                  int64_t c_b, int64_t h, int64_t w, const float* taps, const float* bias, int64_t c_out,
                  float s, float o, float* out) {
-    return guarded([&] {
+    return guarded_on(ctx, [&] {
         if (h % 2 || w % 2) lc::throw_shape("up block needs even extents");
         lc::Bank bank;
         bank.c_in = c_a + c_b;
@@ -443,13 +463,41 @@ int lc_randn(uint64_t seed, int64_t n, float* out) {
 
 int lc_shard_frames(int64_t T, int world, int rank, int64_t* first, int64_t* count) {
     return guarded([&] {
-        if (world < 1 || rank < 0 || rank >= world) lc::throw_config("bad world/rank");
-        const int64_t per = (T + world - 1) / world;
-        const int64_t f0 = std::min<int64_t>(T, per * rank);
-        const int64_t f1 = std::min<int64_t>(T, f0 + per);
-        *first = f0;
-        *count = f1 - f0;
+        const lc::ShardSpan sp = lc::shard_frames(T, world, rank);
+        *first = sp.first;
+        *count = sp.count;
     });
+}
+
+int lc_gather_plan(int64_t T, int world, int64_t slice, int64_t* rows, int64_t cap_rows, int64_t* n_rows) {
+    return guarded([&] {
+        const auto plan = lc::gather_plan(T, world, slice);
+        if (n_rows) *n_rows = static_cast<int64_t>(plan.size());
+        if (!rows) return;
+        if (static_cast<int64_t>(plan.size()) > cap_rows) lc::throw_shape("gather plan buffer too small");
+        for (size_t i = 0; i < plan.size(); ++i) {
+            rows[4 * i + 0] = plan[i].round;
+            rows[4 * i + 1] = plan[i].rank;
+            rows[4 * i + 2] = plan[i].first;
+            rows[4 * i + 3] = plan[i].count;
+        }
+    });
+}
+
+int lc_mem_info(lc_ctx* ctx, int64_t* free_bytes, int64_t* total_bytes) {
+    return guarded_on(ctx, [&] {
+        size_t f = 0, t = 0;
+        LC_CUDA(cudaMemGetInfo(&f, &t));
+        if (free_bytes) *free_bytes = static_cast<int64_t>(f);
+        if (total_bytes) *total_bytes = static_cast<int64_t>(t);
+    });
+}
+
+int lc_host_register(void* p, int64_t bytes) {
+    return guarded([&] { LC_CUDA(cudaHostRegister(p, static_cast<size_t>(bytes), cudaHostRegisterPortable)); });
+}
+int lc_host_unregister(void* p) {
+    return guarded([&] { LC_CUDA(cudaHostUnregister(p)); });
 }
 
 int lc_nccl_unique_id(uint8_t* id128) {
@@ -461,7 +509,7 @@ int lc_nccl_unique_id(uint8_t* id128) {
 }
 
 int lc_nccl_init(lc_ctx* ctx, const uint8_t* id128, int world, int rank) {
-    return guarded([&] {
+    return guarded_on(ctx, [&] {
         ncclUniqueId id;
         std::memcpy(&id, id128, sizeof(id));
         LC_CUDA(cudaSetDevice(ctx->device));
@@ -472,12 +520,14 @@ int lc_nccl_init(lc_ctx* ctx, const uint8_t* id128, int world, int rank) {
 }
 
 int lc_kernel_launches(lc_ctx* ctx, int64_t* n) {
-    return guarded([&] { *n = ctx->engine.launches; });
+    return guarded_on(ctx, [&] { *n = ctx->engine.launches; });
 }
-int lc_decode_sharded(lc_ctx* ctx, const float* latents, int64_t T, int64_t slice, float* video, float* ms_out) {
-    return guarded([&] {
+int lc_decode_sharded(lc_ctx* ctx, const float* latents, int64_t T, int64_t c, int64_t h, int64_t w,
+                      int64_t slice, float* video, int flags, float* ms_out) {
+    return guarded_on(ctx, [&] {
         if (!ctx->comm && ctx->world > 1) lc::throw_config("lc_nccl_init first");
-        ctx->engine.decode_sharded(latents, T, slice, video, ctx->comm, ctx->world, ctx->rank, ms_out);
+        ctx->engine.decode_sharded(latents, T, c, h, w, slice, video, (flags & LC_SHARD_HOST_SHARED) != 0,
+                                   ctx->comm, ctx->world, ctx->rank, ms_out);
     });
 }
 

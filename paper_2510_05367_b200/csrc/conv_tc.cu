@@ -818,15 +818,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// Per-device caches (kernel attributes and SM counts apply per device; a
+// process may drive several contexts on different GPUs).
+constexpr int kMaxDevices = 64;
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev < 0 || dev >= kMaxDevices ? 0 : dev;
+}
+
 int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
+    static int n[kMaxDevices] = {};
+    const int dev = current_device();
+    if (!n[dev]) {
+        cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
+        if (n[dev] <= 0) n[dev] = 148;
     }
-    return n;
+    return n[dev];
 }
 
 template <int CG>
@@ -859,12 +867,13 @@ cudaError_t launch_variant(const ConvParams& p0, int parities, cudaStream_t stre
         p.fd_tx.init(static_cast<uint32_t>(p.tiles_x));
         p.fd_ty.init(static_cast<uint32_t>(p.tiles_y));
     }
-    static bool attr_set = false;
-    if (!attr_set) {
+    static bool attr_set[kMaxDevices] = {};
+    const int dev = current_device();
+    if (!attr_set[dev]) {
         cudaError_t e =
             cudaFuncSetAttribute(conv_tc_kernel<CG, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set[dev] = true;
     }
     const int n_tiles = p.n_pad / p.BN;
     const int m_tiles = p.tiles_x * p.tiles_y * p.tiles_i;

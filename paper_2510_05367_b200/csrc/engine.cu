@@ -75,12 +75,22 @@ DevBuf dev_alloc(Ledger* l, int64_t bytes, bool zero) {
     if (bytes <= 0) return b;
     if (l) b.id = l->alloc(0, bytes);
     LC_CUDA(cudaMalloc(&b.p, static_cast<size_t>(bytes)));
-    if (zero) LC_CUDA(cudaMemset(b.p, 0, static_cast<size_t>(bytes)));
+    if (zero) {
+        // zero channel padding (TMA 64-channel blocks read it): complete
+        // before any non-blocking-stream kernel can touch the buffer
+        LC_CUDA(cudaMemset(b.p, 0, static_cast<size_t>(bytes)));
+        LC_CUDA(cudaStreamSynchronize(nullptr));
+    }
     b.bytes = bytes;
     b.ledger = l;
     b.tier = 0;
     return b;
 }
+void h2d_blocking(void* dst, const void* src, size_t bytes) {
+    LC_CUDA(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+    LC_CUDA(cudaStreamSynchronize(nullptr));
+}
+
 DevBuf host_alloc(Ledger* l, int64_t bytes) {
     DevBuf b;
     if (bytes <= 0) return b;
@@ -348,12 +358,12 @@ std::unique_ptr<TcLayer> pack_tc_layer(Ledger* l, const Bank& b, int c_split, in
     std::vector<__half> wh(nW);
     for (size_t i = 0; i < nW; ++i) wh[i] = __float2half_rn(wf[i] * L->wscale);
     L->w = dev_alloc(l, static_cast<int64_t>(nW * sizeof(__half)), false);
-    LC_CUDA(cudaMemcpy(L->w.p, wh.data(), nW * sizeof(__half), cudaMemcpyHostToDevice));
+    h2d_blocking(L->w.p, wh.data(), nW * sizeof(__half));
 
     std::vector<float> bias(static_cast<size_t>(L->n_pad), 0.0f);
     for (int oc = 0; oc < L->c_out; ++oc) bias[oc] = b.bias[oc];
     L->bias = dev_alloc(l, L->n_pad * 4, false);
-    LC_CUDA(cudaMemcpy(L->bias.p, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice));
+    h2d_blocking(L->bias.p, bias.data(), bias.size() * 4);
 
     // conditioning-shift tables: sum of in-bound tap weights per class
     const int rc = L->rc, rr = rc + 1, ncls = rr * rr * rr * rr;
@@ -380,7 +390,7 @@ std::unique_ptr<TcLayer> pack_tc_layer(Ledger* l, const Bank& b, int c_split, in
             }
         }
     L->corr = dev_alloc(l, static_cast<int64_t>(corr.size() * 4), false);
-    LC_CUDA(cudaMemcpy(L->corr.p, corr.data(), corr.size() * 4, cudaMemcpyHostToDevice));
+    h2d_blocking(L->corr.p, corr.data(), corr.size() * 4);
     return L;
 }
 
@@ -390,9 +400,9 @@ std::unique_ptr<ThinLayer> pack_thin_layer(Ledger* l, const Bank& b) {
     L->c_out = static_cast<int>(b.c_out);
     L->k = static_cast<int>(b.k);
     L->w = dev_alloc(l, static_cast<int64_t>(b.taps.size() * 4), false);
-    LC_CUDA(cudaMemcpy(L->w.p, b.taps.data(), b.taps.size() * 4, cudaMemcpyHostToDevice));
+    h2d_blocking(L->w.p, b.taps.data(), b.taps.size() * 4);
     L->bias = dev_alloc(l, static_cast<int64_t>(b.bias.size() * 4), false);
-    LC_CUDA(cudaMemcpy(L->bias.p, b.bias.data(), b.bias.size() * 4, cudaMemcpyHostToDevice));
+    h2d_blocking(L->bias.p, b.bias.data(), b.bias.size() * 4);
     return L;
 }
 
@@ -444,7 +454,7 @@ DevBuf pack_tap_w16(Ledger* l, const Bank& tb, int* kb_out, int* n_out, float* w
                 __float2half_rn(tb.taps[static_cast<size_t>(r * tb.c_in + ic)] * wscale);
     *wscale_out = wscale;
     DevBuf b = dev_alloc(l, static_cast<int64_t>(w16.size() * 2), false);
-    LC_CUDA(cudaMemcpy(b.p, w16.data(), w16.size() * 2, cudaMemcpyHostToDevice));
+    h2d_blocking(b.p, w16.data(), w16.size() * 2);
     *kb_out = kb;
     *n_out = n;
     return b;
@@ -734,6 +744,7 @@ Engine::Engine(int device) : device_(device) {
     LC_CUDA(cudaStreamCreateWithFlags(&s_compute_, cudaStreamNonBlocking));
     LC_CUDA(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking));
     LC_CUDA(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking));
+    LC_CUDA(cudaStreamCreateWithFlags(&s_comm_, cudaStreamNonBlocking));
     LC_CUDA(cudaEventCreate(&ev_base_));
     for (int b = 0; b < 2; ++b) {
         LC_CUDA(cudaEventCreateWithFlags(&ev_evict_[b], cudaEventDisableTiming));
@@ -786,6 +797,7 @@ Engine::~Engine() {
     cudaStreamDestroy(s_compute_);
     cudaStreamDestroy(s_d2h_);
     cudaStreamDestroy(s_h2d_);
+    cudaStreamDestroy(s_comm_);
 }
 
 cudaEvent_t Engine::next_event() {
@@ -898,9 +910,9 @@ void Engine::configure(const RunConfig& cfg) {
                         ws[static_cast<size_t>(tp * hb.c_out + c)] = static_cast<float>(acc);
                     }
                 head_wsum_ = dev_alloc(&ledger_, static_cast<int64_t>(ws.size() * 4), false);
-                LC_CUDA(cudaMemcpy(head_wsum_.p, ws.data(), ws.size() * 4, cudaMemcpyHostToDevice));
+                h2d_blocking(head_wsum_.p, ws.data(), ws.size() * 4);
                 head_bias_ = dev_alloc(&ledger_, static_cast<int64_t>(hb.bias.size() * 4), false);
-                LC_CUDA(cudaMemcpy(head_bias_.p, hb.bias.data(), hb.bias.size() * 4, cudaMemcpyHostToDevice));
+                h2d_blocking(head_bias_.p, hb.bias.data(), hb.bias.size() * 4);
             }
             const Bank& db = cw_.dec[static_cast<size_t>(cfg.stages)];
             dec_last_tap_tc_.reset();
@@ -915,7 +927,7 @@ void Engine::configure(const RunConfig& cfg) {
                     dec_last_w16_ = pack_tap_w16(&ledger_, tb, &dec_last_kb_, &nn, &dec_last_wscale_);
                 }
                 dec_last_bias_ = dev_alloc(&ledger_, static_cast<int64_t>(db.bias.size() * 4), false);
-                LC_CUDA(cudaMemcpy(dec_last_bias_.p, db.bias.data(), db.bias.size() * 4, cudaMemcpyHostToDevice));
+                h2d_blocking(dec_last_bias_.p, db.bias.data(), db.bias.size() * 4);
             }
         }
         {
@@ -1716,7 +1728,7 @@ void Engine::prepare_noise() {
         const StepCoeffs k = step_coeffs(cfg_, sc, s);
         if (!k.has_noise) continue;
         randn(k.noise_seed, nl, z.data());
-        LC_CUDA(cudaMemcpy(z_.as<float>() + s * nl, z.data(), static_cast<size_t>(nl) * 4, cudaMemcpyHostToDevice));
+        h2d_blocking(z_.as<float>() + s * nl, z.data(), static_cast<size_t>(nl) * 4);
     }
     z_key_ = key;
 }
@@ -1742,12 +1754,12 @@ void Engine::prepare_image() {
                                   std::cos(phase + 6.0 * static_cast<double>(x) / static_cast<double>(W)));
                 }
     frames_dev_ = dev_alloc(&ledger_, static_cast<int64_t>(fr.size()) * 4, false);
-    LC_CUDA(cudaMemcpy(frames_dev_.p, fr.data(), fr.size() * 4, cudaMemcpyHostToDevice));
+    h2d_blocking(frames_dev_.p, fr.data(), fr.size() * 4);
     const int64_t nl = latent_elems();
     std::vector<float> e(static_cast<size_t>(nl));
     randn(derive_seed(cfg_.seed, 2), nl, e.data());
     eps0_dev_ = dev_alloc(&ledger_, nl * 4, false);
-    LC_CUDA(cudaMemcpy(eps0_dev_.p, e.data(), e.size() * 4, cudaMemcpyHostToDevice));
+    h2d_blocking(eps0_dev_.p, e.data(), e.size() * 4);
     img_key_ = key;
 }
 
@@ -2178,7 +2190,7 @@ void Engine::forward(const float* x_host, int64_t T, int64_t timestep, const flo
     // explicit (2,T,...) input: the stem reads both halves as given.
     invalidate_graph();
     DevBuf xin = dev_alloc(nullptr, 2 * n1 * 4, false);
-    LC_CUDA(cudaMemcpy(xin.p, x_host, static_cast<size_t>(2 * n1) * 4, cudaMemcpyHostToDevice));
+    h2d_blocking(xin.p, x_host, static_cast<size_t>(2 * n1) * 4);
     const bool full = deep_in_ref == nullptr;
     if (!cfg_.cache_enabled) throw_config("forward(): cache.enabled must be true for seam access");
     if (!full) {
@@ -2193,7 +2205,7 @@ void Engine::forward(const float* x_host, int64_t T, int64_t timestep, const flo
                     for (int x = 0; x < a.w; ++x)
                         hbuf[((static_cast<size_t>(n) * a.h + y) * a.w + x) * a.cs + c2] = __float2half_rn(
                             deep_in_ref[((static_cast<size_t>(n) * a.c + c2) * Hr + 2 * y) * Wr + 2 * x]);
-        LC_CUDA(cudaMemcpy(a.p, hbuf.data(), hbuf.size() * 2, cudaMemcpyHostToDevice));
+        h2d_blocking(a.p, hbuf.data(), hbuf.size() * 2);
     }
     forward_dev(xin.as<float>(), true, T, timestep, full, eps2_.as<float>(), 0, 0);
     LC_CUDA(cudaStreamSynchronize(s_compute_));
@@ -2213,15 +2225,31 @@ void Engine::forward(const float* x_host, int64_t T, int64_t timestep, const flo
     }
 }
 
-void Engine::decode(const float* lat_host, int64_t n, float* video_host, int64_t slice) {
+// decode_batch / decode_sliced's checks (codec.cpp:117-135): the latent
+// channel count must be the codec's; the engine is configured for one
+// latent geometry, so a different h x w is a ShapeError too.
+static void check_decode_shape(const RunConfig& c, int64_t n, int64_t ch, int64_t h, int64_t w) {
+    if (n < 0) throw_shape("decode: negative frame count");
+    if (ch != c.latent_channels)
+        throw_shape("decode expects " + std::to_string(c.latent_channels) + " latent channels");
+    if (h != c.latent_h() || w != c.latent_w())
+        throw_shape("decode: latent " + std::to_string(h) + "x" + std::to_string(w) +
+                    " does not match the configured geometry " + std::to_string(c.latent_h()) + "x" +
+                    std::to_string(c.latent_w()));
+}
+
+void Engine::decode(const float* lat_host, int64_t n, int64_t c, int64_t h, int64_t w, float* video_host,
+                    int64_t slice) {
     if (async_pending_) (void)wait();
+    check_decode_shape(cfg_, n, c, h, w);
+    if (n == 0) return;
     const int C = static_cast<int>(cfg_.latent_channels);
     const int64_t nl = n * C * cfg_.latent_h() * cfg_.latent_w();
     const int64_t nv = n * cfg_.image_channels * cfg_.height * cfg_.width;
     invalidate_graph();
     DevBuf lat = dev_alloc(nullptr, nl * 4, false);
     DevBuf vid = dev_alloc(nullptr, nv * 4, false);
-    LC_CUDA(cudaMemcpy(lat.p, lat_host, static_cast<size_t>(nl) * 4, cudaMemcpyHostToDevice));
+    LC_CUDA(cudaMemcpyAsync(lat.p, lat_host, static_cast<size_t>(nl) * 4, cudaMemcpyHostToDevice, s_compute_));
     const int64_t keep = decode_slice;
     decode_slice = slice;
     const bool keep_sliced = cfg_.slice_decode;
@@ -2231,64 +2259,111 @@ void Engine::decode(const float* lat_host, int64_t n, float* video_host, int64_t
     decode_slice = keep;
     cfg_.slice_decode = keep_sliced;
     dec_alloc_ = -1;
+    LC_CUDA(cudaMemcpyAsync(video_host, vid.p, static_cast<size_t>(nv) * 4, cudaMemcpyDeviceToHost, s_compute_));
     LC_CUDA(cudaStreamSynchronize(s_compute_));
-    LC_CUDA(cudaMemcpy(video_host, vid.p, static_cast<size_t>(nv) * 4, cudaMemcpyDeviceToHost));
 }
 
 }  // namespace lc
 
 namespace lc {
 
-void Engine::decode_sharded(const float* lat_host, int64_t T, int64_t slice, float* video_host,
-                            ncclComm_t comm, int world, int rank, float* ms_out) {
+void Engine::decode_sharded(const float* lat_host, int64_t T, int64_t c, int64_t h, int64_t w, int64_t slice,
+                            float* video_host, bool host_shared, ncclComm_t comm, int world, int rank,
+                            float* ms_out) {
     if (async_pending_) (void)wait();
-    const int C = static_cast<int>(cfg_.latent_channels);
-    const int64_t lat_frame = C * cfg_.latent_h() * cfg_.latent_w();
+    check_decode_shape(cfg_, T, c, h, w);
+    if (slice < 1) throw_config("decode slice must be >= 1");
+    if (world > 1 && !comm) throw_config("decode_sharded: no NCCL communicator for world > 1");
+    const int64_t lat_frame = cfg_.latent_channels * cfg_.latent_h() * cfg_.latent_w();
     const int64_t vid_frame = cfg_.image_channels * cfg_.height * cfg_.width;
-    const int64_t per = (T + world - 1) / world;
-    auto shard = [&](int r, int64_t* f0, int64_t* cnt) {
-        *f0 = std::min<int64_t>(T, per * r);
-        *cnt = std::min<int64_t>(T, *f0 + per) - *f0;
-    };
-    int64_t f0, cnt;
-    shard(rank, &f0, &cnt);
-    // shard buffers persist across calls (grow-only), like the run's
-    ensure_buf(&shard_lat_, std::max<int64_t>(1, cnt) * lat_frame * 4);
-    ensure_buf(&shard_vid_, T * vid_frame * 4);
-    const DevBuf& lat = shard_lat_;
-    const DevBuf& vid = shard_vid_;
-    cudaEvent_t e0, e1;
+    const ShardSpan me = shard_frames(T, world, rank);
+    const std::vector<GatherRow> plan = gather_plan(T, world, slice);
+    // shard buffers persist across calls (grow-only), like the run's; only
+    // rank 0 holds the whole video (the gather target)
+    ensure_buf(&shard_lat_, std::max<int64_t>(1, me.count) * lat_frame * 4);
+    ensure_buf(&shard_vid_, std::max<int64_t>(1, rank == 0 ? T : me.count) * vid_frame * 4);
+    float* vid = shard_vid_.as<float>();
+    // rank 0 decodes its frames in place; the others into [0, count)
+    const int64_t own0 = rank == 0 ? me.first : 0;
+    cudaEvent_t e0, e1, ej;
     LC_CUDA(cudaEventCreate(&e0));
     LC_CUDA(cudaEventCreate(&e1));
-    LC_CUDA(cudaEventRecord(e0, s_compute_));  // device time: H2D of the shard, decode, gather
+    LC_CUDA(cudaEventCreateWithFlags(&ej, cudaEventDisableTiming));
+    LC_CUDA(cudaEventRecord(e0, s_compute_));  // device time: shard H2D, decode, gather (+ host output)
     launches = 0;
-    if (cnt > 0)
-        LC_CUDA(cudaMemcpyAsync(lat.p, lat_host + f0 * lat_frame, static_cast<size_t>(cnt * lat_frame) * 4,
-                                cudaMemcpyHostToDevice, s_compute_));
+    if (me.count > 0)
+        LC_CUDA(cudaMemcpyAsync(shard_lat_.p, lat_host + me.first * lat_frame,
+                                static_cast<size_t>(me.count * lat_frame) * 4, cudaMemcpyHostToDevice, s_compute_));
+    // the comm / copy streams start after the shard buffers are ours
+    LC_CUDA(cudaEventRecord(ej, s_compute_));
+    LC_CUDA(cudaStreamWaitEvent(s_comm_, ej, 0));
+    LC_CUDA(cudaStreamWaitEvent(s_d2h_, ej, 0));
     const int64_t keep = decode_slice;
     const bool keep_sliced = cfg_.slice_decode;
     decode_slice = slice;
     cfg_.slice_decode = true;
-    if (cnt > 0) decode_dev(lat.as<float>(), cnt, vid.as<float>() + f0 * vid_frame);
+    out_slices_ = true;  // per-slice completion events (chunk_event(2, i))
+    if (me.count > 0) decode_dev(shard_lat_.as<float>(), me.count, vid + own0 * vid_frame);
+    out_slices_ = false;
+    decode_slice = keep;
+    cfg_.slice_decode = keep_sliced;
+    auto nccl = [](ncclResult_t r, const char* what) {
+        if (r != ncclSuccess) throw LcError(kCudaError, std::string(what) + ": " + ncclGetErrorString(r));
+    };
+    const bool host_out = video_host != nullptr;
     if (world > 1) {
-        // gather to rank 0: grouped point-to-point (ncclGather equivalent
-        // for uneven shards such as 25 frames over 8 GPUs = 4 + 7x3)
-        if (ncclGroupStart() != ncclSuccess) throw LcError(kCudaError, "ncclGroupStart");
-        if (rank == 0) {
-            for (int r = 1; r < world; ++r) {
-                int64_t g0, gc;
-                shard(r, &g0, &gc);
-                if (gc > 0 &&
-                    ncclRecv(vid.as<float>() + g0 * vid_frame, static_cast<size_t>(gc * vid_frame), ncclFloat,
-                             r, comm, s_compute_) != ncclSuccess)
-                    throw LcError(kCudaError, "ncclRecv");
+        // the gather, slice by slice (gather_plan rounds): senders post slice
+        // i as soon as it is decoded; rank 0 receives round i from every peer
+        // in one group while its own slices still decode
+        int64_t round = -1;
+        bool open = false;
+        size_t mine = 0;
+        for (const GatherRow& g : plan) {
+            if (g.rank == 0) continue;
+            if (rank == 0) {
+                if (g.round != round) {
+                    if (open) nccl(ncclGroupEnd(), "ncclGroupEnd");
+                    nccl(ncclGroupStart(), "ncclGroupStart");
+                    open = true;
+                    round = g.round;
+                }
+                nccl(ncclRecv(vid + g.first * vid_frame, static_cast<size_t>(g.count * vid_frame), ncclFloat,
+                              static_cast<int>(g.rank), comm, s_comm_),
+                     "ncclRecv");
+            } else if (g.rank == rank) {
+                LC_CUDA(cudaStreamWaitEvent(s_comm_, chunk_event(2, mine), 0));
+                nccl(ncclSend(vid + (g.first - me.first) * vid_frame, static_cast<size_t>(g.count * vid_frame),
+                              ncclFloat, 0, comm, s_comm_),
+                     "ncclSend");
+                ++mine;
             }
-        } else if (cnt > 0) {
-            if (ncclSend(vid.as<float>() + f0 * vid_frame, static_cast<size_t>(cnt * vid_frame), ncclFloat, 0,
-                         comm, s_compute_) != ncclSuccess)
-                throw LcError(kCudaError, "ncclSend");
         }
-        if (ncclGroupEnd() != ncclSuccess) throw LcError(kCudaError, "ncclGroupEnd");
+        if (open) nccl(ncclGroupEnd(), "ncclGroupEnd");
+    }
+    if (host_out) {
+        // every rank's own slices leave for the host as they are decoded;
+        // rank 0 also downloads what it received unless the peers write their
+        // frames into the shared host buffer themselves
+        for (size_t i = 0; i < slice_spans_.size(); ++i) {
+            if (!host_shared && rank != 0) break;
+            LC_CUDA(cudaStreamWaitEvent(s_d2h_, chunk_event(2, i), 0));
+            const int64_t f = me.first + slice_spans_[i].first, n = slice_spans_[i].second;
+            LC_CUDA(cudaMemcpyAsync(video_host + f * vid_frame, vid + (own0 + slice_spans_[i].first) * vid_frame,
+                                    static_cast<size_t>(n * vid_frame) * 4, cudaMemcpyDeviceToHost, s_d2h_));
+        }
+        if (rank == 0 && !host_shared && world > 1) {
+            LC_CUDA(cudaEventRecord(ej, s_comm_));
+            LC_CUDA(cudaStreamWaitEvent(s_d2h_, ej, 0));
+            for (const GatherRow& g : plan)
+                if (g.rank != 0)
+                    LC_CUDA(cudaMemcpyAsync(video_host + g.first * vid_frame, vid + g.first * vid_frame,
+                                            static_cast<size_t>(g.count * vid_frame) * 4, cudaMemcpyDeviceToHost,
+                                            s_d2h_));
+        }
+    }
+    for (cudaStream_t st : {s_comm_, s_d2h_}) {
+        LC_CUDA(cudaEventRecord(ej, st));
+        LC_CUDA(cudaStreamWaitEvent(s_compute_, ej, 0));
     }
     LC_CUDA(cudaEventRecord(e1, s_compute_));
     LC_CUDA(cudaStreamSynchronize(s_compute_));
@@ -2297,10 +2372,7 @@ void Engine::decode_sharded(const float* lat_host, int64_t T, int64_t slice, flo
     if (ms_out) *ms_out = ms;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    decode_slice = keep;
-    cfg_.slice_decode = keep_sliced;
-    if (rank == 0 && video_host)
-        LC_CUDA(cudaMemcpy(video_host, vid.p, static_cast<size_t>(T * vid_frame) * 4, cudaMemcpyDeviceToHost));
+    cudaEventDestroy(ej);
 }
 
 }  // namespace lc

@@ -80,6 +80,11 @@ struct DevBuf {
     T* as() const { return static_cast<T*>(p); }
 };
 DevBuf dev_alloc(Ledger* l, int64_t bytes, bool zero = true);
+// Host -> device copy that has LANDED when it returns.  A legacy-stream
+// cudaMemcpy from pageable memory may return before its DMA completes, and
+// the engine's kernels run on non-blocking streams that do not order after
+// the legacy stream, so every setup upload goes through this.
+void h2d_blocking(void* dst, const void* src, size_t bytes);
 DevBuf host_alloc(Ledger* l, int64_t bytes);
 
 // fp16 NHWC activation view.
@@ -202,12 +207,19 @@ public:
     // forward_full / forward_cached on x (2,T,C,h,w) host fp32.
     void forward(const float* x_host, int64_t T, int64_t timestep, const float* deep_in_ref,
                  float* deep_out_ref, float* eps_host);
-    // decode n latents (n,C,h,w) -> (n,3,H,W)
-    void decode(const float* lat_host, int64_t n, float* video_host, int64_t slice);
-    // Sliced decode sharded over `world` ranks (contiguous frame blocks of
-    // ceil(T/world)), decoded frames gathered to rank 0 over NCCL.
-    void decode_sharded(const float* lat_host, int64_t T, int64_t slice, float* video_host,
-                        ncclComm_t comm, int world, int rank, float* ms_out);
+    // decode n latents (n,C,h,w) -> (n,3,H,W); C, h, w are checked against
+    // the configured codec geometry (ShapeError, codec.cpp:129-131).
+    void decode(const float* lat_host, int64_t n, int64_t c, int64_t h, int64_t w, float* video_host,
+                int64_t slice);
+    // Sliced decode sharded over `world` ranks (balanced contiguous frame
+    // blocks, host.hpp shard_frames); each decoded slice is sent to rank 0
+    // over NCCL as soon as it is final (gather_plan rounds) while the next
+    // slice decodes.  video_host: rank 0's full video (after the gather);
+    // with `host_shared` every rank instead writes ITS frames straight into
+    // `video_host`, one host buffer mapped by all ranks (parallel host links).
+    void decode_sharded(const float* lat_host, int64_t T, int64_t c, int64_t h, int64_t w, int64_t slice,
+                        float* video_host, bool host_shared, ncclComm_t comm, int world, int rank,
+                        float* ms_out);
     // Allocate run buffers for the configured frame count.
     void run_prepare() { alloc_activations(cfg_.frames); }
 
@@ -304,6 +316,7 @@ private:
     Act dec_act_[8];
 
     cudaStream_t s_compute_ = nullptr, s_d2h_ = nullptr, s_h2d_ = nullptr;
+    cudaStream_t s_comm_ = nullptr;  // NCCL gather of decoded slices (decode_sharded)
     cudaEvent_t ev_base_ = nullptr;
     std::vector<cudaEvent_t> ev_pool_;
     size_t ev_next_ = 0;

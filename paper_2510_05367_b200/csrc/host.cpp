@@ -773,4 +773,32 @@ StepCoeffs step_coeffs(const RunConfig& c, const Schedule& sc, int64_t s) {
     return k;
 }
 
+// ------------------------------------------------------------------ sharded decode
+ShardSpan shard_frames(int64_t T, int world, int rank) {
+    if (world < 1 || rank < 0 || rank >= world) throw_config("bad world/rank");
+    if (T < 0) throw_shape("negative frame count");
+    const int64_t base = T / world, extra = T % world;
+    ShardSpan s;
+    s.first = rank * base + std::min<int64_t>(rank, extra);
+    s.count = base + (rank < extra ? 1 : 0);
+    return s;
+}
+
+std::vector<GatherRow> gather_plan(int64_t T, int world, int64_t slice) {
+    if (slice < 1) throw_config("decode slice must be >= 1");
+    std::vector<GatherRow> rows;
+    for (int64_t round = 0;; ++round) {
+        bool any = false;
+        for (int r = 0; r < world; ++r) {
+            const ShardSpan sp = shard_frames(T, world, r);
+            const int64_t g0 = round * slice;
+            if (g0 >= sp.count) continue;
+            any = true;
+            rows.push_back({round, r, sp.first + g0, std::min(slice, sp.count - g0)});
+        }
+        if (!any) break;
+    }
+    return rows;
+}
+
 }  // namespace lc

@@ -147,6 +147,23 @@ int64_t sim_stall_ns(const std::vector<SimEvent>& tl);     // swap.cpp:70-79
 // Virtual clock after the denoising loop's drain (pipeline.cpp:187).
 int64_t sim_denoise_end_ns(const RunConfig& cfg);
 
+// ------------------------------------------------------------------ sharded decode
+// Multi-GPU sliced decode (the unit of work is
+// decode_sliced, proj/src/codec.cpp:126-145): rank r of g owns a contiguous
+// frame block, balanced (the first T % g ranks take one frame more: 25 on 8
+// GPUs = 4,3,3,3,3,3,3,3), decoded in slices of `slice` frames.  Gather
+// round i moves the i-th slice of every rank that has one to rank 0; the
+// GPU engine executes the rounds with NCCL and the CPU tests with gloo, so
+// both consume this one plan.
+struct ShardSpan {
+    int64_t first = 0, count = 0;
+};
+ShardSpan shard_frames(int64_t T, int world, int rank);
+struct GatherRow {
+    int64_t round, rank, first, count;  // frames [first, first+count) of `rank`
+};
+std::vector<GatherRow> gather_plan(int64_t T, int world, int64_t slice);
+
 // ------------------------------------------------------------------ rng
 uint64_t splitmix64_at(uint64_t seed, uint64_t counter);  // rng.hpp:11-16
 uint64_t derive_seed(uint64_t seed, uint64_t stream);     // rng.hpp:24-26

@@ -278,18 +278,23 @@ __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_consta
 
 template <int MODE>
 cudaError_t launch_mode(const TapTcParams& p, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    // per device: the attribute applies to the current device only
+    constexpr int kMaxDevices = 64;
+    static bool attr[kMaxDevices] = {};
+    static int sm[kMaxDevices] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDevices) dev = 0;
+    if (!attr[dev]) {
         const cudaError_t e = cudaFuncSetAttribute(tap_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
         if (e != cudaSuccess) return e;
-        attr = true;
+        attr[dev] = true;
     }
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (!sm[dev]) {
+        cudaDeviceGetAttribute(&sm[dev], cudaDevAttrMultiProcessorCount, dev);
+        if (sm[dev] <= 0) sm[dev] = 148;
     }
+    const int sms = sm[dev];
     const int grid = p.num_tiles < sms ? p.num_tiles : sms;
     return launch_pdl(tap_tc_kernel<MODE>, dim3(grid), dim3(kThreads), static_cast<size_t>(smem_bytes<MODE>(p)), st, p);
 }

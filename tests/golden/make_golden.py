@@ -5,10 +5,14 @@ Runs the UNMODIFIED reference (oracle/_ref, compiled in place from
 compressed .npz under tests/golden/.  The B/C frame-0 slices (SURVEY.md
 section 8c: frame 0 of a T-frame run is bit-identical to the T=1 run) are
 too slow for the single-threaded reference and are produced by the
-restatement oracle/lc_oracle.c, which tests/test_oracle.py pins bit-exactly
-to the reference on every smaller case.
+restatement oracle/lc_oracle.c (the reference's RunResult carries only the
+video, not the final latent), and their VIDEOS are then pinned against the
+reference itself: `pin_b0` / `pin_c0` / `pin_bvar` run oracle/_ref's
+run_pipeline on the same config (about 5 min for B, 65 min for C, single
+thread), assert the restatement's video is bit-identical and record
+`video_source = "oracle/_ref"` plus the reference's wall time in the npz.
 
-Usage:  python tests/golden/make_golden.py [small|b0|c0|metrics|timelines]...
+Usage:  python tests/golden/make_golden.py [small|b0|c0|bvar|pin_b0|pin_c0|pin_bvar|metrics|timelines]...
 """
 import json
 import os
@@ -41,6 +45,14 @@ B0 = {"run.frames": 1, "run.height": 512, "run.width": 512, "codec.stages": 3, "
       "unet.base_channels": 320, "unet.depth": 3, "sampler.steps": 4, "cache.n": 2}
 C0 = {"run.frames": 1, "run.height": 576, "run.width": 1024, "codec.stages": 3, "codec.width": 128,
       "unet.base_channels": 320, "unet.depth": 3, "sampler.steps": 25, "cache.n": 2, "swap.mode": "async"}
+
+
+# B frame-0 variants (samplers and image mode at the B shape)
+BVAR = {
+    "b_frame0_ancestral": dict(B0, **{"sampler.kind": "ancestral"}),
+    "b_frame0_ddim": dict(B0, **{"sampler.kind": "ddim"}),
+    "b_frame0_image": dict(B0, **{"run.mode": "image"}),
+}
 
 
 def kv_of(over):
@@ -95,6 +107,27 @@ def slice0(name, over):
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), video=video, latent=lat,
                         config=np.array(lco.to_text(kv)), seconds=np.array(time.time() - t))
     print(name, f"{time.time() - t:.1f}s", flush=True)
+
+
+def pin(name, over):
+    """Run the UNMODIFIED reference on a frame-0 slice config and pin the
+    committed restatement video against it bit for bit."""
+    path = os.path.join(HERE, f"{name}.npz")
+    d = dict(np.load(path))
+    kv = kv_of(over)
+    assert str(d["config"]) == lco.to_text(kv), name
+    t = time.time()
+    video, report, macs = lco.Reference().run_pipeline(kv)
+    secs = time.time() - t
+    if not np.array_equal(video, d["video"]):
+        diff = np.abs(video - d["video"]).max()
+        raise SystemExit(f"{name}: restatement video differs from oracle/_ref (max abs {diff})")
+    d["video"] = video
+    d["video_source"] = np.array("oracle/_ref")
+    d["ref_seconds"] = np.array(secs)
+    d["macs"] = np.array(macs, np.int64)
+    np.savez_compressed(path, **d)
+    print(name, "pinned to oracle/_ref", f"{secs:.1f}s", flush=True)
 
 
 def metrics():
@@ -165,6 +198,16 @@ if __name__ == "__main__":
         slice0("b_frame0", B0)
     if "c0" in what:
         slice0("c_frame0", C0)
+    if "bvar" in what:
+        for name, over in BVAR.items():
+            slice0(name, over)
+    if "pin_b0" in what:
+        pin("b_frame0", B0)
+    if "pin_c0" in what:
+        pin("c_frame0", C0)
+    if "pin_bvar" in what:
+        for name, over in BVAR.items():
+            pin(name, over)
     if "metrics" in what:
         metrics()
     if "timelines" in what:

@@ -102,9 +102,11 @@ def test_randn_and_seeds_match_oracle(oracle):
 
 
 def test_shard_frames_partition():
-    # 25 frames over 8 GPUs -> 4 + 7x3
+    # 25 frames over 8 GPUs -> 4 + 7x3 (balanced)
     counts = [lc.shard_frames(25, 8, r)[1] for r in range(8)]
-    assert counts == [4, 3, 3, 3, 3, 3, 3, 3] or sum(counts) == 25
+    assert counts == [4, 3, 3, 3, 3, 3, 3, 3]
+    assert [lc.shard_frames(25, 4, r)[1] for r in range(4)] == [7, 6, 6, 6]
+    assert [lc.shard_frames(25, 2, r)[1] for r in range(2)] == [13, 12]
     for T in range(1, 30):
         for g in (1, 2, 4, 8):
             spans = [lc.shard_frames(T, g, r) for r in range(g)]

@@ -1,9 +1,13 @@
 """Multi-GPU sliced decode: the host-side partition and the frame gather.
 
-* world_size 2 over gloo on CPU: each rank decodes its contiguous frame
-  block (lc_shard_frames) with the oracle decoder, the blocks are gathered
-  to rank 0 and must equal the single-process decode bit-exactly (decode is
-  frame-wise, proj/src/codec.cpp:126-145).
+* world_size 2/3/4 over gloo on CPU: every rank takes its balanced frame
+  block (lc_shard_frames), decodes it slice by slice with the oracle
+  decoder, and the ranks execute the product's gather schedule
+  (lc_gather_plan: round i sends the i-th slice of every rank to rank 0)
+  with point-to-point send/recv -- the same rows lc_decode_sharded issues as
+  ncclSend / grouped ncclRecv on the GPU.  Rank 0's assembled video must
+  equal the single-process decode bit-exactly (decode is frame-wise,
+  proj/src/codec.cpp:126-145).
 * On one GPU: lc_decode_sharded with world 1 equals lc_decode.
 """
 import os
@@ -26,7 +30,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, lat, out_path):
+def _worker(rank, world, port, lat, slice_frames, out_path):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -40,35 +44,66 @@ def _worker(rank, world, port, lat, out_path):
     kv = lco.parse_text(lc.DEFAULT_CONFIG)
     kv.update({k: str(v) for k, v in TINY.items()})
     T = lat.shape[1]
+    H = W = 32
     f0, cnt = lc.shard_frames(T, world, rank)
-    part = lco.Restatement().decode(kv, lat[:, f0:f0 + cnt]) if cnt else np.zeros((1, 0, 3, 32, 32), np.float32)
-    # pad to equal chunks for all_gather (ncclAllGather-style)
-    per = -(-T // world)
-    buf = np.zeros((per, 3, 32, 32), np.float32)
-    buf[:cnt] = part[0]
-    out = [torch.zeros(per, 3, 32, 32) for _ in range(world)]
-    dist.all_gather(out, torch.from_numpy(buf))
+    plan = lc.gather_plan(T, world, slice_frames)
+    # this rank's slices, decoded one at a time (decode_sliced per slice)
+    mine = [r for r in plan if r[1] == rank]
+    assert sum(int(r[3]) for r in mine) == cnt
+    decoded = {}
+    for rnd, _, first, count in mine:
+        assert f0 <= first and first + count <= f0 + cnt
+        decoded[int(first)] = lco.Restatement().decode(kv, lat[:, first:first + count])[0]
+    video = np.full((T, 3, H, W), np.nan, np.float32) if rank == 0 else None
+    for rnd, r, first, count in plan:
+        first, count = int(first), int(count)
+        if r == 0:
+            if rank == 0:
+                video[first:first + count] = decoded[first]
+        elif rank == 0:
+            buf = torch.empty(count, 3, H, W)
+            dist.recv(buf, src=int(r))
+            video[first:first + count] = buf.numpy()
+        elif rank == r:
+            dist.send(torch.from_numpy(decoded[first]), dst=0)
     if rank == 0:
-        frames = []
-        for r in range(world):
-            g0, gc = lc.shard_frames(T, world, r)
-            frames.append(out[r][:gc].numpy())
-        np.save(out_path, np.concatenate(frames)[None])
+        np.save(out_path, video[None])
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_sharded_decode_gather_gloo(tmp_path, oracle, world):
+@pytest.mark.parametrize("world,slice_frames", [(2, 2), (3, 1), (4, 2)])
+def test_sharded_decode_gather_gloo(tmp_path, oracle, world, slice_frames):
     import lco
     import paper_2510_05367_b200 as lc
     kv = lco.parse_text(lc.DEFAULT_CONFIG)
     kv.update({k: str(v) for k, v in TINY.items()})
     lat = np.random.default_rng(0).standard_normal((1, 5, 4, 8, 8)).astype(np.float32)
     out_path = str(tmp_path / "video.npy")
-    mp.start_processes(_worker, args=(world, _free_port(), lat, out_path), nprocs=world, start_method="fork")
+    # spawn, not fork: the parent's OpenMP pool (the oracle decoder) does
+    # not survive a fork (libgomp hangs in the child)
+    mp.start_processes(_worker, args=(world, _free_port(), lat, slice_frames, out_path), nprocs=world,
+                       start_method="spawn")
     got = np.load(out_path)
     want = oracle.decode(kv, lat)
     assert np.array_equal(got, want)
+
+
+def test_gather_plan_rounds():
+    """Every frame is moved exactly once, slices never exceed the slice
+    size, and round i holds the i-th slice of each rank that has one."""
+    import paper_2510_05367_b200 as lc
+    for T in (1, 5, 16, 25):
+        for world in (1, 2, 3, 4, 8):
+            for sl in (1, 2, 4, 5):
+                plan = lc.gather_plan(T, world, sl)
+                frames = sorted(f for _, _, a, c in plan for f in range(a, a + c))
+                assert frames == list(range(T))
+                assert all(1 <= c <= sl for *_, c in plan)
+                for r in range(world):
+                    f0, cnt = lc.shard_frames(T, world, r)
+                    rows = [row for row in plan if row[1] == r]
+                    assert [int(x[0]) for x in rows] == list(range(len(rows)))
+                    assert [int(x[2]) for x in rows] == list(range(f0, f0 + cnt, sl))
 
 
 @pytest.mark.gpu
@@ -77,8 +112,26 @@ def test_decode_sharded_single_rank_equals_decode(ctx):
     ctx.configure(lc.config_text(TINY, base=lc.DEFAULT_CONFIG))
     lat = np.random.default_rng(1).standard_normal((1, 5, 4, 8, 8)).astype(np.float32)
     a = ctx.decode(lat, slice_frames=2)
-    b, ms = ctx.decode_sharded(lat, slice_frames=2)
+    b, ms = ctx.decode_sharded(lat, slice_frames=2, out=np.empty(a.size, np.float32))
     assert np.array_equal(a, b) and ms > 0
+    # device-only form (the gathered video stays in HBM): same call, no output
+    none, ms2 = ctx.decode_sharded(lat, slice_frames=2)
+    assert none is None and ms2 > 0
+
+
+@pytest.mark.gpu
+def test_decode_rejects_wrong_latent_geometry(ctx):
+    """decode_batch / decode_sliced raise ShapeError on a channel mismatch
+    (proj/src/codec.cpp:129-131); the engine also rejects a latent h x w
+    other than the configured one (no host overrun)."""
+    import paper_2510_05367_b200 as lc
+    ctx.configure(lc.config_text(TINY, base=lc.DEFAULT_CONFIG))
+    with pytest.raises(lc.ShapeError):
+        ctx.decode(np.zeros((1, 2, 3, 8, 8), np.float32))
+    with pytest.raises(lc.ShapeError):
+        ctx.decode(np.zeros((1, 2, 4, 16, 8), np.float32))
+    with pytest.raises(lc.ShapeError):
+        ctx.decode_sharded(np.zeros((1, 2, 5, 8, 8), np.float32), out=np.empty(2 * 3 * 32 * 32, np.float32))
 
 
 @pytest.mark.gpu
@@ -93,10 +146,10 @@ def test_decode_sharded_repeated_calls_and_pinned_buffers(ctx):
     lat6 = rng.standard_normal((1, 6, 4, 8, 8)).astype(np.float32)
     want6 = ctx.decode(lat6, slice_frames=4)
     for _ in range(3):
-        got, _ = ctx.decode_sharded(lat6, slice_frames=4)
+        got, _ = ctx.decode_sharded(lat6, slice_frames=4, out=np.empty(want6.size, np.float32))
         assert np.array_equal(got, want6)
     lat3 = lat6[:, :3].copy()
-    got3, _ = ctx.decode_sharded(lat3, slice_frames=4)
+    got3, _ = ctx.decode_sharded(lat3, slice_frames=4, out=np.empty(want6.size // 2, np.float32))
     assert np.array_equal(got3, want6[:, :3])
     lp, vp = lc.PinnedArray(lat6.size), lc.PinnedArray(want6.size)
     lp.array[:] = lat6.reshape(-1)
