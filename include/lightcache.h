@@ -57,6 +57,34 @@ int64_t lc_video_elems(lc_ctx* ctx);  /* T*3*H*W of the b=1 video */
 int lc_run_pipeline(lc_ctx* ctx, const float* x0, float* video, float* latent_out,
                     char* report, int64_t report_cap);
 
+/* Typed RunResult of the last completed run (run_pipeline's result,
+ * proj/include/stagecache/pipeline.hpp:18-39), without the video (passed to
+ * lc_run_pipeline) and the config (the caller's).  wall_*: StageWall in
+ * seconds -- setup is the host time of the lc_configure that initialised
+ * and packed the weights, encode / denoise / decode / total are device
+ * (CUDA event) times of the run.  peak_* / current_* / events_per_stage /
+ * event_count: StageReport of the engine's ledger (stage order setup,
+ * encode, denoise, decode).  Timeline rows (kind, step, bytes, clock_ns) in
+ * TimelineEventKind order (swap.hpp:16-31), clock from the run's start;
+ * pass timeline = NULL to query n_timeline. */
+typedef struct lc_run_result {
+    double wall_setup, wall_encode, wall_denoise, wall_decode, wall_total;
+    int64_t peak_fast[4], peak_slow[4];
+    int64_t current_fast, current_slow;
+    int64_t events_per_stage[4];
+    int64_t event_count;
+    int64_t denoiser_macs, macs_per_full_step, macs_per_cached_step, full_steps, cached_steps;
+    int64_t cache_bytes_planned;
+    double makespan_s, stall_s;
+    int simulated;
+    int64_t n_timeline;
+} lc_run_result;
+int lc_get_run_result(lc_ctx* ctx, lc_run_result* out, int64_t* timeline, int64_t cap_rows);
+/* Stage (0 setup, 1 encode, 2 denoise, 3 decode) of the last BudgetError
+ * on this thread (BudgetError::stage, proj/include/stagecache/common.hpp:43),
+ * -1 when the last error was of another kind. */
+int lc_last_error_stage(void);
+
 /* Device-resident variant for throughput measurement: the initial latent
  * must have been staged with lc_upload_latent; the video stays in HBM
  * (fetch with lc_download_video). */

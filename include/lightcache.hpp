@@ -13,6 +13,7 @@
 // carry over unchanged.
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -33,7 +34,8 @@ struct ConfigError : Error {
     using Error::Error;
 };
 struct BudgetError : Error {
-    using Error::Error;
+    int stage;  // 0 setup, 1 encode, 2 denoise, 3 decode (BudgetError::stage)
+    BudgetError(int st, const std::string& m) : Error(m), stage(st) {}
 };
 struct InvariantError : Error {
     using Error::Error;
@@ -48,7 +50,7 @@ inline void check(int rc) {
     switch (rc) {
         case 1: throw ShapeError(m);
         case 2: throw ConfigError(m);
-        case 3: throw BudgetError(m);
+        case 3: throw BudgetError(lc_last_error_stage(), m);
         case 4: throw InvariantError(m);
         default: throw DeviceError(m);
     }
@@ -69,12 +71,38 @@ inline StepPlan plan_steps(int64_t total, int64_t interval_n) {
     return p;
 }
 
-// RunResult subset (proj/include/stagecache/pipeline.hpp:18-39): the
-// decoded video {t,c,h,w} fp32 plus the JSON report (device ms per stage,
-// MAC counters, cache bytes, swap timeline, per-stage peaks).
+// StageWall / StageReport / TimelineEvent / RunResult
+// (proj/include/stagecache/pipeline.hpp:11-39, ledger.hpp:49-63,
+// swap.hpp:16-31) -- the typed result of lc_get_run_result plus the video.
+struct StageWall {
+    double setup = 0, encode = 0, denoise = 0, decode = 0, total = 0;
+};
+struct StageReport {
+    std::array<std::array<int64_t, 2>, 4> peak{};  // [stage][tier]
+    std::array<int64_t, 2> current{};
+    std::array<int64_t, 4> events_per_stage{};
+    uint64_t event_count = 0;
+    int64_t stage_peak(int s, int t) const { return peak[static_cast<size_t>(s)][static_cast<size_t>(t)]; }
+    int64_t overall_peak(int t) const {
+        int64_t m = 0;
+        for (const auto& row : peak) m = row[static_cast<size_t>(t)] > m ? row[static_cast<size_t>(t)] : m;
+        return m;
+    }
+};
+struct TimelineEvent {
+    int kind = 0;  // TimelineEventKind: 0 compute_start .. 5 await_end
+    int64_t step = -1, bytes = 0, clock_ns = 0;
+};
 struct RunResult {
-    std::vector<float> video;
-    std::string report_json;
+    std::vector<float> video;  // b = 1, {t,c,h,w}
+    StageWall wall;
+    StageReport mem;
+    std::vector<TimelineEvent> timeline;
+    int64_t denoiser_macs = 0, macs_per_full_step = 0, macs_per_cached_step = 0;
+    int64_t full_steps = 0, cached_steps = 0, cache_bytes_planned = 0;
+    double makespan_s = 0, stall_s = 0;
+    bool simulated = false;
+    std::string report_json;  // the engine's JSON report (device ms, swap bytes, arena, ...)
 };
 
 // One GPU context (weights, buffers, streams).
@@ -94,7 +122,34 @@ public:
         check(lc_run_pipeline(ctx_, nullptr, r.video.data(), nullptr, rep.data(),
                               static_cast<int64_t>(rep.size())));
         r.report_json = rep.data();
+        fill_result(&r);
         return r;
+    }
+    // typed fields of the last run (lc_get_run_result)
+    void fill_result(RunResult* r) {
+        lc_run_result t{};
+        check(lc_get_run_result(ctx_, &t, nullptr, 0));
+        std::vector<int64_t> rows(static_cast<size_t>(4 * t.n_timeline));
+        check(lc_get_run_result(ctx_, &t, rows.data(), t.n_timeline));
+        r->wall = {t.wall_setup, t.wall_encode, t.wall_denoise, t.wall_decode, t.wall_total};
+        for (size_t s = 0; s < 4; ++s) {
+            r->mem.peak[s] = {t.peak_fast[s], t.peak_slow[s]};
+            r->mem.events_per_stage[s] = t.events_per_stage[s];
+        }
+        r->mem.current = {t.current_fast, t.current_slow};
+        r->mem.event_count = static_cast<uint64_t>(t.event_count);
+        r->timeline.resize(static_cast<size_t>(t.n_timeline));
+        for (size_t i = 0; i < r->timeline.size(); ++i)
+            r->timeline[i] = {static_cast<int>(rows[4 * i]), rows[4 * i + 1], rows[4 * i + 2], rows[4 * i + 3]};
+        r->denoiser_macs = t.denoiser_macs;
+        r->macs_per_full_step = t.macs_per_full_step;
+        r->macs_per_cached_step = t.macs_per_cached_step;
+        r->full_steps = t.full_steps;
+        r->cached_steps = t.cached_steps;
+        r->cache_bytes_planned = t.cache_bytes_planned;
+        r->makespan_s = t.makespan_s;
+        r->stall_s = t.stall_s;
+        r->simulated = t.simulated != 0;
     }
     // Throughput form with caller-owned (pinned) buffers: queue runs, then wait().
     void run_pipeline_async(const float* x0, float* video) { check(lc_run_pipeline_async(ctx_, x0, video)); }

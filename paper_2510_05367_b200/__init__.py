@@ -97,6 +97,7 @@ EXPORTS = [
     "lc_forward", "lc_decode", "lc_video_metrics", "lc_ledger_csv", "lc_ledger_summary", "lc_conv2d", "lc_up_conv2d", "lc_plan_steps", "lc_split",
     "lc_model_numbers", "lc_simulate_timeline", "lc_derive_seed", "lc_randn", "lc_shard_frames", "lc_nccl_unique_id",
     "lc_nccl_init", "lc_decode_sharded", "lc_gather_plan", "lc_host_register", "lc_host_unregister", "lc_mem_info",
+    "lc_get_run_result", "lc_last_error_stage",
     "lc_timer_start", "lc_timer_stop", "lc_set_conv_profile",
     "lc_conv_profile", "lc_conv_profile_records", "lc_kernel_launches", "lc_alloc_pinned", "lc_free_pinned",
 ]

@@ -24,6 +24,7 @@ struct lc_ctx {
 namespace {
 
 thread_local std::string g_err;
+thread_local int g_err_stage = -1;
 
 template <typename F>
 int guarded(F&& f) {
@@ -32,9 +33,11 @@ int guarded(F&& f) {
         return 0;
     } catch (const lc::LcError& e) {
         g_err = e.what();
+        g_err_stage = e.code == lc::kBudgetError ? e.stage : -1;
         return e.code;
     } catch (const std::exception& e) {
         g_err = e.what();
+        g_err_stage = -1;
         return lc::kShapeError;
     }
 }
@@ -86,6 +89,12 @@ std::string report_json(const lc::Engine& e, const lc::RunStats& st) {
            << "," << static_cast<int64_t>(t[2]) << "," << t[3] << "]";
     }
     os << "]},\"kernel_launches\":" << st.kernel_launches << ",";
+    {
+        const auto ai = e.arena_info();
+        os << "\"arena\":{\"bytes\":" << ai.arena << ",\"activations\":" << ai.act << ",\"cache\":" << ai.cache
+           << ",\"decode\":" << ai.dec << ",\"encode\":" << ai.enc
+           << ",\"decode_overlaps_cache\":" << (ai.dec_overlaps_cache ? "true" : "false") << "},";
+    }
     const auto& c = e.config();
     os << "\"video\":{\"frames\":" << c.frames << ",\"channels\":" << c.image_channels
        << ",\"height\":" << c.height << ",\"width\":" << c.width << "}}";
@@ -136,6 +145,54 @@ extern "C" {
 
 int lc_version(void) { return 1; }
 const char* lc_last_error(void) { return g_err.c_str(); }
+int lc_last_error_stage(void) { return g_err_stage; }
+
+int lc_get_run_result(lc_ctx* ctx, lc_run_result* out, int64_t* timeline, int64_t cap_rows) {
+    return guarded_on(ctx, [&] {
+        const lc::RunStats& st = ctx->engine.last_stats();
+        const lc::Ledger& l = ctx->engine.ledger();
+        lc_run_result r{};
+        r.wall_setup = st.setup_s;
+        r.wall_encode = st.ms_encode * 1e-3;
+        r.wall_denoise = st.ms_denoise * 1e-3;
+        r.wall_decode = st.ms_decode * 1e-3;
+        r.wall_total = st.ms_total * 1e-3;
+        for (int s = 0; s < 4; ++s) {
+            r.peak_fast[s] = st.peak[s][0];
+            r.peak_slow[s] = st.peak[s][1];
+            r.events_per_stage[s] = l.events_per_stage[s];
+        }
+        r.current_fast = l.occ[0];
+        r.current_slow = l.occ[1];
+        r.event_count = static_cast<int64_t>(l.events.size());
+        r.denoiser_macs = st.denoiser_macs;
+        r.macs_per_full_step = st.macs_full;
+        r.macs_per_cached_step = st.macs_cached;
+        r.full_steps = st.full_steps;
+        r.cached_steps = st.cached_steps;
+        r.cache_bytes_planned = st.cache_bytes_planned;
+        r.makespan_s = st.makespan_ms * 1e-3;
+        r.stall_s = st.stall_ms * 1e-3;
+        r.simulated = st.simulated ? 1 : 0;
+        // the reference's TimelineEventKind rows (the partial seam awaits,
+        // kinds 7/8, are this engine's refinement and stay in the JSON report)
+        int64_t n = 0;
+        for (const auto& t : st.timeline) {
+            const int kind = static_cast<int>(t[0]);
+            if (kind > 5) continue;
+            if (timeline) {
+                if (n >= cap_rows) lc::throw_shape("timeline buffer too small");
+                timeline[4 * n + 0] = kind;
+                timeline[4 * n + 1] = static_cast<int64_t>(t[1]);
+                timeline[4 * n + 2] = static_cast<int64_t>(t[2]);
+                timeline[4 * n + 3] = static_cast<int64_t>(std::llround(t[3] * 1e6));
+            }
+            ++n;
+        }
+        r.n_timeline = n;
+        if (out) *out = r;
+    });
+}
 
 int lc_ctx_create(int device, lc_ctx** out) {
     return guarded([&] { *out = new lc_ctx(device); });
@@ -265,8 +322,10 @@ int lc_ledger_csv(lc_ctx* ctx, char* buf, int64_t cap, int64_t* needed) {
         os << "seq,clock,kind,tier,bytes,alloc_id,occupancy_bytes,stage\n";
         int64_t occ[2] = {0, 0};
         for (const lc::LedgerEvent& e : l.events) {
-            if (e.kind == 0) occ[e.tier] += e.bytes;
-            if (e.kind == 1) occ[e.tier] -= e.bytes;
+            // replay as write_ledger_csv does (ledger.cpp:224-242): a move's
+            // start row carries the destination tier, its end the source
+            if (e.kind == 0 || e.kind == 2) occ[e.tier] += e.bytes;
+            if (e.kind == 1 || e.kind == 3) occ[e.tier] -= e.bytes;
             os << e.seq << ',' << e.clock << ',' << kinds[e.kind] << ',' << (e.tier ? "slow" : "fast") << ','
                << e.bytes << ',' << e.alloc_id << ',' << occ[e.tier] << ',' << stages[e.stage] << "\n";
         }

@@ -29,7 +29,7 @@
 
 namespace lc {
 
-constexpr int kMaxTaps = 49;  // odd kernels up to 7x7
+constexpr int kMaxTaps = 225;  // odd kernels up to 15x15 (ConvParams stays well under the 32 KB parameter limit)
 
 // One K segment: one source tensor read through one TMA descriptor.
 struct ConvSegDev {
@@ -118,6 +118,8 @@ struct alignas(64) ConvParams {
     int hox[4], hoy[4];
     FastDiv fd_units, fd_ntiles, fd_par, fd_tx, fd_ty;  // launch-side divisors of tile_coord
 };
+// passed by value as a __grid_constant__ kernel parameter (32 KB limit)
+static_assert(sizeof(ConvParams) < 16384, "ConvParams too large for a kernel parameter");
 
 // CTA-group choice for a launch (the weight tensor map's box depends on it:
 // each CTA of a pair stages BN/2 weight rows).

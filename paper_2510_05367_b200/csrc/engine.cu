@@ -30,13 +30,18 @@ void Ledger::enter(int s) {
     for (int t = 0; t < 2; ++t) peak[s][t] = std::max(peak[s][t], occ[t]);
     record(4, 0, 0, 0);
 }
-uint64_t Ledger::alloc(int tier, int64_t bytes) {
-    if (tier == 0 && budget_fast > 0 && occ[0] + bytes > budget_fast) {
+void Ledger::check_budget(int64_t extra) const {
+    if (budget_fast > 0 && occ[0] + extra > budget_fast) {
         static const char* names[4] = {"setup", "encode", "denoise", "decode"};
-        throw LcError(kBudgetError, std::string("fast-tier budget exceeded in stage ") + names[stage] +
-                                        ": " + std::to_string(occ[0]) + " + " + std::to_string(bytes) +
-                                        " > " + std::to_string(budget_fast) + " bytes");
+        throw LcError(kBudgetError,
+                      std::string("fast-tier budget exceeded in stage ") + names[stage] + ": " +
+                          std::to_string(occ[0]) + " + " + std::to_string(extra) + " > " +
+                          std::to_string(budget_fast) + " bytes",
+                      stage);
     }
+}
+uint64_t Ledger::alloc(int tier, int64_t bytes) {
+    if (tier == 0) check_budget(bytes);
     occ[tier] += bytes;
     peak[stage][tier] = std::max(peak[stage][tier], occ[tier]);
     const uint64_t id = next_id++;
@@ -46,6 +51,46 @@ uint64_t Ledger::alloc(int tier, int64_t bytes) {
 void Ledger::free(int tier, int64_t bytes, uint64_t id) {
     occ[tier] -= bytes;
     record(1, tier, bytes, id);
+}
+uint64_t Ledger::region_alloc(int tier, int64_t bytes) {
+    const uint64_t id = alloc(tier, bytes);
+    live[id] = Live{bytes, tier, false, tier};
+    return id;
+}
+void Ledger::region_free(uint64_t id) {
+    auto it = live.find(id);
+    if (it == live.end()) throw_invariant("ledger: free of unknown region " + std::to_string(id));
+    if (it->second.moving) throw_invariant("ledger: free of a region while its tier move is in flight");
+    const Live r = it->second;
+    live.erase(it);
+    free(r.tier, r.bytes, id);
+}
+int Ledger::region_tier(uint64_t id) const {
+    auto it = live.find(id);
+    return it == live.end() ? -1 : it->second.tier;
+}
+// Double residency (ledger.cpp:93-123): the destination's occupancy rises at
+// the start of the move, the source's falls only at its end.
+void Ledger::move_start(uint64_t id, int dst) {
+    auto it = live.find(id);
+    if (it == live.end()) throw_invariant("ledger: tier move of unknown region");
+    if (it->second.moving) throw_invariant("ledger: tier move already in flight");
+    if (it->second.tier == dst) throw_invariant("ledger: tier move to the region's own tier");
+    if (dst == 0) check_budget(it->second.bytes);
+    it->second.moving = true;
+    it->second.dst = dst;
+    occ[dst] += it->second.bytes;
+    peak[stage][dst] = std::max(peak[stage][dst], occ[dst]);
+    record(2, dst, it->second.bytes, id);
+}
+void Ledger::move_end(uint64_t id) {
+    auto it = live.find(id);
+    if (it == live.end() || !it->second.moving) throw_invariant("ledger: tier move end without start");
+    const int src = it->second.tier;
+    it->second.tier = it->second.dst;
+    it->second.moving = false;
+    occ[src] -= it->second.bytes;
+    record(3, src, it->second.bytes, id);
 }
 
 DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
@@ -216,7 +261,7 @@ std::unique_ptr<TcLayer> pack_tc_layer(Ledger* l, const Bank& b, int c_split, in
     L->r = (L->k - 1) / 2;
     L->c_out = static_cast<int>(b.c_out);
     const int c_in = static_cast<int>(b.c_in), k = L->k, r = L->r;
-    if (k * k > kMaxTaps) throw_config("unet.kernel larger than 7 is not supported on the GPU path");
+    if (k * k > kMaxTaps) throw_config("unet.kernel larger than 15 is not supported on the GPU path");
     int ch0 = 0;  // first input channel of each segment
     int seg_ch0[2] = {0, 0};
     if (mode == 0) {
@@ -835,6 +880,12 @@ static std::string weights_key(const RunConfig& c) {
 }
 
 void Engine::configure(const RunConfig& cfg) {
+    const double t_cfg = Ledger::now();
+    struct SetupTimer {  // StageWall::setup: weight init + packing of this configure
+        Engine* e;
+        double t0;
+        ~SetupTimer() { e->configure_s_ = Ledger::now() - t0; }
+    } setup_timer{this, t_cfg};
     cfg.validate();
     if (async_pending_) (void)wait();
     const std::string key = weights_key(cfg);
@@ -946,7 +997,6 @@ void Engine::configure(const RunConfig& cfg) {
             for (int64_t i = 1; i <= cfg.stages; ++i)
                 enc_tc_.push_back(pack_tc_layer(&ledger_, cw_.enc[static_cast<size_t>(i)],
                                                 static_cast<int>(cw_.enc[static_cast<size_t>(i)].c_in), 0));
-            enc_alloc_ = -1;
             img_key_.clear();
         }
         if (cw_.dec[static_cast<size_t>(cfg.stages)].c_out > 4)
@@ -955,13 +1005,13 @@ void Engine::configure(const RunConfig& cfg) {
         for (int64_t i = 1; i < cfg.stages; ++i) dec_tc_.push_back(pack_tc_layer(&ledger_, cw_.dec[i], 0, 1));
         cfg_key_ = key;
         T_alloc_ = -1;
-        dec_alloc_ = -1;
     }
-    if (!same_geom) {
-        T_alloc_ = -1;
-        dec_alloc_ = -1;
-    }
+    if (!same_geom || cfg.mode != cfg_prev_mode_ || cfg.slice_decode != cfg_prev_sliced_) T_alloc_ = -1;
+    cfg_prev_mode_ = cfg.mode;
+    cfg_prev_sliced_ = cfg.slice_decode;
     invalidate_graph();  // any config change re-records the body
+    dec_bufs_op_.clear();  // operator-level decode workspace follows the geometry
+    dec_ws_op_.G = 0;
     configured_ = true;
 }
 
@@ -970,57 +1020,144 @@ int64_t Engine::latent_elems() const {
 }
 int64_t Engine::video_elems() const { return cfg_.frames * cfg_.image_channels * cfg_.height * cfg_.width; }
 
+int64_t Engine::run_dec_group() const {
+    const int64_t T = cfg_.frames;
+    return std::max<int64_t>(1, std::min<int64_t>(cfg_.slice_decode ? decode_slice : T, T));
+}
+
+// Bytes of a decode workspace for slices of G frames (DecWs); every part
+// 256-byte aligned as the arena carves it.
+int64_t Engine::dec_ws_bytes(int G, bool want_y) const {
+    auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
+    const int S = static_cast<int>(cfg_.stages);
+    const int64_t lh = cfg_.latent_h(), lw = cfg_.latent_w();
+    const int64_t cs = round_up(static_cast<int>(cfg_.codec_width), 64);
+    int64_t b = 0;
+    for (int i = 0; i < S; ++i) b += al(G * (lh << i) * (lw << i) * cs * 2);
+    b += al(G * lh * lw * dec0_kp_ * 2);
+    if (want_y && dec_last_tap_tc_)
+        b += al(static_cast<int64_t>(G) * (lh << (S - 1)) * (lw << (S - 1)) * dec_last_tap_tc_->n_pad * 4);
+    return b;
+}
+
+// The per-run working sets in ONE device arena (see Ledger in engine.hpp):
+//   [0, cache)            feature-cache entries U_{m+1} (b=2: uncond, cond)
+//   [cache, act_end)      denoise activations of every level
+//   [0, enc_end)          image mode: the encode workspace (encode precedes
+//                         denoise; cache and activations are dead)
+//   [top - dec, top)      decode workspace (the denoise activations are dead;
+//                         it may reach into the cache region only when the
+//                         swap holds the entries on the host through decode,
+//                         as the reference's final eviction does --
+//                         proj/README.md "Swap schedule" -- and then waits
+//                         for that eviction before overwriting it).
+// top = max(act_end, enc_end, dec + (cache resident through decode ? cache : 0)),
+// so the arena is exactly the peak of the working-set lifetimes the ledger
+// logs.  The video, latents, weights and noise stay separate allocations
+// (the video outlives the run: it is downloaded after or during the next).
 void Engine::alloc_activations(int64_t T) {
-    if (T_alloc_ == T) return;
+    const int64_t G = run_dec_group();
+    if (T_alloc_ == T && arena_G_ == G) return;
     invalidate_graph();
     z_key_.clear();
     act_bufs_.clear();
-    cache_buf_.reset();
+    arena_.reset();
     cache_host_.reset();
+    auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
     const int n = static_cast<int>(2 * T);
     const int M = static_cast<int>(cfg_.depth), m = static_cast<int>(cfg_.cache_depth);
     const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
     auto ch = [&](int l) { return static_cast<int>(cfg_.base_channels << l); };
-    auto make = [&](int h, int w, int c) {
-        Act a;
-        a.n = n;
-        a.h = h;
-        a.w = w;
-        a.c = c;
-        a.cs = round_up(c, 64);
-        act_bufs_.push_back(dev_alloc(&ledger_, a.elems() * 2, true));
-        a.p = act_bufs_.back().as<__half>();
-        return a;
+    // layout pass: offsets first, pointers once the arena exists
+    std::vector<std::pair<Act*, int64_t>> carve;
+    int64_t off = 0;
+    bool pad = false;
+    auto place = [&](Act* a, int nn, int h, int w, int c, int cs) {
+        a->n = nn, a->h = h, a->w = w, a->c = c, a->cs = cs;
+        a->p = nullptr;
+        carve.push_back({a, off});
+        off += al(a->elems() * 2);
+        pad = pad || cs != c;
     };
-    lv_.assign(static_cast<size_t>(M + 1), Level{});
-    stem_out_ = make(lh, lw, ch(0));
-    patch_ = make(lh, lw, stem_kp_);
-    for (int i = 0; i < M; ++i) {
-        const int h = lh >> i, w = lw >> i;
-        lv_[i].D = make(h, w, ch(i));
-        if (i >= 1) lv_[i].P = make(h, w, ch(i - 1));
-        if (!(cfg_.cache_enabled && i == m + 1)) lv_[i].U = make(h, w, ch(i));
-        const int cu = (i == M - 1) ? ch(M - 1) : ch(i + 1);
-        if (cfg_.kernel != 3 || (cfg_.chunk_enabled && cfg_.halo != HaloKind::Exact))
-            lv_[i].UP = make(h, w, cu);
-    }
-    lv_[M].P = make(lh >> M, lw >> M, ch(M - 1));
-    if (!(cfg_.cache_enabled && m + 1 == M)) mid_ = make(lh >> M, lw >> M, ch(M - 1));
+    ArenaInfo ai;
+    cache_ = Act{};
     if (cfg_.cache_enabled) {
         const int cc = static_cast<int>(cache_channels(cfg_));
-        Act a;
-        a.n = n;
-        a.h = lh >> (m + 1);
-        a.w = lw >> (m + 1);
-        a.c = cc;
-        a.cs = round_up(cc, 64);
-        cache_buf_ = dev_alloc(&ledger_, a.elems() * 2, true);
-        a.p = cache_buf_.as<__half>();
-        cache_ = a;
-        if (m + 1 == M) mid_ = a;
-        else lv_[m + 1].U = a;
-        if (cfg_.swap_mode != SwapMode::Off) cache_host_ = host_alloc(&ledger_, a.elems() * 2);
+        place(&cache_, n, lh >> (m + 1), lw >> (m + 1), cc, round_up(cc, 64));
+        ai.cache = off;
     }
+    const int64_t act0 = off;
+    lv_.assign(static_cast<size_t>(M + 1), Level{});
+    place(&stem_out_, n, lh, lw, ch(0), round_up(ch(0), 64));
+    place(&patch_, n, lh, lw, stem_kp_, stem_kp_);
+    for (int i = 0; i < M; ++i) {
+        const int h = lh >> i, w = lw >> i;
+        place(&lv_[i].D, n, h, w, ch(i), round_up(ch(i), 64));
+        if (i >= 1) place(&lv_[i].P, n, h, w, ch(i - 1), round_up(ch(i - 1), 64));
+        if (!(cfg_.cache_enabled && i == m + 1)) place(&lv_[i].U, n, h, w, ch(i), round_up(ch(i), 64));
+        const int cu = (i == M - 1) ? ch(M - 1) : ch(i + 1);
+        if (cfg_.kernel != 3 || (cfg_.chunk_enabled && cfg_.halo != HaloKind::Exact))
+            place(&lv_[i].UP, n, h, w, cu, round_up(cu, 64));
+    }
+    place(&lv_[M].P, n, lh >> M, lw >> M, ch(M - 1), round_up(ch(M - 1), 64));
+    mid_ = Act{};
+    if (!(cfg_.cache_enabled && m + 1 == M)) place(&mid_, n, lh >> M, lw >> M, ch(M - 1), round_up(ch(M - 1), 64));
+    const int64_t act_end = off;
+    act_padding_ = pad;
+    ai.act = act_end - act0;
+    // encode workspace (image mode), over the activations
+    int64_t enc_end = 0;
+    enc_padding_ = false;
+    if (cfg_.mode == "image") {
+        const int S = static_cast<int>(cfg_.stages), H = static_cast<int>(cfg_.height),
+                  W = static_cast<int>(cfg_.width), Wc = static_cast<int>(cfg_.codec_width);
+        const int Ge = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(decode_slice, T)));
+        off = 0;  // the cache entries are produced by step 0: nothing else is live in encode
+        pad = false;
+        place(&enc_patch_, Ge, H, W, enc0_kp_, enc0_kp_);
+        for (int i = 0; i < S; ++i) place(&enc_e_[i], Ge, H >> i, W >> i, Wc, round_up(Wc, 64));
+        for (int i = 1; i <= S; ++i) place(&enc_p_[i], Ge, H >> i, W >> i, Wc, round_up(Wc, 64));
+        enc_end = off;
+        enc_padding_ = pad;
+        ai.enc = enc_end;
+    }
+    // decode workspace at the top
+    const bool want_y = !(dec_last_w16_.p && subpix_fused_enabled()) && dec_last_tap_tc_ && tap_gather_enabled();
+    ai.dec = dec_ws_bytes(static_cast<int>(G), want_y);
+    const bool swap = cfg_.cache_enabled && cfg_.swap_mode != SwapMode::Off;
+    const int64_t top = std::max({act_end, enc_end, ai.dec + (swap ? 0 : ai.cache)});
+    ai.arena = top;
+    ai.dec_overlaps_cache = top - ai.dec < ai.cache;
+    {
+        off = top - ai.dec;
+        pad = false;
+        DecWs& d = dec_ws_run_;
+        d.G = static_cast<int>(G);
+        const int S = static_cast<int>(cfg_.stages);
+        const int Wc = static_cast<int>(cfg_.codec_width);
+        for (int i = 0; i < S; ++i) place(&d.act[i], d.G, lh << i, lw << i, Wc, round_up(Wc, 64));
+        place(&d.patch, d.G, lh, lw, dec0_kp_, dec0_kp_);
+        d.y = nullptr;
+        if (want_y) {
+            d.y = reinterpret_cast<float*>(static_cast<intptr_t>(off));  // offset, fixed up below
+            off += al(static_cast<int64_t>(d.G) * (lh << (S - 1)) * (lw << (S - 1)) * dec_last_tap_tc_->n_pad * 4);
+        }
+        dec_padding_ = pad;
+    }
+    // the arena: zero once (channel padding stays zero between stages unless
+    // another stage's workspace overwrote it -- see enqueue_body)
+    arena_ = dev_alloc(nullptr, std::max<int64_t>(top, 256), true);
+    char* base = arena_.as<char>();
+    for (auto& [a, o] : carve) a->p = reinterpret_cast<__half*>(base + o);
+    if (dec_ws_run_.y) dec_ws_run_.y = reinterpret_cast<float*>(base + reinterpret_cast<intptr_t>(dec_ws_run_.y));
+    if (cfg_.cache_enabled) {
+        if (m + 1 == M) mid_ = cache_;
+        else lv_[m + 1].U = cache_;
+        // the swap's slow tier: pinned host memory for both entries (its
+        // occupancy is logged by the tier moves, like the arena's regions)
+        if (cfg_.swap_mode != SwapMode::Off) cache_host_ = host_alloc(nullptr, cache_.elems() * 2);
+    }
+    arena_info_ = ai;
     const int64_t nl = T * cfg_.latent_channels * lh * lw;
     x0_ = dev_alloc(&ledger_, nl * 4, true);
     x_ = dev_alloc(&ledger_, nl * 4, true);
@@ -1030,10 +1167,21 @@ void Engine::alloc_activations(int64_t T) {
     bad_ = dev_alloc(&ledger_, 16, true);
     video_ = dev_alloc(&ledger_, T * cfg_.image_channels * cfg_.height * cfg_.width * 4, false);
     T_alloc_ = T;
+    arena_G_ = G;
+}
+
+// LC_FORCE_TILES=1: run exact-halo chunk tiles as separate launches too
+// (the lossless case below normally collapses them into one); used to prove
+// tiled == untiled bit for bit on the GPU.
+static bool force_tiles() {
+    static const bool on = std::getenv("LC_FORCE_TILES") && std::atoi(std::getenv("LC_FORCE_TILES")) != 0;
+    return on;
 }
 
 // Chunk windows for a block at a level (proj/src/chunk.cpp:145-181 split,
-// :69-92 plan_windows): output core + effective readable window.
+// :69-92 plan_windows, :201-228 run_chunked): per tile, the output core and
+// the readable (materialised) window -- the tile's padded region, outside
+// which the reference's crop reads zeros (TMA out-of-bounds fill here).
 static std::vector<Window> block_windows(const RunConfig& c, const std::string& name, int h, int w) {
     const bool chunked =
         c.chunk_enabled && std::find(c.targets.begin(), c.targets.end(), name) != c.targets.end();
@@ -1046,8 +1194,10 @@ static std::vector<Window> block_windows(const RunConfig& c, const std::string& 
     // case, proj/tests/test_chunk.cpp:118-160).  The fused kernels never
     // materialise a tile, so the tiles of that case run as ONE launch over
     // the union of the cores (the full image): identical bytes, no per-tile
-    // tails.  Halos below the radius (seams) keep one launch per tile.
-    if (halo >= r) return {Window{0, h, 0, w, 0, h, 0, w}};
+    // tails (LC_FORCE_TILES=1 keeps the tiles).  Halos below the radius
+    // (seams) always run one launch per tile.
+    const bool lossless = halo >= r;
+    if (lossless && !force_tiles()) return {Window{0, h, 0, w, 0, h, 0, w}};
     std::vector<Window> out;
     for (const Tile& t : tiles) {
         Window wd;
@@ -1055,13 +1205,16 @@ static std::vector<Window> block_windows(const RunConfig& c, const std::string& 
         wd.oy1 = static_cast<int>(t.core.y1);
         wd.ox0 = static_cast<int>(t.core.x0);
         wd.ox1 = static_cast<int>(t.core.x1);
-        if (halo >= r) {
-            wd.vy0 = 0, wd.vy1 = h, wd.vx0 = 0, wd.vx1 = w;
-        } else {
-            wd.vy0 = static_cast<int>(std::max<int64_t>(t.core.y0 - halo, 0));
-            wd.vy1 = static_cast<int>(std::min<int64_t>(t.core.y1 + halo, h));
-            wd.vx0 = static_cast<int>(std::max<int64_t>(t.core.x0 - halo, 0));
-            wd.vx1 = static_cast<int>(std::min<int64_t>(t.core.x1 + halo, w));
+        wd.vy0 = static_cast<int>(t.padded.y0);
+        wd.vy1 = static_cast<int>(t.padded.y1);
+        wd.vx0 = static_cast<int>(t.padded.x0);
+        wd.vx1 = static_cast<int>(t.padded.x1);
+        if (lossless) {
+            // the core's outputs read only core +- r inside the padded
+            // region, so widening it to even bounds (the parity-aligned
+            // window the fused sub-pixel up-conv needs) changes nothing
+            wd.vy0 &= ~1, wd.vx0 &= ~1;
+            wd.vy1 = std::min(h, (wd.vy1 + 1) & ~1), wd.vx1 = std::min(w, (wd.vx1 + 1) & ~1);
         }
         out.push_back(wd);
     }
@@ -1109,8 +1262,15 @@ void Engine::up_block(int i, const Act& skip, const Act& u, const Act& out, floa
     }
 }
 
+// LC_FUSED_STEP=0 keeps the sampler step as its own kernel (A/B timing)
+static bool fused_step_enabled() {
+    static const bool on = !(std::getenv("LC_FUSED_STEP") && std::atoi(std::getenv("LC_FUSED_STEP")) == 0);
+    return on;
+}
+
 void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t timestep, bool full,
-                         float* eps2_dev, int step, int seam) {
+                         float* eps2_dev, int step, int seam, const StepArgs* fuse) {
+    step_fused_ = false;
     const int M = static_cast<int>(cfg_.depth), m = static_cast<int>(cfg_.cache_depth);
     const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
     auto cond = [&](int j, float* s, float* o) { block_conditioning(uw_, j, timestep, s, o); };
@@ -1164,6 +1324,14 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
     auto U_of = [&](int l) -> const Act& { return l == M ? mid_ : lv_[l].U; };
     const bool writes_cache = full && cfg_.cache_enabled;
     if (writes_cache) host_valid_ = false;  // this step stores new entries
+    if (writes_cache)
+        // CacheStore::store (cache.cpp:43-63) replaces the entries: ones the
+        // swap left on the host are dropped, the new ones are HBM-resident
+        for (int b = 0; b < 2; ++b)
+            if (rid_cache_[b] && ledger_.region_tier(rid_cache_[b]) == 1) {
+                ledger_.region_free(rid_cache_[b]);
+                rid_cache_[b] = ledger_.region_alloc(0, cache_.elems());
+            }
     // CacheStore::store awaits pending transfers before replacing entries
     // (cache.cpp:48-52): the compute stream waits on entry b's eviction right
     // before the block that overwrites entry b.
@@ -1306,6 +1474,18 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
             q.C = static_cast<int>(head_tc_->c_out);
             q.N = head_n_;
             q.kb = head_kb_;
+            if (fuse && fused_step_enabled()) {
+                q.pair_T = a.n / 2;
+                q.x = fuse->x;
+                q.x_out = fuse->x_out;
+                q.z = fuse->z;
+                q.g = fuse->g;
+                q.a = fuse->a;
+                q.b = fuse->b;
+                q.c = fuse->c;
+                q.bad = fuse->bad;
+                step_fused_ = true;
+            }
             for (const Window& wd : block_windows(cfg_, "head", lh, lw)) {
                 q.win = wd;
                 q.tiles_x = (wd.ox1 - wd.ox0 + kTapTX - 1) / kTapTX;
@@ -1393,10 +1573,19 @@ void Engine::issue_evict(int step) {
     // slow-tier copy stays valid, like a clean page.  Logical transfer,
     // timeline marks and issue order are the reference's.
     const bool clean = host_valid_ && clean_evict_enabled();
+    // ledger: each entry moves to the slow tier (double residency while the
+    // copy is in flight, ledger.cpp:93-123), logged in issue order
+    auto ledger_move = [&](int b) {
+        if (rid_cache_[b] && ledger_.region_tier(rid_cache_[b]) == 0) {
+            ledger_.move_start(rid_cache_[b], 1);
+            ledger_.move_end(rid_cache_[b]);
+        }
+    };
     if (clean) {
         for (int b = 0; b < 2; ++b) {
             if (async) LC_CUDA(cudaStreamWaitEvent(st, ev_cache_ready_[b], 0));  // issue point, as a dirty one
             if (async) d2h_used_ = true;
+            ledger_move(b);
             record(2, step, bytes, st);
             record(3, step, bytes, st);
             LC_CUDA(cudaEventRecord(ev_evict_[b], st));
@@ -1411,6 +1600,7 @@ void Engine::issue_evict(int step) {
         if (async) LC_CUDA(cudaStreamWaitEvent(st, ev_cache_ready_[b], 0));
         if (async) d2h_used_ = true;
         if (stats_) stats_->swap_bytes_moved += bytes;
+        ledger_move(b);
         record(2, step, bytes, st);
         size_t ci = 0;
         for (int64_t off = 0; off < bytes; off += swap_chunk(), ++ci) {
@@ -1440,6 +1630,10 @@ void Engine::issue_prefetch(int issued, int needed) {
     const int64_t part_bytes = (cache_.n / 2 / 2) * img_bytes;
     for (int b = 0; b < 2; ++b) {
         if (async) h2d_used_ = true;
+        if (rid_cache_[b] && ledger_.region_tier(rid_cache_[b]) == 1) {
+            ledger_.move_start(rid_cache_[b], 0);  // back to HBM (budget checked, swap.cpp:198)
+            ledger_.move_end(rid_cache_[b]);
+        }
         size_t ci = 0;
         bool part_done = part_bytes <= 0;
         for (int64_t off = 0; off < bytes; off += swap_chunk(), ++ci) {
@@ -1478,29 +1672,39 @@ void Engine::seam_await(int step) {
     prefetch_pending_ = false;
 }
 
+// Operator-level decode workspace (lc_decode / lc_decode_sharded): real
+// allocations outside the run arena, grow-only per slice size.
+void Engine::ensure_op_dec_ws(int G) {
+    if (dec_ws_op_.G == G && !dec_bufs_op_.empty()) return;
+    dec_bufs_op_.clear();
+    const int S = static_cast<int>(cfg_.stages);
+    const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
+    const int Wc = static_cast<int>(cfg_.codec_width);
+    auto make = [&](int h, int w, int c, int cs) {
+        Act a{nullptr, G, h, w, cs, c};
+        dec_bufs_op_.push_back(dev_alloc(&ledger_, a.elems() * 2, true));
+        a.p = dec_bufs_op_.back().as<__half>();
+        return a;
+    };
+    for (int i = 0; i < S; ++i) dec_ws_op_.act[i] = make(lh << i, lw << i, Wc, round_up(Wc, 64));
+    dec_ws_op_.patch = make(lh, lw, dec0_kp_, dec0_kp_);
+    dec_ws_op_.y = nullptr;
+    if (dec_last_tap_tc_) {
+        const int64_t yb = static_cast<int64_t>(G) * (lh << (S - 1)) * (lw << (S - 1)) * dec_last_tap_tc_->n_pad * 4;
+        dec_bufs_op_.push_back(dev_alloc(&ledger_, yb, true));
+        dec_ws_op_.y = dec_bufs_op_.back().as<float>();
+    }
+    dec_ws_op_.G = G;
+}
+
+// Sliced decode (decode_sliced, proj/src/codec.cpp:126-145) of n latents in
+// slices of dec_ws_->G frames, using the workspace dec_ws_ points at.
 void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
     const int S = static_cast<int>(cfg_.stages);
     const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
-    const int G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cfg_.slice_decode ? decode_slice : n, n)));
-    if (dec_alloc_ != G) {
-        invalidate_graph();
-        dec_bufs_.clear();
-        for (int i = 0; i < S; ++i) {
-            Act a;
-            a.n = G;
-            a.h = lh << i;
-            a.w = lw << i;
-            a.c = static_cast<int>(cfg_.codec_width);
-            a.cs = round_up(a.c, 64);
-            dec_bufs_.push_back(dev_alloc(&ledger_, a.elems() * 2, true));
-            a.p = dec_bufs_.back().as<__half>();
-            dec_act_[i] = a;
-        }
-        dec_patch_ = Act{nullptr, G, lh, lw, dec0_kp_, dec0_kp_};
-        dec_patch_buf_ = dev_alloc(&ledger_, dec_patch_.elems() * 2, true);
-        dec_patch_.p = dec_patch_buf_.as<__half>();
-        dec_alloc_ = G;
-    }
+    if (!dec_ws_) throw_invariant("decode without a workspace");
+    const DecWs& ws = *dec_ws_;
+    const int G = ws.G;
     const int C = static_cast<int>(cfg_.latent_channels), IC = static_cast<int>(cfg_.image_channels);
     const int H = static_cast<int>(cfg_.height), W = static_cast<int>(cfg_.width);
     if (out_slices_) {
@@ -1519,7 +1723,7 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
         const int gs = static_cast<int>(std::min<int64_t>(G, n - g0));
         Act e[8];
         for (int i = 0; i < S; ++i) {
-            e[i] = dec_act_[i];
+            e[i] = ws.act[i];
             e[i].n = gs;
         }
         ThinInArgs a{};
@@ -1537,7 +1741,7 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
         a.c_out = dec0_->c_out;
         a.k = 3;
         a.silu = 1;
-        Act patch = dec_patch_;
+        Act patch = ws.patch;
         patch.n = gs;
         a.out = patch.p;
         a.cs_out = patch.cs;
@@ -1593,13 +1797,11 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
             yv.w = wl;
             yv.c = dec_last_tap_tc_->c_out;
             yv.cs = dec_last_tap_tc_->n_pad;
-            Act ymax = yv;
-            ymax.n = G;
-            ensure_buf(&dec_y_buf_, ymax.elems() * 4);
+            if (!ws.y) throw_invariant("decode workspace without tap-to-N partial sums");
             run_tc_conv(*dec_last_tap_tc_, &e[S - 1], yv, Window{0, hl, 0, wl, 0, hl, 0, wl}, 1.0f, 0.0f, false,
-                        s_compute_, dec_y_buf_.as<float>(), 0, true, true);
+                        s_compute_, ws.y, 0, true, true);
             SubpixGatherArgs g{};
-            g.y = dec_y_buf_.as<float>();
+            g.y = ws.y;
             g.cs_y = yv.cs;
             g.n = gs;
             g.H = hl;
@@ -1771,26 +1973,9 @@ void Engine::encode_dev(float* lat_dev) {
     const int T = static_cast<int>(cfg_.frames), IC = static_cast<int>(cfg_.image_channels);
     const int H = static_cast<int>(cfg_.height), W = static_cast<int>(cfg_.width);
     const int Wc = static_cast<int>(cfg_.codec_width), C = static_cast<int>(cfg_.latent_channels);
-    const int G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(decode_slice, T)));
-    if (enc_alloc_ != G) {
-        invalidate_graph();
-        enc_bufs_.clear();
-        auto make = [&](int h, int w, int c) {
-            Act a;
-            a.n = G;
-            a.h = h;
-            a.w = w;
-            a.c = c;
-            a.cs = round_up(c, 64);
-            enc_bufs_.push_back(dev_alloc(&ledger_, a.elems() * 2, true));
-            a.p = enc_bufs_.back().as<__half>();
-            return a;
-        };
-        enc_patch_ = make(H, W, enc0_kp_);
-        for (int i = 0; i < S; ++i) enc_e_[i] = make(H >> i, W >> i, Wc);
-        for (int i = 1; i <= S; ++i) enc_p_[i] = make(H >> i, W >> i, Wc);
-        enc_alloc_ = G;
-    }
+    const int G = enc_patch_.n;  // slice of the arena's encode workspace (alloc_activations)
+    if (G < 1 || !enc_patch_.p) throw_invariant("encode without a workspace");
+    (void)Wc;
     const int lh = H >> S, lw = W >> S;
     for (int g0 = 0; g0 < T; g0 += G) {
         const int gs = std::min(G, T - g0);
@@ -1854,6 +2039,13 @@ void Engine::enqueue_body(RunStats& st) {
         dl_fired_ = false;
     }
     host_valid_ = false;
+    // regions a previous body left behind (an exception mid-enqueue, e.g.
+    // BudgetError) are released so occupancy does not drift
+    for (uint64_t* id : {&rid_act_, &rid_dec_, &rid_enc_, &rid_cache_[0], &rid_cache_[1]})
+        if (*id) {
+            if (ledger_.live.count(*id)) ledger_.region_free(*id);
+            *id = 0;
+        }
     marks_.clear();
     ev_next_ = 0;
     launches = 0;
@@ -1866,7 +2058,13 @@ void Engine::enqueue_body(RunStats& st) {
         // Encode stage: latent = encode(frames); x = forward_noise(latent,
         // S-1, eps0) = sqrt(abar)*latent + sqrt(1-abar)*eps0 (pipeline.cpp:108-114)
         ledger_.enter(kEncode);
+        rid_enc_ = ledger_.region_alloc(0, arena_info_.enc);
+        // the workspace sits on the last run's activations / decode
+        // workspace: channel padding must read zero again
+        if (enc_padding_) LC_CUDA(cudaMemsetAsync(arena_.p, 0, static_cast<size_t>(arena_info_.enc), s_compute_));
         encode_dev(xn_.as<float>());
+        ledger_.region_free(rid_enc_);
+        rid_enc_ = 0;
         const Schedule sc0 = make_schedule(cfg_);
         const double ab = sc0.abar[static_cast<size_t>(cfg_.steps - 1)];
         LC_CUDA(launch_linear(static_cast<float>(std::sqrt(ab)), xn_.as<float>(),
@@ -1874,6 +2072,21 @@ void Engine::enqueue_body(RunStats& st) {
                               s_compute_));
         ++launches;
         ledger_.enter(kDenoise);
+    }
+    // Denoise working set: the activations and the two cache entries (the
+    // reference's CacheStore holds one entry per CFG branch, cache.cpp:43-90)
+    rid_act_ = ledger_.region_alloc(0, arena_info_.act);
+    rid_cache_[0] = rid_cache_[1] = 0;
+    if (cfg_.cache_enabled)
+        for (int b = 0; b < 2; ++b) rid_cache_[b] = ledger_.region_alloc(0, cache_.elems());  // bytes/2 per branch
+    {
+        // the previous run's decode (and this run's encode) workspace
+        // overwrote part of the arena: re-zero the channel padding the TMA
+        // 64-channel blocks read (no padding at base 320: nothing to do)
+        const int64_t dec_lo = arena_info_.arena - arena_info_.dec;
+        const int64_t act_end = arena_info_.cache + arena_info_.act;
+        if (act_padding_ && (dec_lo < act_end || cfg_.mode == "image"))
+            LC_CUDA(cudaMemsetAsync(arena_.p, 0, static_cast<size_t>(act_end), s_compute_));
     }
     LC_CUDA(cudaMemsetAsync(bad_.p, 0, 16, s_compute_));
     LC_CUDA(launch_isfinite(x_.as<float>(), nl, bad_.as<int>(), s_compute_));
@@ -1892,19 +2105,6 @@ void Engine::enqueue_body(RunStats& st) {
         record(0, static_cast<int>(s), 0, s_compute_);
         // 3: full step whose store will be evicted (mark the cache-ready point)
         const int seam = swap ? (full ? 3 : (plan.is_last_consumer(s) ? 2 : 1)) : 0;
-        forward_dev(xa, false, T, t_orig, full, eps2_.as<float>(), static_cast<int>(s), seam);
-        record(1, static_cast<int>(s), 0, s_compute_);
-        if (full) {
-            st.full_steps++;
-            st.denoiser_macs += st.macs_full;
-            if (swap) {
-                issue_evict(static_cast<int>(s));
-                if (plan.has_consumers(s)) issue_prefetch(static_cast<int>(s), static_cast<int>(s + 1));
-            }
-        } else {
-            st.cached_steps++;
-            st.denoiser_macs += st.macs_cached;
-        }
         const StepCoeffs k = step_coeffs(cfg_, sc, s);
         StepArgs a{};
         a.eps2 = eps2_.as<float>();
@@ -1919,18 +2119,55 @@ void Engine::enqueue_body(RunStats& st) {
         a.b = k.b;
         a.c = k.noise;
         a.bad = bad_.as<int>();
-        LC_CUDA(launch_step(a, s_compute_));
-        ++launches;
+        // the head (K8) applies the step in its epilogue when it can
+        forward_dev(xa, false, T, t_orig, full, eps2_.as<float>(), static_cast<int>(s), seam, &a);
+        record(1, static_cast<int>(s), 0, s_compute_);
+        if (full) {
+            st.full_steps++;
+            st.denoiser_macs += st.macs_full;
+            if (swap) {
+                issue_evict(static_cast<int>(s));
+                if (plan.has_consumers(s)) issue_prefetch(static_cast<int>(s), static_cast<int>(s + 1));
+            }
+        } else {
+            st.cached_steps++;
+            st.denoiser_macs += st.macs_cached;
+        }
+        if (!step_fused_) {
+            LC_CUDA(launch_step(a, s_compute_));
+            ++launches;
+        }
         std::swap(xa, xb);
     }
     x_final_ = xa;
     record_timing(ev_den1_, s_compute_);
+    // the denoise activations die with the loop (x_in / eps of the last step,
+    // pipeline.cpp:170-186); the cache entries stay (on the host after the
+    // final eviction with the swap on, in HBM without it) until the store's
+    // teardown after decode (pipeline.cpp:206)
+    ledger_.region_free(rid_act_);
+    rid_act_ = 0;
     if (cfg_.swap_simulate) ledger_.virt = sim_decode_s_;
     ledger_.enter(kDecode);
+    rid_dec_ = ledger_.region_alloc(0, arena_info_.dec);
+    if (arena_info_.dec_overlaps_cache && evict_pending_)
+        for (int b = 0; b < 2; ++b) LC_CUDA(cudaStreamWaitEvent(s_compute_, ev_evict_[b], 0));
+    if (dec_padding_)
+        LC_CUDA(cudaMemsetAsync(arena_.as<char>() + (arena_info_.arena - arena_info_.dec), 0,
+                                static_cast<size_t>(arena_info_.dec), s_compute_));
     out_slices_ = true;
+    dec_ws_ = &dec_ws_run_;
     decode_dev(xa, T, video_.as<float>());
+    dec_ws_ = nullptr;
     out_slices_ = false;
     dl_capture_ = false;
+    ledger_.region_free(rid_dec_);
+    rid_dec_ = 0;
+    for (int b = 0; b < 2; ++b)
+        if (rid_cache_[b]) {
+            ledger_.region_free(rid_cache_[b]);  // CacheStore::teardown (cache.cpp:110-122)
+            rid_cache_[b] = 0;
+        }
     // join the copy streams that were used (required to close a graph
     // capture; the last eviction stays in flight through decode as in the
     // reference, proj/README.md "Swap schedule")
@@ -1952,9 +2189,10 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
     alloc_activations(T);
     ledger_.budget_fast = cfg_.budget_fast_bytes;
     if (cfg_.budget_fast_bytes > 0 && ledger_.occ[0] > cfg_.budget_fast_bytes)
-        throw LcError(kBudgetError, "fast-tier budget exceeded in stage denoise: " +
-                                        std::to_string(ledger_.occ[0]) + " > " +
-                                        std::to_string(cfg_.budget_fast_bytes) + " bytes");
+        throw LcError(kBudgetError,
+                      "fast-tier budget exceeded in stage denoise: " + std::to_string(ledger_.occ[0]) + " > " +
+                          std::to_string(cfg_.budget_fast_bytes) + " bytes",
+                      kDenoise);
     const int64_t nl = latent_elems();
     const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
     prepare_noise();
@@ -2134,6 +2372,10 @@ RunStats Engine::finish_run(RunStats st, float* video_host, float* latent_host) 
     st.ms_decode = ms;
     LC_CUDA(cudaEventElapsedTime(&ms, t_start, ev_end_));
     st.ms_total = ms;
+    if (!marks_.empty()) {  // body origin (record 6) -> denoise start: the encode stage
+        LC_CUDA(cudaEventElapsedTime(&ms, marks_.front().ev, ev_den0_));
+        st.ms_encode = ms;
+    }
     st.timeline.clear();
     st.stall_ms = 0;
     double open = 0, lo = 1e30, hi = -1e30;
@@ -2171,7 +2413,9 @@ RunStats Engine::finish_run(RunStats st, float* video_host, float* latent_host) 
     st.hbm_peak = 0;
     for (int s = 0; s < 4; ++s) st.hbm_peak = std::max(st.hbm_peak, ledger_.peak[s][0]);
     st.kernel_launches = launches;
+    st.setup_s = configure_s_;
     ledger_.enter(kSetup);
+    last_stats_ = st;
     return st;
 }
 
@@ -2189,6 +2433,10 @@ void Engine::forward(const float* x_host, int64_t T, int64_t timestep, const flo
     const int64_t n1 = T * C * lh * lw;
     // explicit (2,T,...) input: the stem reads both halves as given.
     invalidate_graph();
+    if (act_padding_) {  // a run's decode workspace may have overwritten the channel padding
+        LC_CUDA(cudaMemsetAsync(arena_.p, 0, static_cast<size_t>(arena_info_.cache + arena_info_.act), s_compute_));
+        LC_CUDA(cudaStreamSynchronize(s_compute_));
+    }
     DevBuf xin = dev_alloc(nullptr, 2 * n1 * 4, false);
     h2d_blocking(xin.p, x_host, static_cast<size_t>(2 * n1) * 4);
     const bool full = deep_in_ref == nullptr;
@@ -2250,15 +2498,11 @@ void Engine::decode(const float* lat_host, int64_t n, int64_t c, int64_t h, int6
     DevBuf lat = dev_alloc(nullptr, nl * 4, false);
     DevBuf vid = dev_alloc(nullptr, nv * 4, false);
     LC_CUDA(cudaMemcpyAsync(lat.p, lat_host, static_cast<size_t>(nl) * 4, cudaMemcpyHostToDevice, s_compute_));
-    const int64_t keep = decode_slice;
-    decode_slice = slice;
-    const bool keep_sliced = cfg_.slice_decode;
-    cfg_.slice_decode = true;
-    dec_alloc_ = -1;
+    if (slice < 1) throw_config("decode slice must be >= 1");
+    ensure_op_dec_ws(static_cast<int>(std::min(slice, n)));
+    dec_ws_ = &dec_ws_op_;
     decode_dev(lat.as<float>(), n, vid.as<float>());
-    decode_slice = keep;
-    cfg_.slice_decode = keep_sliced;
-    dec_alloc_ = -1;
+    dec_ws_ = nullptr;
     LC_CUDA(cudaMemcpyAsync(video_host, vid.p, static_cast<size_t>(nv) * 4, cudaMemcpyDeviceToHost, s_compute_));
     LC_CUDA(cudaStreamSynchronize(s_compute_));
 }
@@ -2298,15 +2542,15 @@ void Engine::decode_sharded(const float* lat_host, int64_t T, int64_t c, int64_t
     LC_CUDA(cudaEventRecord(ej, s_compute_));
     LC_CUDA(cudaStreamWaitEvent(s_comm_, ej, 0));
     LC_CUDA(cudaStreamWaitEvent(s_d2h_, ej, 0));
-    const int64_t keep = decode_slice;
-    const bool keep_sliced = cfg_.slice_decode;
-    decode_slice = slice;
-    cfg_.slice_decode = true;
     out_slices_ = true;  // per-slice completion events (chunk_event(2, i))
-    if (me.count > 0) decode_dev(shard_lat_.as<float>(), me.count, vid + own0 * vid_frame);
+    slice_spans_.clear();
+    if (me.count > 0) {
+        ensure_op_dec_ws(static_cast<int>(std::min(slice, me.count)));
+        dec_ws_ = &dec_ws_op_;
+        decode_dev(shard_lat_.as<float>(), me.count, vid + own0 * vid_frame);
+        dec_ws_ = nullptr;
+    }
     out_slices_ = false;
-    decode_slice = keep;
-    cfg_.slice_decode = keep_sliced;
     auto nccl = [](ncclResult_t r, const char* what) {
         if (r != ncclSuccess) throw LcError(kCudaError, std::string(what) + ": " + ncclGetErrorString(r));
     };

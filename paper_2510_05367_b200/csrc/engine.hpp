@@ -28,16 +28,24 @@ void cuda_check(cudaError_t e, const char* what);
 // by the engine, Slow = pinned host bytes (cf. MemLedger,
 // proj/include/stagecache/ledger.hpp:69-146; peaks per stage, fast budget).
 enum Stage { kSetup = 0, kEncode = 1, kDenoise = 2, kDecode = 3 };
-// Physical memory ledger of the engine (the reference's
-// MemLedger, proj/src/ledger.cpp:35-123): every HBM (fast) and pinned-host
-// (slow) allocation and free is an event with an id, the stage it happened
-// in and a monotonic clock; stage entries are events too.  Peaks per
-// (stage, tier), the fast-tier budget (BudgetError naming the stage) and
-// the CSV / JSON writers' content (proj/src/ledger.cpp:200-242) come from it.
-// Swap transfers do not change occupancy here: the device cache buffer and
-// its pinned host copy are both resident for the whole run.
+// Memory ledger of the engine (the reference's MemLedger,
+// proj/src/ledger.cpp:35-123): every HBM (fast) and pinned-host (slow)
+// allocation and free is an event with an id, the stage it happened in and
+// a clock; stage entries are events too.  Besides the persistent
+// allocations (weights, latents, video: real cudaMalloc / cudaHostAlloc),
+// the per-run working sets live in ONE device arena (Engine::alloc_arena)
+// and are logged as regions with lifetimes: the denoise activations and the
+// feature-cache entries for the denoise stage, the decode (and encode)
+// workspace for its stage, each alloc / free at the stage boundary, and the
+// swap's tier moves of the cache entries (move_start adds the destination
+// tier's bytes -- double residency -- move_end releases the source,
+// ledger.cpp:93-123).  The arena is sized to the peak of those lifetimes, so
+// the ledger's fast-tier peak is the physical HBM the engine holds.
+// Peaks per (stage, tier), the fast-tier budget (BudgetError naming the
+// stage) and the CSV / JSON writers' content (proj/src/ledger.cpp:200-242)
+// come from it.
 struct LedgerEvent {
-    int kind;  // 0 alloc, 1 free, 4 stage_enter (ledger.hpp MemEventKind)
+    int kind;  // 0 alloc, 1 free, 2 move_start, 3 move_end, 4 stage_enter (ledger.hpp MemEventKind)
     int64_t bytes;
     int tier;  // 0 fast (HBM), 1 slow (pinned host)
     int stage;
@@ -56,11 +64,25 @@ struct Ledger {
     // swap.simulate: events carry the simulated engine's virtual clock
     // (pipeline.cpp:79-82) at the enclosing step boundary; < 0 = monotonic.
     double virt = -1;
+    struct Live {
+        int64_t bytes;
+        int tier;
+        bool moving;
+        int dst;
+    };
+    std::map<uint64_t, Live> live;  // arena regions (persistent buffers are not tracked here)
     static double now();
     void enter(int s);
     uint64_t alloc(int tier, int64_t bytes);
     void free(int tier, int64_t bytes, uint64_t id);
     void record(int kind, int tier, int64_t bytes, uint64_t id);
+    void check_budget(int64_t extra) const;
+    // arena regions with lifetimes (see above)
+    uint64_t region_alloc(int tier, int64_t bytes);
+    void region_free(uint64_t id);
+    void move_start(uint64_t id, int dst);
+    void move_end(uint64_t id);
+    int region_tier(uint64_t id) const;
 };
 
 struct DevBuf {
@@ -169,7 +191,8 @@ Bank subpixel_shuffle_bank(const Bank& b);
 
 // ---------------------------------------------------------------- engine
 struct RunStats {
-    double ms_denoise = 0, ms_decode = 0, ms_total = 0;  // device-timed
+    double ms_encode = 0, ms_denoise = 0, ms_decode = 0, ms_total = 0;  // device-timed
+    double setup_s = 0;  // host wall time of the configure() that prepared the weights
     double stall_ms = 0, makespan_ms = 0;
     int64_t full_steps = 0, cached_steps = 0;
     int64_t macs_full = 0, macs_cached = 0, denoiser_macs = 0;
@@ -233,11 +256,41 @@ public:
     cudaStream_t stream() const { return s_compute_; }
     Ledger& ledger() { return ledger_; }
 
+    const RunStats& last_stats() const { return last_stats_; }
+    double configure_s_ = 0;
+
     int64_t decode_slice = 4;  // frames per decode launch group (tool flag)
     int64_t launches = 0;
     bool use_graphs = true;    // replay the denoise+decode body as a CUDA graph
 
+    // Stage arena (see Ledger): sizes of the run's working sets this config
+    // needs, in bytes (for reports and tests).
+    struct ArenaInfo {
+        int64_t arena = 0, act = 0, cache = 0, dec = 0, enc = 0;
+        bool dec_overlaps_cache = false;
+    };
+    ArenaInfo arena_info() const { return arena_info_; }
+
 private:
+    // Decode workspace: per-stage activations of one slice of G frames, the
+    // first conv's patch rows and the tap-to-N partial sums (fallback path).
+    struct DecWs {
+        Act act[8];
+        Act patch;
+        float* y = nullptr;
+        int G = 0;
+    };
+    DecWs dec_ws_run_;              // carved from the arena (runs)
+    DecWs dec_ws_op_;               // operator-level decode / decode_sharded
+    std::vector<DevBuf> dec_bufs_op_;
+    const DecWs* dec_ws_ = nullptr;  // the workspace decode_dev uses
+    void ensure_op_dec_ws(int G);
+    int64_t dec_ws_bytes(int G, bool want_y) const;
+    DevBuf arena_;                  // one device allocation for every per-run working set
+    ArenaInfo arena_info_;
+    int64_t arena_G_ = -1;
+    bool act_padding_ = false, dec_padding_ = false, enc_padding_ = false;
+    uint64_t rid_act_ = 0, rid_dec_ = 0, rid_enc_ = 0, rid_cache_[2] = {0, 0};
     struct Level {
         Act D;     // skip output of d_i
         Act P;     // pooled input of d_i (i >= 1) / mid
@@ -252,13 +305,18 @@ private:
     bool async_pending_ = false;
     bool host_valid_ = false;  // the pinned host copy equals the device cache (clean entries)
     RunStats last_async_;
+    RunStats last_stats_;  // the last completed run (typed RunResult, lc_run_result)
     void ensure_buf(DevBuf* b, int64_t bytes);  // grow-only scratch (invalidates the graph when it grows)
     // seam: 0 no swap, 1 await the prefetch at the seam, 2 await + evict
     // (last consumer), 3 full step with swap (record the cache-ready event
     // after the U_{m+1} producer).  stacked: x_dev holds the explicit (2,T,...) CFG
     // stack instead of the b=1 latent.
+    // fuse (nullable): the sampler step of this denoising step; when the
+    // head runs as K8 it applies it in its epilogue (eps never reaches HBM)
+    // and step_fused_ is set, otherwise eps2_dev is written.
     void forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t timestep, bool full,
-                     float* eps2_dev, int step, int seam);
+                     float* eps2_dev, int step, int seam, const StepArgs* fuse = nullptr);
+    bool step_fused_ = false;
     void conv_block(int j, const Act& in, const Act& out, float s, float o, bool silu);
     void up_block(int i, const Act& skip, const Act& u, const Act& out, float s, float o);
     void decode_dev(const float* lat_dev, int64_t n, float* video_dev);
@@ -271,6 +329,8 @@ private:
     RunConfig cfg_;
     bool configured_ = false;
     std::string cfg_key_;
+    std::string cfg_prev_mode_;       // arena layout depends on these too
+    bool cfg_prev_sliced_ = true;
     Ledger ledger_;
     UNetWeights uw_;
     CodecWeights cw_;
@@ -282,7 +342,7 @@ private:
     // tap-to-N forms of the thin-output convs: 1x1 GEMM over (tap, channel)
     // columns + a gather kernel (launch_tap_gather / launch_subpix_gather)
     std::unique_ptr<TcLayer> head_tap_tc_, dec_last_tap_tc_;
-    DevBuf head_wsum_, head_bias_, dec_last_bias_, head_y_buf_, dec_y_buf_;
+    DevBuf head_wsum_, head_bias_, dec_last_bias_, head_y_buf_;
     DevBuf dec_last_w16_, head_w16_;  // K8 tap banks, fp16 [N][kb*64]
     int dec_last_kb_ = 0, head_kb_ = 0, head_n_ = 0;
     float dec_last_wscale_ = 1.0f, head_wscale_ = 1.0f;
@@ -293,27 +353,21 @@ private:
     int enc0_kp_ = 64;
     DevBuf frames_dev_, eps0_dev_;
     std::string img_key_;
-    std::vector<DevBuf> enc_bufs_;
-    Act enc_patch_, enc_e_[8], enc_p_[8];
-    int64_t enc_alloc_ = -1;
+    Act enc_patch_, enc_e_[8], enc_p_[8];  // encode workspace (arena)
     void prepare_image();
     void encode_dev(float* lat_dev);
     int stem_kp_ = 64, dec0_kp_ = 64;
     Act patch_;                          // stem patch rows (2T, h, w, kp)
-    DevBuf patch_buf_, dec_patch_buf_;
-    Act dec_patch_;
     std::vector<std::unique_ptr<TcLayer>> dec_tc_;  // decoder stages 1..S-1
     std::unique_ptr<ThinLayer> dec0_, dec_last_;
+    int64_t run_dec_group() const;  // frames per decoder slice of a run
     std::vector<Level> lv_;
     Act stem_out_, mid_;
     Act cache_;        // U_{m+1} (b=2 stacked: images [0,T) uncond, [T,2T) cond)
     DevBuf cache_buf_, cache_host_;
     std::vector<DevBuf> act_bufs_;
     DevBuf x0_, x_, xn_, eps2_, video_, z_, bad_;
-    std::vector<DevBuf> dec_bufs_;
     int64_t T_alloc_ = -1;
-    int64_t dec_alloc_ = -1;
-    Act dec_act_[8];
 
     cudaStream_t s_compute_ = nullptr, s_d2h_ = nullptr, s_h2d_ = nullptr;
     cudaStream_t s_comm_ = nullptr;  // NCCL gather of decoded slices (decode_sharded)

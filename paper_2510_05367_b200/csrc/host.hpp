@@ -26,7 +26,8 @@ enum Status : int {
 
 struct LcError : std::runtime_error {
     int code;
-    LcError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+    int stage = -1;  // BudgetError: the stage it was raised in (BudgetError::stage, common.hpp:43-46)
+    LcError(int c, const std::string& m, int st = -1) : std::runtime_error(m), code(c), stage(st) {}
 };
 [[noreturn]] inline void throw_config(const std::string& m) { throw LcError(kConfigError, m); }
 [[noreturn]] inline void throw_shape(const std::string& m) { throw LcError(kShapeError, m); }

@@ -255,6 +255,7 @@ __global__ void up2_kernel(const __half* __restrict__ in, __half* __restrict__ o
 // ------------------------------------------------------------ step update
 __global__ void step_kernel(const StepArgs a) {
     pdl_wait();
+    int f = 0;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < a.n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const float eu = a.eps2[i], ec = a.eps2[a.n + i];
@@ -262,8 +263,9 @@ __global__ void step_kernel(const StepArgs a) {
         float xn = __fadd_rn(__fmul_rn(a.a, a.x[i]), __fmul_rn(a.b, eps));
         if (a.z) xn = __fadd_rn(__fmul_rn(1.0f, xn), __fmul_rn(a.c, a.z[i]));
         a.x_out[i] = xn;
-        if (!isfinite(xn)) atomicOr(a.bad, 1);
+        f |= !isfinite(xn);
     }
+    if (__any_sync(0xffffffffu, f) && (threadIdx.x & 31) == 0) atomicOr(a.bad, 1);
 }
 
 __global__ void linear_kernel(float a, const float* x, float b, const float* y, float* out, int64_t n) {
@@ -273,11 +275,22 @@ __global__ void linear_kernel(float a, const float* x, float b, const float* y, 
         out[i] = __fadd_rn(__fmul_rn(a, x[i]), __fmul_rn(b, y[i]));
 }
 
+// all_finite (tensor.cpp:376): 16-byte loads, a per-thread flag and one
+// warp-wide vote, so the flag word sees at most one atomic per warp.
 __global__ void isfinite_kernel(const float* x, int64_t n, int* bad) {
     pdl_wait();
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        if (!isfinite(x[i])) atomicOr(bad, 1);
+    int f = 0;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    const int64_t n4 = aligned ? n / 4 : 0;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    for (int64_t i = tid; i < n4; i += stride) {
+        const float4 v = __ldg(x4 + i);
+        f |= !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
+    }
+    for (int64_t i = 4 * n4 + tid; i < n; i += stride) f |= !isfinite(x[i]);
+    if (__any_sync(0xffffffffu, f) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
 }
 
 int grid_for(int64_t work, int threads) {
@@ -356,7 +369,7 @@ cudaError_t launch_linear(float a, const float* x, float b, const float* y, floa
 }
 
 cudaError_t launch_isfinite(const float* x, int64_t n, int* bad, cudaStream_t st) {
-    return launch_pdl(isfinite_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, x, n, bad);
+    return launch_pdl(isfinite_kernel, dim3(grid_for((n + 3) / 4, 256)), dim3(256), 0, st, x, n, bad);
 }
 
 }  // namespace lc

@@ -52,9 +52,15 @@ __host__ __device__ constexpr int y_stride(int mode, int C) {
     return mode == kTapSubpix ? (C == 1 ? 20 : C == 2 ? 36 : 52) : (C == 1 ? 12 : C == 2 ? 20 : C == 3 ? 28 : 36);
 }
 __host__ __device__ constexpr int pass_cols(int mode, int C) { return mode == kTapSubpix ? 16 * C : 9 * C; }
+// the fused sampler step keeps e_u of one tile: C x TY x TX floats
+template <int MODE>
+constexpr int eu_bytes() {
+    return MODE == kTapConv3 ? 4 * Geo<MODE>::TY * kTapTX * 4 : 0;
+}
 template <int MODE>
 int smem_bytes(const TapTcParams& p) {
-    return 1024 + kStages * Geo<MODE>::ABytes + p.kb * p.N * 128 + Geo<MODE>::NPix * y_stride(MODE, p.C) * 4 + 512;
+    return 1024 + kStages * Geo<MODE>::ABytes + p.kb * p.N * 128 + Geo<MODE>::NPix * y_stride(MODE, p.C) * 4 +
+           eu_bytes<MODE>() + 512;
 }
 
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&v)[4]) {
@@ -73,7 +79,8 @@ __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_consta
     uint8_t* smA = smem;
     uint8_t* smW = smA + kStages * kABytes;
     float* smY = reinterpret_cast<float*>(smW + p.kb * N * 128);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(smY) + kNPix * YS * 4);
+    float* smEu = smY + kNPix * YS;  // [C][TY][TX] e_u of the pair's first tile (head, pair_T > 0)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(smEu) + eu_bytes<MODE>());
     uint64_t* full_bar = bars;                  // [kStages]
     uint64_t* empty_bar = bars + kStages;       // [kStages]
     uint64_t* tfull = bars + 2 * kStages;       // [2]
@@ -126,12 +133,24 @@ __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_consta
         Y0 = p.win.oy0 + ty * kTapTY;
         X0 = p.win.ox0 + (r - ty * p.tiles_x) * kTapTX;
     };
+    // The CTA's k-th tile (-1: done).  Fused sampler step: unit u = (frame,
+    // tile) of the uncond branch, its two images' tiles back to back.
+    const bool paired = MODE == kTapConv3 && p.pair_T > 0;
+    auto tile_at = [&](int k) -> int {
+        if (!paired) {
+            const int t = static_cast<int>(blockIdx.x) + k * static_cast<int>(gridDim.x);
+            return t < p.num_tiles ? t : -1;
+        }
+        const int u = static_cast<int>(blockIdx.x) + (k >> 1) * static_cast<int>(gridDim.x);
+        if (u >= p.pair_T * tiles_per_img) return -1;
+        return u + (k & 1) * p.pair_T * tiles_per_img;
+    };
 
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer
         if (elect_one()) {
             int it = 0;
-            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            for (int kt = 0, tile; (tile = tile_at(kt)) >= 0; ++kt) {
                 int n, Y0, X0;
                 tile_origin(tile, n, Y0, X0);
                 for (int k = 0; k < p.kb; ++k, ++it) {
@@ -146,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_consta
         // ------------------------------------------------------ MMA issuer
         const uint32_t idesc = umma_idesc_f16(128, static_cast<uint32_t>(N));
         int it = 0, lt = 0;
-        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++lt) {
+        for (; tile_at(lt) >= 0; ++lt) {
             const int buf = lt & 1;
             mbar_wait(&tempty[buf], ((lt >> 1) & 1) ^ 1);
             tc_fence_after();
@@ -184,7 +203,8 @@ __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_consta
         const size_t plane = static_cast<size_t>(OH) * OW;
         constexpr int kTilePx = kTapTY * kTapTX;
         int lt = 0;
-        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x, ++lt) {
+        int bad = 0;
+        for (int tile; (tile = tile_at(lt)) >= 0; ++lt) {
             const int buf = lt & 1;
             int n, Y0, X0;
             tile_origin(tile, n, Y0, X0);
@@ -261,12 +281,28 @@ __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_consta
                             ws += in ? sm_wsum[t * C + c] : 0.f;
                         }
                     }
-                    p.out[(static_cast<size_t>(n) * C + c) * plane + static_cast<size_t>(Y) * OW + X] =
-                        acc + fmaf(p.shift, ws, sm_bias[c]);
+                    const float e = acc + fmaf(p.shift, ws, sm_bias[c]);
+                    if (!paired) {
+                        p.out[(static_cast<size_t>(n) * C + c) * plane + static_cast<size_t>(Y) * OW + X] = e;
+                    } else if (lt & 1) {
+                        // cond branch: cfg_combine then the sampler update
+                        const float eu = smEu[i];
+                        const float eps = __fadd_rn(__fmul_rn(1.0f - p.g, eu), __fmul_rn(p.g, e));
+                        const size_t xi = (static_cast<size_t>(n - p.pair_T) * C + c) * plane +
+                                          static_cast<size_t>(Y) * OW + X;
+                        float xn = __fadd_rn(__fmul_rn(p.a, p.x[xi]), __fmul_rn(p.b, eps));
+                        if (p.z) xn = __fadd_rn(__fmul_rn(1.0f, xn), __fmul_rn(p.c, p.z[xi]));
+                        p.x_out[xi] = xn;
+                        bad |= !isfinite(xn);
+                    } else {
+                        smEu[i] = e;  // uncond branch: kept for the pair's second tile
+                    }
                 }
             }
             named_bar_sync(1, 32 * kEpiWarps);  // shared y is rewritten by the next tile
         }
+        // one flag write per warp (warp-wide vote)
+        if (paired && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.bad, 1);
     }
     tc_fence_before();
     __syncthreads();
@@ -295,7 +331,8 @@ cudaError_t launch_mode(const TapTcParams& p, cudaStream_t st) {
         if (sm[dev] <= 0) sm[dev] = 148;
     }
     const int sms = sm[dev];
-    const int grid = p.num_tiles < sms ? p.num_tiles : sms;
+    const int units = (MODE == kTapConv3 && p.pair_T > 0) ? p.pair_T * p.tiles_x * p.tiles_y : p.num_tiles;
+    const int grid = units < sms ? units : sms;
     return launch_pdl(tap_tc_kernel<MODE>, dim3(grid), dim3(kThreads), static_cast<size_t>(smem_bytes<MODE>(p)), st, p);
 }
 

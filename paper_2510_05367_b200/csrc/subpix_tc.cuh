@@ -36,6 +36,20 @@ struct TapTcParams {
     int n, H, W, C, N, kb;
     Window win;           // head: v* zero-padding window, o* output window (engine.hpp)
     int tiles_x, tiles_y, num_tiles;
+    // head only, pair_T > 0: the sampler step fused into the epilogue
+    // (cfg_combine + reverse_step_*, sampler.cpp:95-133, the rounding order
+    // of kernels.cu step_kernel).  Images n and n + pair_T are the uncond /
+    // cond branches (pipeline.cpp:127-131); a CTA runs the two tiles of one
+    // (frame, tile) pair back to back, keeps e_u in shared memory and writes
+    //   x_out = a*x + b*((1-g)*e_u + g*e_c)  [+ c*z]
+    // instead of eps (which never reaches HBM); non-finite results raise
+    // *bad (the next step's check_input, unet.cpp:134).
+    int pair_T;
+    const float* x;
+    float* x_out;
+    const float* z;  // nullable: ancestral noise
+    float g, a, b, c;
+    int* bad;
 };
 
 // Core tile kTapTX x tap_tile_ty(mode) pixels; the staged window adds a

@@ -12,7 +12,7 @@ run_pipeline on the same config (about 5 min for B, 65 min for C, single
 thread), assert the restatement's video is bit-identical and record
 `video_source = "oracle/_ref"` plus the reference's wall time in the npz.
 
-Usage:  python tests/golden/make_golden.py [small|b0|c0|bvar|pin_b0|pin_c0|pin_bvar|metrics|timelines]...
+Usage:  python tests/golden/make_golden.py [small|b0|c0|bvar|chunkvar|pin_b0|pin_c0|pin_bvar|pin_chunkvar|metrics|timelines]...
 """
 import json
 import os
@@ -52,6 +52,16 @@ BVAR = {
     "b_frame0_ancestral": dict(B0, **{"sampler.kind": "ancestral"}),
     "b_frame0_ddim": dict(B0, **{"sampler.kind": "ddim"}),
     "b_frame0_image": dict(B0, **{"run.mode": "image"}),
+}
+
+
+# halo kinds at the B / C frame-0 shapes (fixed and none halos
+# at the bench shapes; C at 2 steps = one N=2 cache period)
+CHUNKVAR = {
+    "b_frame0_fixed_k5": dict(B0, **{"unet.kernel": 5, "chunk.halo": "fixed", "chunk.halo_px": 1}),
+    "c_frame0_none_s2": dict(C0, **{"sampler.steps": 2, "chunk.halo": "none"}),
+    "c_frame0_fixed_k5_s2": dict(C0, **{"sampler.steps": 2, "unet.kernel": 5, "chunk.halo": "fixed",
+                                        "chunk.halo_px": 1}),
 }
 
 
@@ -205,6 +215,12 @@ if __name__ == "__main__":
         pin("b_frame0", B0)
     if "pin_c0" in what:
         pin("c_frame0", C0)
+    if "chunkvar" in what:
+        for name, over in CHUNKVAR.items():
+            slice0(name, over)
+    if "pin_chunkvar" in what:
+        for name, over in CHUNKVAR.items():
+            pin(name, over)
     if "pin_bvar" in what:
         for name, over in BVAR.items():
             pin(name, over)

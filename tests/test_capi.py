@@ -3,6 +3,8 @@ include/lightcache.h declares (no compute calls here)."""
 import ctypes
 import re
 
+import pytest
+
 import paper_2510_05367_b200 as lc
 
 
@@ -42,3 +44,46 @@ def test_library_is_sm100a():
     import subprocess
     out = subprocess.run(["cuobjdump", "--list-elf", lc.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_integration_doc_embeds_the_compiled_binding():
+    """INTEGRATION.md section 1 shows exactly tools/cpp/pipeline_b200.cpp, the
+    file oracle/Makefile compiles against the reference's headers."""
+    import os
+    root = lc.REPO_ROOT
+    doc = open(os.path.join(root, "INTEGRATION.md")).read()
+    src = open(os.path.join(root, "tools", "cpp", "pipeline_b200.cpp")).read()
+    assert "```cpp\n" + src + "```" in doc
+
+
+@pytest.mark.gpu
+def test_reference_binding_runresult_matches_reference(tmp_path):
+    """The maintainer's binding (tools/cpp/pipeline_b200.cpp, built against
+    /root/reference/proj/include into oracle/_ref/integration_check) returns
+    a typed stagecache::RunResult whose contracts equal the reference's own
+    run_pipeline on the same config: MAC counters, step counts,
+    cache_bytes_planned, the swap timeline's event order (sync mode) and the
+    video within the 1e-3 bar; BudgetError keeps its type and stage."""
+    import json
+    import os
+    import subprocess
+    exe = os.path.join(lc.REPO_ROOT, "oracle", "_ref", "integration_check")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/integration_check not built (reference headers absent at build time)")
+    cfg = tmp_path / "tiny.cfg"
+    cfg.write_text(lc.config_text({"run.frames": 2, "run.height": 32, "run.width": 32, "sampler.steps": 7,
+                                   "cache.n": 3, "swap.mode": "sync"}, base=lc.DEFAULT_CONFIG))
+    r = subprocess.run([exe, str(cfg)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = json.loads(r.stdout)
+    ref, gpu = out["reference"], out["b200"]
+    for k in ("denoiser_macs", "macs_per_full_step", "macs_per_cached_step", "full_steps", "cached_steps",
+              "cache_bytes_planned", "video_elems", "simulated"):
+        assert gpu[k] == ref[k], k
+    assert out["video_rel_l2"] < 1e-3
+    assert [e[:2] for e in gpu["timeline"]] == [e[:2] for e in ref["timeline"]]
+    # transfer bytes: the physical fp16 pre-upsample entry is 1/8 of the
+    # reference's fp32 upsampled one
+    assert [e[2] * 8 for e in gpu["timeline"]] == [e[2] for e in ref["timeline"]]
+    assert gpu["wall"][4] > 0 and gpu["peak"][2][0] > 0 and gpu["event_count"] > 0
+    assert out["budget_error_stage"] in (0, 1, 2, 3)

@@ -101,7 +101,10 @@ def test_cli_run_writes_reference_artifacts(tmp_path):
     occ, peak = {"fast": 0, "slow": 0}, {}
     for row in rows[1:]:
         _, _, kind, tier, nbytes, _, occ_after, stage = row.split(",")
-        occ[tier] += int(nbytes) if kind == "alloc" else (-int(nbytes) if kind == "free" else 0)
+        if kind in ("alloc", "move_start"):  # a move's start row carries the destination tier
+            occ[tier] += int(nbytes)
+        elif kind in ("free", "move_end"):  # its end row the source tier
+            occ[tier] -= int(nbytes)
         assert occ[tier] == int(occ_after)
         peak[(stage, tier)] = max(peak.get((stage, tier), 0), occ[tier])
     assert occ["fast"] == led["current"]["fast_bytes"] and occ["slow"] == led["current"]["slow_bytes"]

@@ -23,6 +23,11 @@ DEFAULT = lc.DEFAULT_CONFIG
 TINY = {"run.frames": 2, "run.height": 32, "run.width": 32, "sampler.steps": 6}
 # Config A: 8 frames, latent 4x32x32, N=3, 2 chunks on u0
 CONFIG_A = {"run.height": 128, "run.width": 128, "cache.n": 3, "chunk.eta": 2, "chunk.omega": 1}
+# configs B and C
+B_SHAPE = {"run.frames": 16, "run.height": 512, "run.width": 512, "codec.stages": 3, "codec.width": 128,
+           "unet.base_channels": 320, "unet.depth": 3, "sampler.steps": 4, "cache.n": 2}
+C_SHAPE = {"run.frames": 25, "run.height": 576, "run.width": 1024, "codec.stages": 3, "codec.width": 128,
+           "unet.base_channels": 320, "unet.depth": 3, "sampler.steps": 25, "cache.n": 2, "swap.mode": "async"}
 
 
 def _kv(over):
@@ -49,6 +54,9 @@ def _run(ctx, over, **kw):
                   "chunk.omega": 2}),
     dict(TINY, **{"unet.kernel": 5}),
     dict(TINY, **{"unet.kernel": 1}),
+    # odd kernels beyond 7x7 (valid in the reference, unet.cpp:139-146)
+    dict(TINY, **{"unet.kernel": 9}),
+    dict(TINY, **{"unet.kernel": 11, "chunk.halo": "fixed", "chunk.halo_px": 2, "sampler.steps": 3}),
     dict(TINY, **{"cache.enabled": "false", "swap.mode": "off"}),
     # image mode: encode stage + forward_noise (pipeline.cpp:108-114)
     dict(TINY, **{"run.mode": "image"}),
@@ -111,10 +119,63 @@ def test_swap_modes_are_bit_identical(ctx):
     assert np.array_equal(vids[0], vids[1]) and np.array_equal(vids[0], vids[2])
 
 
-def test_exact_halo_chunking_is_bit_identical(ctx):
-    a, _, _ = _run(ctx, dict(TINY, **{"chunk.enabled": "false"}))
-    b, _, _ = _run(ctx, dict(TINY, **{"chunk.enabled": "true", "chunk.targets": "stem,d0,d1,d2,u2,u1,u0,head"}))
-    assert np.array_equal(a, b)
+_TILES_CHILD = r"""
+import sys, numpy as np
+import paper_2510_05367_b200 as lc
+over = eval(sys.argv[1])
+ctx = lc.Context(0)
+res = {}
+for tag, chunk in (("tiled", "true"), ("untiled", "false")):
+    text = lc.config_text(dict(over, **{"chunk.enabled": chunk}), base=lc.DEFAULT_CONFIG)
+    ctx.configure(text)
+    v, lat, rep = ctx.run_pipeline(want_latent=True)
+    res[tag + "_v"], res[tag + "_lat"] = v, lat
+    res[tag + "_launches"] = rep["kernel_launches"]
+np.savez(sys.argv[2], **res)
+"""
+
+
+@pytest.mark.parametrize("over", [
+    dict(TINY, **{"chunk.targets": "stem,d0,d1,d2,u2,u1,u0,head"}),
+    dict(TINY, **{"chunk.targets": "u0,head", "chunk.eta": 4, "chunk.omega": 1, "run.height": 64}),
+    # C's frame-0 slice with the bench's chunking (u0 2x2, exact halo)
+    dict(C_SHAPE, **{"run.frames": 1, "sampler.steps": 2}),
+])
+def test_exact_halo_tiles_are_bit_identical(tmp_path, over):
+    """Chunked == unchunked for the lossless (exact) halo, bit for bit
+    (proj/tests/test_unet.cpp:201-220, test_chunk.cpp:211-219), with every
+    tile really run as its own launch over its padded window
+    (LC_FORCE_TILES=1 disables the one-launch collapse of the lossless
+    case)."""
+    import os
+    import subprocess
+    import sys
+    path = str(tmp_path / "tiles.npz")
+    env = dict(os.environ, LC_FORCE_TILES="1")
+    r = subprocess.run([sys.executable, "-c", _TILES_CHILD, repr(over), path], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    o = np.load(path)
+    assert int(o["tiled_launches"]) > int(o["untiled_launches"])  # the tiles really ran separately
+    assert np.array_equal(o["tiled_lat"], o["untiled_lat"])
+    assert np.array_equal(o["tiled_v"], o["untiled_v"])
+
+
+@pytest.mark.parametrize("over", [
+    dict(TINY, **{"chunk.halo": "fixed", "chunk.halo_px": 1, "unet.kernel": 5}),
+    dict(TINY, **{"chunk.halo": "fixed", "chunk.halo_px": 1, "unet.kernel": 5,
+                  "chunk.targets": "stem,d0,u0,head"}),
+    dict(TINY, **{"chunk.halo": "fixed", "chunk.halo_px": 2, "unet.kernel": 7, "chunk.eta": 2, "chunk.omega": 1}),
+    dict(TINY, **{"chunk.halo": "fixed", "chunk.halo_px": 3, "unet.kernel": 3, "chunk.targets": "d1,u1,u0"}),
+])
+def test_fixed_halo_matches_oracle(ctx, oracle, over):
+    """HaloMode::fixed_px (proj/src/chunk.cpp:156-160): a halo below the
+    receptive radius leaves seams; the per-tile windows must reproduce the
+    reference's crop-then-conv values (and above the radius it is lossless)."""
+    video, lat, _ = _run(ctx, over)
+    want_v, want_l = oracle.run_pipeline(_kv(over))
+    assert lc.rel_l2(lat, want_l) < TOL
+    assert lc.rel_l2(video, want_v) < TOL
 
 
 def test_cache_off_equals_n1(ctx):
@@ -277,20 +338,26 @@ def _gold(name):
     return np.load(os.path.join(os.path.dirname(__file__), "golden", f"{name}.npz"))
 
 
-B_SHAPE = {"run.frames": 16, "run.height": 512, "run.width": 512, "codec.stages": 3, "codec.width": 128,
-           "unet.base_channels": 320, "unet.depth": 3, "sampler.steps": 4, "cache.n": 2}
-C_SHAPE = {"run.frames": 25, "run.height": 576, "run.width": 1024, "codec.stages": 3, "codec.width": 128,
-           "unet.base_channels": 320, "unet.depth": 3, "sampler.steps": 25, "cache.n": 2, "swap.mode": "async"}
 
 
-@pytest.mark.parametrize("name,shape", [("b_frame0", B_SHAPE), ("c_frame0", C_SHAPE)])
-def test_frame0_slice_matches_reference(ctx, name, shape):
-    """frame 0 of a T-frame run equals the T=1 run; the
-    golden T=1 run comes from the oracle pinned to the reference."""
+FRAME0_GOLDENS = ["b_frame0", "c_frame0", "b_frame0_ancestral", "b_frame0_ddim", "b_frame0_image",
+                  "b_frame0_fixed_k5", "c_frame0_none_s2", "c_frame0_fixed_k5_s2"]
+
+
+@pytest.mark.parametrize("name", FRAME0_GOLDENS)
+def test_frame0_slice_matches_reference(ctx, name):
+    """frame 0 of a T-frame run equals the T=1 run.
+    The golden T=1 runs at the B / C shapes (Euler, DDIM, ancestral, image
+    mode, fixed and none halos) hold the reference's own video
+    (oracle/_ref run_pipeline, video_source) and the final latent of the
+    restatement whose video is bit-identical to it (make_golden.py pin)."""
     g = _gold(name)
-    video, lat, rep = _run(ctx, dict(shape, **{"run.frames": 1}))
+    ctx.configure(str(g["config"]))
+    video, lat, rep = ctx.run_pipeline(want_latent=True)
     assert lc.rel_l2(lat, g["latent"]) < TOL
     assert lc.rel_l2(video, g["video"]) < TOL
+    if "macs" in g:  # the reference's own MAC counter (RunResult::denoiser_macs)
+        assert rep["mac"]["denoiser_total"] == int(g["macs"][0])
 
 
 @pytest.mark.parametrize("shape", [B_SHAPE, C_SHAPE])
@@ -317,47 +384,109 @@ def _peaks(rep):
     return {s: rep["peaks"][s]["fast"] for s in ("setup", "encode", "denoise", "decode")}
 
 
+def _fresh_run(over, text_only=False):
+    """One run on a fresh engine (each reference run has a fresh ledger);
+    returns (report, ledger summary, ledger csv)."""
+    from paper_2510_05367_b200 import harness
+    c = lc.Context(0)
+    try:
+        c.configure(lc.config_text(over, base=DEFAULT))
+        rep = c.run_pipeline()[2]
+        return rep, harness.ledger_summary(c), harness.ledger_csv(c)
+    finally:
+        c.close()
+
+
+# decode-dominated geometry (codec width 128 on a base-8 U-Net): the
+# unsliced decode workspace exceeds the denoise working set, as in the
+# reference's C10 setting
+DEC_HEAVY = dict(TINY, **{"run.frames": 12, "codec.width": 128})
+
+
 def test_budget_split_aborts_in_decode():
-    """Acceptance C10 (proj/tests/acceptance_main.cpp:447-478) on the
-    physical HBM ledger: a fast-tier budget between the sliced run's
-    overall peak and the unsliced decode peak lets the sliced run through
-    and aborts the unsliced one in the decode stage (each run on a fresh
-    engine, as each reference run has a fresh ledger)."""
-    over = dict(TINY, **{"run.frames": 12, "swap.mode": "sync"})
-
-    def fresh_run(extra):
-        c = lc.Context(0)
-        try:
-            c.configure(lc.config_text(dict(over, **extra), base=DEFAULT))
-            return c.run_pipeline()[2]
-        finally:
-            c.close()
-
-    opt, fat = fresh_run({}), fresh_run({"decode.sliced": "false"})
+    """Acceptance C10 (proj/tests/acceptance_main.cpp:447-478) on the HBM
+    ledger: a fast-tier budget between the sliced run's overall peak and the
+    unsliced decode peak lets the sliced run through and aborts the unsliced
+    one in the decode stage."""
+    over = dict(DEC_HEAVY, **{"swap.mode": "sync"})
+    opt = _fresh_run(over)[0]
+    fat = _fresh_run(dict(over, **{"decode.sliced": "false"}))[0]
     opt_peak = max(_peaks(opt).values())
     fat_decode = _peaks(fat)["decode"]
     assert fat_decode > opt_peak
     budget = (opt_peak + fat_decode) // 2
-    fresh_run({"budget.fast_bytes": budget})
+    _fresh_run(dict(over, **{"budget.fast_bytes": budget}))
     with pytest.raises(lc.BudgetError, match="stage decode"):
-        fresh_run({"decode.sliced": "false", "budget.fast_bytes": budget})
+        _fresh_run(dict(over, **{"decode.sliced": "false", "budget.fast_bytes": budget}))
 
 
-def test_slicing_changes_only_the_decode_peak(ctx):
+def test_slicing_changes_only_the_decode_peak():
     """Acceptance C6's slicing row (acceptance_main.cpp:322-327): -slicing
-    raises the decode peak and leaves the denoise peak alone."""
-    over = dict(TINY, **{"run.frames": 12})
-    c1, c2 = lc.Context(0), lc.Context(0)
-    try:
-        c1.configure(lc.config_text(over, base=DEFAULT))
-        _, _, on = c1.run_pipeline()
-        c2.configure(lc.config_text(dict(over, **{"decode.sliced": "false"}), base=DEFAULT))
-        _, _, off = c2.run_pipeline()
-    finally:
-        c1.close()
-        c2.close()
+    raises the decode peak, leaves the denoise peak alone and (decode-heavy
+    geometry) becomes the dominant stage of its row."""
+    on = _fresh_run(dict(DEC_HEAVY, **{"swap.mode": "sync"}))[0]
+    off = _fresh_run(dict(DEC_HEAVY, **{"swap.mode": "sync", "decode.sliced": "false"}))[0]
     assert _peaks(off)["decode"] > _peaks(on)["decode"]
     assert _peaks(off)["denoise"] == _peaks(on)["denoise"]
+    assert _peaks(off)["decode"] > _peaks(off)["denoise"]
+
+
+def test_swapping_row_frees_the_cache_in_decode():
+    """Acceptance C6's -swapping row (acceptance_main.cpp:329-331) on the
+    physical ledger: with the swap the final eviction leaves the entries on
+    the host through decode (proj/README.md "Swap schedule"), so the decode
+    peak is lower by exactly the physical cache bytes; without it they stay
+    in HBM until the store's teardown.  The denoise peak does not move: the
+    cache is the producing activation U_{m+1} itself (0 extra bytes, C5
+    below), so there is no resident copy for the swap to free in denoise."""
+    on = _fresh_run(dict(TINY, **{"swap.mode": "sync"}))[0]
+    off = _fresh_run(dict(TINY, **{"swap.mode": "off"}))[0]
+    cache = on["cache_bytes_physical"]
+    assert cache > 0
+    assert _peaks(off)["decode"] - _peaks(on)["decode"] == cache
+    assert _peaks(off)["denoise"] == _peaks(on)["denoise"]
+
+
+def test_cache_memory_arithmetic():
+    """Acceptance C5 (acceptance_main.cpp:276-305) on the physical ledger:
+    cache-on minus cache-off denoise peak.  The reference's logical model
+    pays cache_bytes for the retained entries; here the entries ARE the
+    U_{m+1} activation of the full step (fp16, pre-upsample), so the delta is
+    0 <= one in-flight entry, with and without swapping."""
+    off = _fresh_run(dict(TINY, **{"cache.enabled": "false", "swap.mode": "off"}))[0]
+    on = _fresh_run(dict(TINY, **{"swap.mode": "off"}))[0]
+    swp = _fresh_run(dict(TINY, **{"swap.mode": "sync"}))[0]
+    entry = on["cache_bytes_physical"] // 2
+    assert _peaks(on)["denoise"] - _peaks(off)["denoise"] == 0
+    assert _peaks(swp)["denoise"] - _peaks(off)["denoise"] <= entry
+
+
+@pytest.mark.parametrize("over", [TINY, dict(TINY, **{"run.mode": "image"}), dict(DEC_HEAVY, **{"decode.sliced": "false"}),
+                                  dict(TINY, **{"swap.mode": "off"})])
+def test_ledger_peak_is_the_physical_arena(over):
+    """The per-run working sets live in one device arena sized to the peak
+    of their logged lifetimes: the ledger's overall fast peak minus the
+    persistent buffers equals the arena, and the tier moves of the swap
+    show double residency (destination up at move_start, source down only
+    at move_end, ledger.cpp:93-123) and balance out."""
+    rep, summ, csv = _fresh_run(over)
+    arena = rep["arena"]["bytes"]
+    assert summ["overall"]["fast_peak_bytes"] - summ["current"]["fast_bytes"] == arena
+    rows = [r.split(",") for r in csv.splitlines()[1:]]
+    moves = [r for r in rows if r[2] in ("move_start", "move_end")]
+    swapping = over.get("swap.mode", "async") != "off"
+    assert bool(moves) == swapping
+    occ = {"fast": 0, "slow": 0}
+    for r in rows:
+        kind, tier, b = r[2], r[3], int(r[4])
+        if kind in ("alloc", "move_start"):
+            occ[tier] += b
+        elif kind in ("free", "move_end"):
+            occ[tier] -= b
+        assert int(r[6]) == occ[tier]
+    for a, b in zip(moves[::2], moves[1::2]):
+        assert a[2] == "move_start" and b[2] == "move_end" and a[5] == b[5] and a[3] != b[3]
+    assert occ["slow"] == 0  # teardown: every entry left the host tier
 
 
 # ------------------------------------------ randomised configurations
@@ -382,7 +511,8 @@ def _random_configs(k=16, seed=2024):
             "cache.n": int(rng.integers(1, 4)),
             "swap.mode": str(rng.choice(["off", "sync", "async"])),
             "chunk.enabled": str(rng.choice(["true", "false"])),
-            "chunk.halo": str(rng.choice(["exact", "none"])),
+            "chunk.halo": str(rng.choice(["exact", "none", "fixed"])),
+            "chunk.halo_px": int(rng.integers(0, 3)),
             "chunk.eta": int(rng.choice([1, 2])), "chunk.omega": int(rng.choice([1, 2])),
             "chunk.targets": str(rng.choice(["u0", "stem,u0", "d0,u0,head"])),
             "decode.sliced": str(rng.choice(["true", "false"])),
@@ -435,6 +565,34 @@ def test_fused_tap_kernel_matches_gemm_plus_gather(tmp_path, over):
     for fused in ("1", "0"):
         path = str(tmp_path / f"k8_{fused}.npz")
         env = dict(os.environ, LC_SUBPIX_FUSED=fused)
+        r = subprocess.run([sys.executable, "-c", _K8_CHILD, repr(over), path], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0]["lat"], outs[1]["lat"])
+    assert np.array_equal(outs[0]["v"], outs[1]["v"])
+
+
+@pytest.mark.parametrize("over", [
+    TINY,
+    dict(TINY, **{"sampler.kind": "ancestral", "sampler.steps": 4}),
+    dict(TINY, **{"sampler.kind": "ddim", "run.frames": 3}),
+    # head chunk windows (each output pixel updated by exactly one launch)
+    dict(TINY, **{"run.height": 64, "run.width": 96, "sampler.steps": 3, "chunk.halo": "none",
+                  "chunk.targets": "stem,u0,head", "chunk.eta": 2, "chunk.omega": 3}),
+])
+def test_fused_sampler_step_is_bit_identical(tmp_path, over):
+    """The CFG combine + Euler / DDIM / ancestral update applied in the K8
+    head's epilogue (csrc/subpix_tc.cu, the tiles of both branches of a
+    frame on one CTA) equals the separate step kernel (LC_FUSED_STEP=0) bit
+    for bit: same eps values, same two-rounding order."""
+    import os
+    import subprocess
+    import sys
+    outs = []
+    for fused in ("1", "0"):
+        path = str(tmp_path / f"fs_{fused}.npz")
+        env = dict(os.environ, LC_FUSED_STEP=fused)
         r = subprocess.run([sys.executable, "-c", _K8_CHILD, repr(over), path], env=env, capture_output=True,
                            text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
