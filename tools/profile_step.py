@@ -8,7 +8,8 @@ over = bench.WORKLOADS[wl]
 text = lc.config_text(over, base=lc.DEFAULT_CONFIG)
 ctx = lc.Context(0)
 ctx.configure(text)
-ctx.set_decode_slice(4)
+T = int(over.get("run.frames", 8))
+ctx.set_decode_slice(2 if wl == "A" else max(d for d in range(1, 6) if T % d == 0))  # bench.py's default
 kv = lc.parse_config(text)
 n = ctx.latent_elems()
 ctx.upload_latent(lc.randn(lc.derive_seed(int(kv["run.seed"]), 1), n))
