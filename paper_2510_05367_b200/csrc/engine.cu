@@ -2039,6 +2039,7 @@ void Engine::enqueue_body(RunStats& st) {
         dl_fired_ = false;
     }
     host_valid_ = false;
+    body_enqueued_ = true;
     // regions a previous body left behind (an exception mid-enqueue, e.g.
     // BudgetError) are released so occupancy does not drift
     for (uint64_t* id : {&rid_act_, &rid_dec_, &rid_enc_, &rid_cache_[0], &rid_cache_[1]})
@@ -2188,6 +2189,10 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
     const int64_t T = cfg_.frames;
     alloc_activations(T);
     ledger_.budget_fast = cfg_.budget_fast_bytes;
+    // per-run peaks, as each reference run has a fresh ledger
+    // (pipeline.cpp:69); the persistent buffers are the starting occupancy
+    for (int s = 0; s < 4; ++s)
+        for (int t = 0; t < 2; ++t) ledger_.peak[s][t] = ledger_.occ[t];
     if (cfg_.budget_fast_bytes > 0 && ledger_.occ[0] > cfg_.budget_fast_bytes)
         throw LcError(kBudgetError,
                       "fast-tier budget exceeded in stage denoise: " + std::to_string(ledger_.occ[0]) + " > " +
@@ -2409,6 +2414,13 @@ RunStats Engine::finish_run(RunStats st, float* video_host, float* latent_host) 
                                        (lw >> cfg_.cache_depth) * 4
                                  : 0;
     st.cache_bytes_physical = cfg_.cache_enabled ? cache_.elems() * 2 : 0;
+    // A graph replay logs no ledger events (the body was not enqueued on the
+    // host): its peaks are those of the run that enqueued / captured it.
+    if (body_enqueued_) std::memcpy(body_peak_, ledger_.peak, sizeof(body_peak_));
+    else
+        for (int s = 0; s < 4; ++s)
+            for (int t = 0; t < 2; ++t) ledger_.peak[s][t] = std::max(ledger_.peak[s][t], body_peak_[s][t]);
+    body_enqueued_ = false;
     std::memcpy(st.peak, ledger_.peak, sizeof(st.peak));
     st.hbm_peak = 0;
     for (int s = 0; s < 4; ++s) st.hbm_peak = std::max(st.hbm_peak, ledger_.peak[s][0]);

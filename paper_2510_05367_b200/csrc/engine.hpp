@@ -306,6 +306,8 @@ private:
     bool host_valid_ = false;  // the pinned host copy equals the device cache (clean entries)
     RunStats last_async_;
     RunStats last_stats_;  // the last completed run (typed RunResult, lc_run_result)
+    bool body_enqueued_ = false;  // this run's body was enqueued on the host (eager or capture)
+    int64_t body_peak_[4][2] = {};  // ledger peaks of that run (graph replays report them)
     void ensure_buf(DevBuf* b, int64_t bytes);  // grow-only scratch (invalidates the graph when it grows)
     // seam: 0 no swap, 1 await the prefetch at the seam, 2 await + evict
     // (last consumer), 3 full step with swap (record the cache-ready event
