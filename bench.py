@@ -362,6 +362,13 @@ def swap_summary(rep: dict) -> dict:
             "overlap_frac": 1.0 - stall / xfer_ms if xfer_ms > 0 else None}
 
 
+def _traffic(workload):
+    """Mean DRAM bytes per conv_tc launch of the workload from the round's
+    ncu launch list (tools/conv_traffic.py -> profiles/conv_traffic.json)."""
+    tpath = os.path.join(ROOT, "profiles", "conv_traffic.json")
+    return json.load(open(tpath)).get(workload) if os.path.exists(tpath) else None
+
+
 def workload_config(args, world) -> dict:
     """`config` of the JSON line -- identical for both arms (the reference
     arm times a bounded sample of this same workload, see SAMPLES)."""
@@ -430,10 +437,7 @@ def gpu_arm(args, world, rank, local):
     peak, peak_src = peaks()
     achieved = prof["alg_flops"] / (prof["ms"] / 1000.0) / 1e12 if prof["ms"] > 0 else 0.0
     executed = prof["exec_flops"] / (prof["ms"] / 1000.0) / 1e12 if prof["ms"] > 0 else 0.0
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "conv_traffic.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(args.workload)
+    traffic = _traffic(args.workload)
 
     # ---- uncached GPU anchor: RunConfig::baseline() (config.cpp:148-156)
     base_text = lc.config_text(dict(over, **{"cache.enabled": "false", "chunk.enabled": "false",
@@ -474,7 +478,7 @@ def gpu_arm(args, world, rank, local):
             "uncached": uncached,
             "speedup_vs_uncached": value / uncached["value"],
             "denoise_ms": rep["device_ms"]["denoise"], "decode_ms": rep["device_ms"]["decode"],
-            "swap": swap_summary(rep),
+            "swap": dict(swap_summary(rep), **{"schedule": rep.get("swap_schedule")}),
             "e2e": {"value": e2e, "unit": "frames/s", "h2d_bytes_per_step": n_lat * 4,
                     "d2h_bytes_per_step": n_vid * 4},
             "roofline": {"bound": "tensor", "kernel": "conv_tc_kernel (tcgen05 implicit-GEMM conv)",
@@ -601,7 +605,7 @@ def decode_arm(args, world, rank, local):
             "config": workload_config(args, world), "e2e": d["e2e"],
             "roofline": {"bound": "tensor", "kernel": "conv_tc_kernel (decoder convs)", "achieved": achieved,
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                         "traffic": None, "peak_source": peak_src},
+                         "traffic": _traffic("D"), "peak_source": peak_src},
             "gpu_launches": d["gpu_launches"], "clocks": clk, "video_finite": d["video_finite"],
         }
         if world == 1 and not args.no_cpu_baseline:
@@ -627,7 +631,7 @@ def main():
         args.decode_slice = 2 if args.workload == "A" else max(d for d in range(1, 6) if T % d == 0)
     if args.warmup < 3 and args.impl != "reference":
         args.warmup = 3
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args.gpus))
     world, rank, local = dist_init()
     if args.impl == "reference":

@@ -1020,6 +1020,57 @@ int64_t Engine::latent_elems() const {
 }
 int64_t Engine::video_elems() const { return cfg_.frames * cfg_.image_channels * cfg_.height * cfg_.width; }
 
+// Host-link bandwidth per direction with D2H and H2D concurrent (the swap's
+// evict / prefetch pattern): 64 MB each way on the swap's copy streams,
+// once per device and process.
+double Engine::probe_link_gbs() {
+    static double cached[64] = {};
+    const int dev = device_ >= 0 && device_ < 64 ? device_ : 0;
+    if (cached[dev] > 0) return cached[dev];
+    const size_t bytes = size_t{64} << 20;
+    DevBuf hd = host_alloc(nullptr, 2 * static_cast<int64_t>(bytes));
+    DevBuf dd = dev_alloc(nullptr, 2 * static_cast<int64_t>(bytes), false);
+    char* h = hd.as<char>();
+    char* d = dd.as<char>();
+    cudaEvent_t e[4];
+    for (auto& x : e) LC_CUDA(cudaEventCreate(&x));
+    double best = 0;
+    for (int rep = 0; rep < 3; ++rep) {
+        LC_CUDA(cudaEventRecord(e[0], s_d2h_));
+        LC_CUDA(cudaEventRecord(e[2], s_h2d_));
+        LC_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s_d2h_));
+        LC_CUDA(cudaMemcpyAsync(d + bytes, h + bytes, bytes, cudaMemcpyHostToDevice, s_h2d_));
+        LC_CUDA(cudaEventRecord(e[1], s_d2h_));
+        LC_CUDA(cudaEventRecord(e[3], s_h2d_));
+        LC_CUDA(cudaEventSynchronize(e[1]));
+        LC_CUDA(cudaEventSynchronize(e[3]));
+        float a = 0, b = 0;
+        LC_CUDA(cudaEventElapsedTime(&a, e[0], e[1]));
+        LC_CUDA(cudaEventElapsedTime(&b, e[2], e[3]));
+        if (rep > 0) best = std::max(best, static_cast<double>(bytes) / (std::max(a, b) * 1e-3) / 1e9);
+    }
+    for (auto& x : e) cudaEventDestroy(x);
+    cached[dev] = best;
+    return best;
+}
+
+// The per-branch deep path starts the swap's transfers half a deep path
+// earlier and lets entry 1's eviction start before entry 0's has finished
+// queueing on the link.  Measured on C, same box back to back: 241.4
+// frames/s with it, 239.7 without (42 GB/s link, no cost); on a 32 GB/s
+// host link the whole-batch path left 12 ms of seam stall per video.  On by
+// default (LC_BRANCH_DEEP=0 turns it off); the host link is probed once
+// (reported as swap_schedule.link_gbs_probe) for swaps of >= 32 MB entries.
+void Engine::decide_branch_deep() {
+    branch_deep_ = false;
+    const bool swap_async = cfg_.cache_enabled && cfg_.swap_mode == SwapMode::Async &&
+                            cfg_.cache_depth + 1 < cfg_.depth;
+    if (!swap_async) return;
+    const char* env = std::getenv("LC_BRANCH_DEEP");
+    branch_deep_ = !(env && std::atoi(env) == 0 && env[0] == '0');
+    if (cache_.elems() * 2 >= (int64_t{32} << 20)) link_gbs_ = probe_link_gbs();
+}
+
 int64_t Engine::run_dec_group() const {
     const int64_t T = cfg_.frames;
     return std::max<int64_t>(1, std::min<int64_t>(cfg_.slice_decode ? decode_slice : T, T));
@@ -1158,6 +1209,7 @@ void Engine::alloc_activations(int64_t T) {
         if (cfg_.swap_mode != SwapMode::Off) cache_host_ = host_alloc(nullptr, cache_.elems() * 2);
     }
     arena_info_ = ai;
+    decide_branch_deep();
     const int64_t nl = T * cfg_.latent_channels * lh * lw;
     x0_ = dev_alloc(&ledger_, nl * 4, true);
     x_ = dev_alloc(&ledger_, nl * 4, true);
@@ -1311,8 +1363,17 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
     cond(1, &s, &o);
     dl_gate(step, "d0");
     conv_block(1, stem_out_, lv_[0].D, s, o, true);
+    const bool writes_cache = full && cfg_.cache_enabled;
+    // Per-branch deep path (async swap, full step whose U_{m+1} is evicted,
+    // slow host link -- see branch_deep_wanted): everything below level m
+    // runs on the uncond half, then on the cond half, so entry 0 is complete
+    // (and its eviction starts) half a deep path earlier, and entry 1's
+    // eviction no longer queues behind it on the link.  Same per-image
+    // arithmetic (bit-identical), same transfer issue points.
+    const bool branch_deep = writes_cache && seam == 3 && cfg_.swap_mode == SwapMode::Async && m + 1 < M &&
+                             branch_deep_;
     const int deepest = full ? M - 1 : m;
-    for (int i = 1; i <= deepest; ++i) {
+    for (int i = 1; i <= (branch_deep ? m : deepest); ++i) {
         const Act& prev = lv_[i - 1].D;
         LC_CUDA(launch_down2(prev.p, lv_[i].P.p, prev.n, prev.h, prev.w, prev.cs, s_compute_));
         ++launches;
@@ -1322,7 +1383,6 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
     // U_l holder: output of u_l (l < M) or mid (l == M); the cache slot when
     // l == m+1 and caching is on.
     auto U_of = [&](int l) -> const Act& { return l == M ? mid_ : lv_[l].U; };
-    const bool writes_cache = full && cfg_.cache_enabled;
     if (writes_cache) host_valid_ = false;  // this step stores new entries
     if (writes_cache)
         // CacheStore::store (cache.cpp:43-63) replaces the entries: ones the
@@ -1349,7 +1409,32 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
             if (b < 0 || e == b) LC_CUDA(cudaEventRecord(ev_cache_ready_[e], s_compute_));
         cache_ready_recorded_ = true;
     };
-    if (full) {
+    auto half = [&](const Act& a, int b) {
+        Act h = a;
+        h.n = a.n / 2;
+        h.p = a.p + static_cast<int64_t>(b) * h.n * a.h * a.w * a.cs;
+        return h;
+    };
+    if (branch_deep) {
+        for (int b = 0; b < 2; ++b) {
+            for (int i = m + 1; i <= M; ++i) {
+                const Act prev = half(lv_[i - 1].D, b);
+                const Act pin = half(lv_[i].P, b);
+                LC_CUDA(launch_down2(prev.p, pin.p, prev.n, prev.h, prev.w, prev.cs, s_compute_));
+                ++launches;
+                cond(1 + i, &s, &o);
+                conv_block(1 + i, pin, half(i == M ? mid_ : lv_[i].D, b), s, o, true);
+            }
+            for (int i = M - 1; i >= m + 1; --i) {
+                const int j = static_cast<int>(block_index(cfg_, "u" + std::to_string(i)));
+                cond(j, &s, &o);
+                if (i == m + 1) await_store(b);
+                up_block(i, half(lv_[i].D, b), half(U_of(i + 1), b), half(U_of(i), b), s, o);
+            }
+            cache_ready(b);
+        }
+    }
+    if (full && !branch_deep) {
         const Act& prev = lv_[M - 1].D;
         LC_CUDA(launch_down2(prev.p, lv_[M].P.p, prev.n, prev.h, prev.w, prev.cs, s_compute_));
         ++launches;
@@ -1369,12 +1454,6 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
         // last consumer: evict_all right after assemble (pipeline.cpp:156-160)
         if (seam == 2) issue_evict(step);
     }
-    auto half = [&](const Act& a, int b) {
-        Act h = a;
-        h.n = a.n / 2;
-        h.p = a.p + static_cast<int64_t>(b) * h.n * a.h * a.w * a.cs;
-        return h;
-    };
     const int top = full ? M - 1 : m;
     dl_gate(step, "up");
     // Per-branch store (async swap, full step whose U_{m+1} is evicted): the
@@ -1383,10 +1462,10 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
     // cond half.  Same per-image arithmetic (bit-identical), same transfer
     // issue points.
     const bool split_store = writes_cache && seam == 3 && cfg_.swap_mode == SwapMode::Async && m + 1 < M &&
-                             split_store_enabled();
+                             split_store_enabled() && !branch_deep;
     // Deeper up blocks stay whole-batch (their weight panels, up to 170 MB,
     // would be streamed twice); only the producing block u_{m+1} is split.
-    int first = top;
+    int first = branch_deep ? m : top;
     if (split_store) {
         for (int i = top; i > m + 1; --i) {
             const int j = static_cast<int>(block_index(cfg_, "u" + std::to_string(i)));

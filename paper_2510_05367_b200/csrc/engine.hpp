@@ -270,6 +270,8 @@ public:
         bool dec_overlaps_cache = false;
     };
     ArenaInfo arena_info() const { return arena_info_; }
+    double link_gbs() const { return link_gbs_; }  // host-link probe (GB/s per direction, 0 = not probed)
+    bool branch_deep() const { return branch_deep_; }
 
 private:
     // Decode workspace: per-stage activations of one slice of G frames, the
@@ -288,6 +290,7 @@ private:
     int64_t dec_ws_bytes(int G, bool want_y) const;
     DevBuf arena_;                  // one device allocation for every per-run working set
     ArenaInfo arena_info_;
+    double link_gbs_ = 0;
     int64_t arena_G_ = -1;
     bool act_padding_ = false, dec_padding_ = false, enc_padding_ = false;
     uint64_t rid_act_ = 0, rid_dec_ = 0, rid_enc_ = 0, rid_cache_[2] = {0, 0};
@@ -319,6 +322,11 @@ private:
     void forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t timestep, bool full,
                      float* eps2_dev, int step, int seam, const StepArgs* fuse = nullptr);
     bool step_fused_ = false;
+    // per-branch deep path in full steps that evict (forward_dev): chosen
+    // from the measured host-link bandwidth (LC_BRANCH_DEEP=0/1 forces it)
+    bool branch_deep_ = false;
+    void decide_branch_deep();
+    double probe_link_gbs();
     void conv_block(int j, const Act& in, const Act& out, float s, float o, bool silu);
     void up_block(int i, const Act& skip, const Act& u, const Act& out, float s, float o);
     void decode_dev(const float* lat_dev, int64_t n, float* video_dev);

@@ -601,6 +601,32 @@ def test_fused_sampler_step_is_bit_identical(tmp_path, over):
     assert np.array_equal(outs[0]["v"], outs[1]["v"])
 
 
+@pytest.mark.parametrize("over", [
+    TINY,
+    dict(TINY, **{"unet.cache_depth": 1, "sampler.steps": 5}),
+    dict(TINY, **{"sampler.kind": "ancestral", "cache.n": 3, "sampler.steps": 7}),
+    dict(TINY, **{"chunk.targets": "d1,u1,u0", "chunk.halo": "none"}),
+])
+def test_branch_deep_path_is_bit_identical(tmp_path, over):
+    """The per-branch deep path of evicting full steps (forward_dev,
+    chosen on slow host links) runs the same per-image arithmetic as the
+    whole-batch path: bit-identical latents and videos (LC_BRANCH_DEEP=1
+    vs 0)."""
+    import os
+    import subprocess
+    import sys
+    outs = []
+    for bd in ("1", "0"):
+        path = str(tmp_path / f"bd_{bd}.npz")
+        env = dict(os.environ, LC_BRANCH_DEEP=bd)
+        r = subprocess.run([sys.executable, "-c", _K8_CHILD, repr(over), path], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0]["lat"], outs[1]["lat"])
+    assert np.array_equal(outs[0]["v"], outs[1]["v"])
+
+
 _HALO_CHILD = r"""
 import sys, numpy as np
 import paper_2510_05367_b200 as lc

@@ -41,6 +41,17 @@ if os.path.exists(src):
         "absolute sums are not)\n" + out)
     out = run([sys.executable, os.path.join(ROOT, "tools", "membound_report.py"), src, "2"])
     open(os.path.join(P, f"membound_c_{rnd}.txt"), "w").write(out)
+src = os.path.join(G, "launch_d.csv")
+if os.path.exists(src):
+    shutil.copy(src, os.path.join(P, f"ncu_launches_d_{rnd}.csv"))
+    print(run([sys.executable, os.path.join(ROOT, "tools", "conv_traffic.py"), src, "D", "2"]))
+    out = run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), src, "2", "-v"])
+    open(os.path.join(P, f"ncu_launches_d_{rnd}.txt"), "w").write(
+        "# ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none "
+        "python tools/profile_step.py D 2\n" + out)
+src = os.path.join(G, "launch_c.csv")
+if os.path.exists(src):
+    print(run([sys.executable, os.path.join(ROOT, "tools", "conv_traffic.py"), src, "C", "2"]))
 KEEP = ("sm__pipe_tc_cycles_active.avg.pct", "sm__pipe_tensor_cycles_active.avg.pct", "dram__bytes_read.sum",
         "dram__bytes_write.sum", "gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "lts__t_bytes.sum",
         "smsp__average_warps_issue_stalled_", "sm__throughput.avg.pct_of_peak_sustained_elapsed",

@@ -30,3 +30,6 @@ ncu --set full --clock-control none --import-source on -k regex:tap_tc --launch-
 python tools/layer_report.py C gpurun_out/layers_c.json > gpurun_out/layers_c.txt 2>&1
 python tools/swap_timeline.py C > gpurun_out/swap_timeline_c.txt 2>&1
 ls -la gpurun_out
+# D: launch list with DRAM bytes (conv traffic per launch for bench's roofline.traffic)
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+    --log-file gpurun_out/launch_d.csv python tools/profile_step.py D 2 > gpurun_out/ncu_d.log 2>&1
