@@ -1448,7 +1448,10 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
     // so the seam block starts on the uncond half as soon as that entry has
     // landed and overlaps the cond entry's transfer.  Same bytes, same order
     // of awaits and issue points as assemble() + evict_all().
-    const bool branch_seam = !full && seam > 0 && prefetch_pending_ && cfg_.swap_mode == SwapMode::Async;
+    static const bool branch_seam_on =
+        !(std::getenv("LC_BRANCH_SEAM") && std::atoi(std::getenv("LC_BRANCH_SEAM")) == 0);
+    const bool branch_seam =
+        !full && seam > 0 && prefetch_pending_ && cfg_.swap_mode == SwapMode::Async && branch_seam_on;
     if (!full && seam > 0 && !branch_seam) {
         seam_await(step);
         // last consumer: evict_all right after assemble (pipeline.cpp:156-160)
