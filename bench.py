@@ -458,7 +458,7 @@ def gpu_arm(args, world, rank, local):
     vid.free()
     ctx.close()
 
-    sharded = decode_sharded_leg(args, world, rank, local) if world > 1 else None
+    sharded = decode_sharded_leg(args, world, rank, local) if world > 1 and not args.plumbing_test else None
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -625,6 +625,9 @@ def main():
                     help="frames per decoder slice (default: config A's 4 slices of 2 frames; otherwise the "
                          "largest divisor of the frame count <= 5: B 4, C/D 5 -- even slices, no 1-frame tail)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--plumbing-test", action="store_true",
+                    help="(testing only) every rank on GPU 0 and no NCCL leg: exercises the N > 1 host plumbing "
+                         "(spawn, barriers, max over ranks) on a one-GPU box; not a measurement")
     args = ap.parse_args()
     if args.decode_slice is None:
         T = int(WORKLOADS[args.workload].get("run.frames", 8))
@@ -634,6 +637,8 @@ def main():
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(spawn_ranks(args.gpus))
     world, rank, local = dist_init()
+    if args.plumbing_test:
+        local = 0
     if args.impl == "reference":
         reference_arm(args, world, rank)
     elif args.workload == "D":

@@ -495,7 +495,10 @@ class SharedVideo:
             lib().lc_host_unregister(self.ptr)
             self.ptr = None
             self.array = None
-            self.shm.close()
+            try:
+                self.shm.close()
+            except BufferError:  # a caller still holds a view of the video: unmapped at exit
+                pass
             if self._owner:
                 self.shm.unlink()
 

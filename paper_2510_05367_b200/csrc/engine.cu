@@ -533,6 +533,40 @@ Bank subpix_tap_bank(const Bank& b) {
     return t;
 }
 
+// K8 decoder operand (row-summed sub-pixel form): rows (py, px, dx, c) --
+// ((py*2 + px)*2 + dx)*C + c -- and K blocks (o, channel block) with o the
+// window-row offset dy + py of the merged 2x2 tap (dy = o - py in {0, 1},
+// zero otherwise), fp16 times the power-of-two scale of the tap bank
+// (fan_in = c_in), padded to [round_up(8C, 16)][3 * kb * 64].
+DevBuf pack_rowsum_w16(Ledger* l, const Bank& b, int* kb_out, int* n_out, float* wscale_out) {
+    if (b.k != 3 || b.c_out > 4) throw_invariant("row-summed sub-pixel bank needs k == 3, c_out <= 4");
+    const Bank t = subpix_tap_bank(b);  // rows (p*4 + tp)*C + c, tp = dy*2 + dx
+    const int C = static_cast<int>(b.c_out), kb = static_cast<int>((b.c_in + 63) / 64);
+    const int n = (8 * C + 15) / 16 * 16, kp = 3 * kb * 64;
+    const float wscale = std::ldexp(1.0f, static_cast<int>(std::lround(0.5 * std::log2(static_cast<double>(b.c_in)))));
+    std::vector<__half> w16(static_cast<size_t>(n) * kp, __float2half_rn(0.0f));
+    for (int py = 0; py < 2; ++py)
+        for (int px = 0; px < 2; ++px)
+            for (int dx = 0; dx < 2; ++dx)
+                for (int c = 0; c < C; ++c) {
+                    const int row = ((py * 2 + px) * 2 + dx) * C + c;
+                    for (int o = 0; o < 3; ++o) {
+                        const int dy = o - py;
+                        if (dy < 0 || dy > 1) continue;
+                        const int trow = ((py * 2 + px) * 4 + dy * 2 + dx) * C + c;
+                        for (int64_t ic = 0; ic < b.c_in; ++ic)
+                            w16[static_cast<size_t>(row) * kp + o * kb * 64 + ic] =
+                                __float2half_rn(t.taps[static_cast<size_t>(trow * t.c_in + ic)] * wscale);
+                    }
+                }
+    *wscale_out = wscale;
+    DevBuf buf = dev_alloc(l, static_cast<int64_t>(w16.size() * 2), false);
+    h2d_blocking(buf.p, w16.data(), w16.size() * 2);
+    *kb_out = kb;
+    *n_out = n;
+    return buf;
+}
+
 Bank subpixel_shuffle_bank(const Bank& b) {
     if (b.k != 3) throw_invariant("sub-pixel shuffle needs k == 3");
     Bank s;
@@ -972,10 +1006,9 @@ void Engine::configure(const RunConfig& cfg) {
             if (db.k == 3 && db.c_out <= 4) {
                 const Bank tb = subpix_tap_bank(db);
                 dec_last_tap_tc_ = pack_tc_layer(&ledger_, tb, static_cast<int>(db.c_in), 0);
-                if (tap_tc_supported(kTapSubpix, static_cast<int>(db.c_out), static_cast<int>((tb.c_in + 63) / 64),
-                                     static_cast<int>((tb.c_out + 15) / 16 * 16))) {
-                    int nn = 0;
-                    dec_last_w16_ = pack_tap_w16(&ledger_, tb, &dec_last_kb_, &nn, &dec_last_wscale_);
+                if (tap_tc_supported(kTapSubpix, static_cast<int>(db.c_out), static_cast<int>((db.c_in + 63) / 64),
+                                     static_cast<int>((8 * db.c_out + 15) / 16 * 16))) {
+                    dec_last_w16_ = pack_rowsum_w16(&ledger_, db, &dec_last_kb_, &dec_last_n_, &dec_last_wscale_);
                 }
                 dec_last_bias_ = dev_alloc(&ledger_, static_cast<int64_t>(db.bias.size() * 4), false);
                 h2d_blocking(dec_last_bias_.p, db.bias.data(), db.bias.size() * 4);
@@ -1864,7 +1897,7 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
             q.H = hl;
             q.W = wl;
             q.C = IC;
-            q.N = 16 * IC;
+            q.N = dec_last_n_;
             q.kb = dec_last_kb_;
             q.win = Window{0, hl, 0, wl, 0, hl, 0, wl};
             q.tiles_x = (wl + kTapTX - 1) / kTapTX;

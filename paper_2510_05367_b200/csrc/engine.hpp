@@ -354,7 +354,7 @@ private:
     std::unique_ptr<TcLayer> head_tap_tc_, dec_last_tap_tc_;
     DevBuf head_wsum_, head_bias_, dec_last_bias_, head_y_buf_;
     DevBuf dec_last_w16_, head_w16_;  // K8 tap banks, fp16 [N][kb*64]
-    int dec_last_kb_ = 0, head_kb_ = 0, head_n_ = 0;
+    int dec_last_kb_ = 0, dec_last_n_ = 0, head_kb_ = 0, head_n_ = 0;
     float dec_last_wscale_ = 1.0f, head_wscale_ = 1.0f;
     DevBuf shard_lat_, shard_vid_;  // decode_sharded buffers
     // encoder (image mode, codec.cpp:64-81): patch GEMM + [down2 + conv]xS

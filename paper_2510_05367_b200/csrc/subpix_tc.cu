@@ -34,12 +34,17 @@ namespace {
 // bank): those rows only feed accumulator rows that are never read.
 template <int MODE> struct Geo {
     static constexpr int TY = tap_tile_ty(MODE), SY = tap_stage_sy(MODE);
-    static constexpr int NPix = kTapSX * SY;                   // decoder 462, head 330
-    static constexpr int MT = (NPix + 127) / 128;              // 4, 3
+    static constexpr int NPix = kTapSX * SY;                   // staged pixels: decoder 462, head 330
+    // GEMM rows: the head multiplies every staged pixel; the decoder only
+    // the TY output rows of the window (its row taps are summed inside the
+    // MMA through row-shifted A descriptors, see the kernel)
+    static constexpr int MRows = MODE == kTapSubpix ? kTapSX * TY : NPix;  // 330, 330
+    static constexpr int MT = (MRows + 127) / 128;             // 3, 3
     static constexpr int ABytes = (NPix * 128 + 1023) / 1024 * 1024;
+    static constexpr int KRep = MODE == kTapSubpix ? 3 : 1;    // weight K blocks per input K block
 };
 constexpr int kStages = 2;
-constexpr int kMaxPC = 48;  // tap columns per staged pixel (decoder 16*3, head 9*4)
+constexpr int kMaxPC = 36;  // tap columns per GEMM row (decoder 8*4, head 9*4)
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 32 * (2 + kEpiWarps);
 constexpr int kAccCols = 256;                    // TMEM columns per accumulator buffer
@@ -49,9 +54,10 @@ constexpr int kSmemMax = 232448;
 // a multiple of 4 whose lane stride spreads 8 consecutive lanes' 16-byte
 // stores over distinct bank quads
 __host__ __device__ constexpr int y_stride(int mode, int C) {
-    return mode == kTapSubpix ? (C == 1 ? 20 : C == 2 ? 36 : 52) : (C == 1 ? 12 : C == 2 ? 20 : C == 3 ? 28 : 36);
+    return mode == kTapSubpix ? (C == 1 ? 12 : C == 2 ? 20 : C == 3 ? 28 : 36) : (C == 1 ? 12 : C == 2 ? 20 : C == 3 ? 28 : 36);
 }
-__host__ __device__ constexpr int pass_cols(int mode, int C) { return mode == kTapSubpix ? 16 * C : 9 * C; }
+// columns per GEMM row: decoder (py, px, dx, c) after the MMA summed dy; head (tap, c)
+__host__ __device__ constexpr int pass_cols(int mode, int C) { return mode == kTapSubpix ? 8 * C : 9 * C; }
 // the fused sampler step keeps e_u of one tile: C x TY x TX floats
 template <int MODE>
 constexpr int eu_bytes() {
@@ -59,8 +65,8 @@ constexpr int eu_bytes() {
 }
 template <int MODE>
 int smem_bytes(const TapTcParams& p) {
-    return 1024 + kStages * Geo<MODE>::ABytes + p.kb * p.N * 128 + Geo<MODE>::NPix * y_stride(MODE, p.C) * 4 +
-           eu_bytes<MODE>() + 512;
+    return 1024 + kStages * Geo<MODE>::ABytes + Geo<MODE>::KRep * p.kb * p.N * 128 +
+           Geo<MODE>::MRows * y_stride(MODE, p.C) * 4 + eu_bytes<MODE>() + 512;
 }
 
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&v)[4]) {
@@ -73,13 +79,14 @@ template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_constant__ TapTcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     constexpr int kNPix = Geo<MODE>::NPix, kMT = Geo<MODE>::MT, kABytes = Geo<MODE>::ABytes;
+    constexpr int kMRows = Geo<MODE>::MRows, kKRep = Geo<MODE>::KRep;
     constexpr int kTapTY = Geo<MODE>::TY;
     const int C = p.C, N = p.N, YS = y_stride(MODE, C), PC = pass_cols(MODE, C);
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* smA = smem;
     uint8_t* smW = smA + kStages * kABytes;
-    float* smY = reinterpret_cast<float*>(smW + p.kb * N * 128);
-    float* smEu = smY + kNPix * YS;  // [C][TY][TX] e_u of the pair's first tile (head, pair_T > 0)
+    float* smY = reinterpret_cast<float*>(smW + kKRep * p.kb * N * 128);
+    float* smEu = smY + kMRows * YS;  // [C][TY][TX] e_u of the pair's first tile (head, pair_T > 0)
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(smEu) + eu_bytes<MODE>());
     uint64_t* full_bar = bars;                  // [kStages]
     uint64_t* empty_bar = bars + kStages;       // [kStages]
@@ -108,10 +115,11 @@ __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_consta
     // tap bank -> shared, K-major rows of 128 B in the 128B-swizzle layout
     // the MMA descriptor expects (16 B chunk j of row r at j ^ (r & 7))
     {
-        const int chunks = p.kb * N * 8;
+        const int wkb = kKRep * p.kb;  // decoder: K blocks ordered (row offset o, channel block)
+        const int chunks = wkb * N * 8;
         for (int i = static_cast<int>(threadIdx.x); i < chunks; i += kThreads) {
             const int k = i / (N * 8), r = (i / 8) % N, j = i % 8;
-            const uint4 v = *reinterpret_cast<const uint4*>(p.w + static_cast<size_t>(r) * (p.kb * 64) + k * 64 + j * 8);
+            const uint4 v = *reinterpret_cast<const uint4*>(p.w + static_cast<size_t>(r) * (wkb * 64) + k * 64 + j * 8);
             sts128u(smem_u32(smW + k * N * 128 + r * 128 + ((j ^ (r & 7)) << 4)), v);
         }
         fence_proxy_async_smem();
@@ -175,13 +183,22 @@ __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_consta
                 mbar_wait(&full_bar[s], (it / kStages) & 1);
                 tc_fence_after();
                 if (elect_one()) {
-                    const uint64_t bdesc = umma_desc_sw128(smem_u32(smW + k * N * 128));
+                    // decoder: one pass per window-row offset o of the output
+                    // rows' taps (dy + py), its A rows shifted by o image rows
+                    // (a 128 B-row start-address shift of the SW128 tile, see
+                    // conv_tc.cu halo staging); the head: o = 0 only
 #pragma unroll
-                    for (int mt = 0; mt < kMT; ++mt) {
-                        const uint64_t adesc = umma_desc_sw128(smem_u32(smA + s * kABytes + mt * 128 * 128));
+                    for (int o = 0; o < kKRep; ++o) {
+                        const uint64_t bdesc = umma_desc_sw128(smem_u32(smW + (o * p.kb + k) * N * 128));
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            umma_f16(d0 + mt * N, adesc + 2 * kk, bdesc + 2 * kk, idesc, (k | kk) != 0 ? 1u : 0u);
+                        for (int mt = 0; mt < kMT; ++mt) {
+                            const uint64_t adesc =
+                                umma_desc_sw128(smem_u32(smA + s * kABytes + (mt * 128 + o * kTapSX) * 128));
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                umma_f16(d0 + mt * N, adesc + 2 * kk, bdesc + 2 * kk, idesc,
+                                         (k | o | kk) != 0 ? 1u : 0u);
+                        }
                     }
                     umma_commit(&empty_bar[s]);
                 }
@@ -220,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_consta
                 for (int j = 0; j < kMaxPC / 4; ++j)
                     if (j < nld) tmem_ld4(ta + 4 * j, *reinterpret_cast<uint32_t(*)[4]>(&v[4 * j]));
                 tmem_ld_wait();
-                if (q < kNPix) {
+                if (q < kMRows) {
 #pragma unroll
                     for (int j = 0; j < kMaxPC / 4; ++j)
                         if (j < nld)
@@ -236,7 +253,8 @@ __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_consta
             if (lane == 0) mbar_arrive(&tempty[buf]);
             named_bar_sync(1, 32 * kEpiWarps);
             if (MODE == kTapSubpix) {
-                // task (c, py, ry, rx): out(2Y+py, 2X+{0,1}) = bias + sum_t y[src(t)][((py*2+px)*4+t)*C + c]
+                // task (c, py, ry, rx): out(2Y+py, 2X+px) = bias + sum_dx y[(ry, rx+px+dx)][((py*2+px)*2+dx)*C + c]
+                // (the row taps dy are already summed by the MMA)
                 for (int i = et; i < kTilePx * 2 * C; i += 32 * kEpiWarps) {
                     const int c = i / (2 * kTilePx);
                     const int r = i - c * 2 * kTilePx;
@@ -247,13 +265,9 @@ __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_consta
                     float o2[2];
 #pragma unroll
                     for (int px = 0; px < 2; ++px) {
-                        float acc = sm_bias[c];
-#pragma unroll
-                        for (int t = 0; t < 4; ++t) {
-                            const int q = (ry + (t >> 1) + py) * kTapSX + rx + (t & 1) + px;
-                            acc += smY[q * YS + ((py * 2 + px) * 4 + t) * C + c];
-                        }
-                        o2[px] = acc;
+                        const int q = ry * kTapSX + rx + px;
+                        const int col = ((py * 2 + px) * 2) * C + c;
+                        o2[px] = sm_bias[c] + smY[q * YS + col] + smY[(q + 1) * YS + col + C];
                     }
                     *reinterpret_cast<float2*>(p.out + (static_cast<size_t>(n) * C + c) * plane +
                                                static_cast<size_t>(2 * Y + py) * OW + 2 * X) = make_float2(o2[0], o2[1]);

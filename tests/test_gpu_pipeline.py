@@ -555,9 +555,12 @@ np.savez(sys.argv[2], v=v, lat=lat)
     dict(TINY, **{"run.height": 64, "run.width": 64, "sampler.steps": 2, "codec.width": 192}),
 ])
 def test_fused_tap_kernel_matches_gemm_plus_gather(tmp_path, over):
-    """K8 (csrc/subpix_tc.cu) sums the same tap products in the same order
-    as the tap-to-N GEMM + gather pair it replaces (LC_SUBPIX_FUSED=0):
-    bit-identical latents and videos, head chunk windows included."""
+    """K8 (csrc/subpix_tc.cu) against the tap-to-N GEMM + gather pair it
+    replaces (LC_SUBPIX_FUSED=0).  The head sums the same tap products in the
+    same order: bit-identical latents, head chunk windows included.  The
+    decoder's last stage sums its two row taps inside the MMA (fp32 tensor
+    core accumulation) instead of in the gather: the videos agree to fp32
+    rounding (relative L2 <= 1e-6, far inside the 1e-3 parity bar)."""
     import os
     import subprocess
     import sys
@@ -570,7 +573,7 @@ def test_fused_tap_kernel_matches_gemm_plus_gather(tmp_path, over):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(path))
     assert np.array_equal(outs[0]["lat"], outs[1]["lat"])
-    assert np.array_equal(outs[0]["v"], outs[1]["v"])
+    assert lc.rel_l2(outs[0]["v"], outs[1]["v"]) <= 1e-6
 
 
 @pytest.mark.parametrize("over", [

@@ -157,3 +157,27 @@ def test_decode_sharded_repeated_calls_and_pinned_buffers(ctx):
     assert np.array_equal(vid, want6)
     lp.free()
     vp.free()
+
+
+@pytest.mark.gpu
+def test_decode_sharded_into_shared_host_video(ctx):
+    """LC_SHARD_HOST_SHARED: the rank writes its frames straight into one
+    page-locked shared-memory video (the multi-rank e2e path of bench.py);
+    at world 1 that is every frame, bit-identical to lc_decode."""
+    import paper_2510_05367_b200 as lc
+    over = dict(TINY, **{"run.frames": 6})
+    ctx.configure(lc.config_text(over, base=lc.DEFAULT_CONFIG))
+    lat = np.random.default_rng(4).standard_normal((1, 6, 4, 8, 8)).astype(np.float32)
+    want = ctx.decode(lat, slice_frames=4)
+    name = f"lc_test_video_{os.getpid()}"
+    shared = lc.SharedVideo(name, want.size, create=True)
+    try:
+        shared.array[:] = np.nan
+        got, ms = ctx.decode_sharded(lat, slice_frames=4, out=shared, host_shared=True)
+        assert ms > 0 and np.array_equal(got, want)
+        # a second mapping of the same segment sees the frames (another rank's view)
+        other = lc.SharedVideo(name, want.size, create=False)
+        assert np.array_equal(other.array.reshape(want.shape), want)
+        other.free()
+    finally:
+        shared.free()
