@@ -1573,7 +1573,8 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
                                       static_cast<uint64_t>(a.n)};
             const uint64_t strides[3] = {static_cast<uint64_t>(a.cs) * 2, static_cast<uint64_t>(lw) * a.cs * 2,
                                          static_cast<uint64_t>(lh) * lw * a.cs * 2};
-            const uint32_t box[4] = {64, kTapSX, static_cast<uint32_t>(tap_stage_sy(kTapConv3)), 1};
+            const int hty = tap_tile_rows(kTapConv3, static_cast<int>(head_tc_->c_out), head_kb_, head_n_);
+            const uint32_t box[4] = {64, kTapSX, static_cast<uint32_t>(hty + 2), 1};
             const uint32_t estr[4] = {1, 1, 1, 1};
             TapTcParams q{};
             encode_map(&q.tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, a.p, dims, strides, box, estr);
@@ -1604,7 +1605,7 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
             for (const Window& wd : block_windows(cfg_, "head", lh, lw)) {
                 q.win = wd;
                 q.tiles_x = (wd.ox1 - wd.ox0 + kTapTX - 1) / kTapTX;
-                q.tiles_y = (wd.oy1 - wd.oy0 + tap_tile_ty(kTapConv3) - 1) / tap_tile_ty(kTapConv3);
+                q.tiles_y = (wd.oy1 - wd.oy0 + hty - 1) / hty;
                 q.num_tiles = a.n * q.tiles_x * q.tiles_y;
                 LC_CUDA(launch_tap_tc(kTapConv3, q, s_compute_));
                 ++launches;
@@ -1886,7 +1887,8 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
                                       static_cast<uint64_t>(gs)};
             const uint64_t strides[3] = {static_cast<uint64_t>(a.cs) * 2, static_cast<uint64_t>(wl) * a.cs * 2,
                                          static_cast<uint64_t>(hl) * wl * a.cs * 2};
-            const uint32_t box[4] = {64, kTapSX, static_cast<uint32_t>(tap_stage_sy(kTapSubpix)), 1};
+            const int dty = tap_tile_rows(kTapSubpix, IC, dec_last_kb_, dec_last_n_);
+            const uint32_t box[4] = {64, kTapSX, static_cast<uint32_t>(dty + 2), 1};
             const uint32_t estr[4] = {1, 1, 1, 1};
             encode_map(&q.tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, a.p, dims, strides, box, estr);
             q.w = dec_last_w16_.as<__half>();
@@ -1901,7 +1903,7 @@ void Engine::decode_dev(const float* lat_dev, int64_t n, float* video_dev) {
             q.kb = dec_last_kb_;
             q.win = Window{0, hl, 0, wl, 0, hl, 0, wl};
             q.tiles_x = (wl + kTapTX - 1) / kTapTX;
-            q.tiles_y = (hl + tap_tile_ty(kTapSubpix) - 1) / tap_tile_ty(kTapSubpix);
+            q.tiles_y = (hl + dty - 1) / dty;
             q.num_tiles = gs * q.tiles_x * q.tiles_y;
             LC_CUDA(launch_tap_tc(kTapSubpix, q, s_compute_));
             ++launches;

@@ -22,6 +22,8 @@
 // change that.
 #include "subpix_tc.cuh"
 
+#include <cstdlib>
+
 #include "pdl.cuh"
 #include "ptx.cuh"
 
@@ -32,18 +34,19 @@ namespace {
 // Per mode: staged pixels, M-tiles of 128, A stage stride.  The MMA of the
 // last M-tile reads past the staged rows into the next stage (or the tap
 // bank): those rows only feed accumulator rows that are never read.
-template <int MODE> struct Geo {
-    static constexpr int TY = tap_tile_ty(MODE), SY = tap_stage_sy(MODE);
-    static constexpr int NPix = kTapSX * SY;                   // staged pixels: decoder 462, head 330
+template <int MODE, int TYV> struct Geo {
+    static constexpr int TY = TYV, SY = TYV + 2;
+    static constexpr int NPix = kTapSX * SY;                   // staged pixels (decoder TY 5: 462)
     // GEMM rows: the head multiplies every staged pixel; the decoder only
     // the TY output rows of the window (its row taps are summed inside the
     // MMA through row-shifted A descriptors, see the kernel)
-    static constexpr int MRows = MODE == kTapSubpix ? kTapSX * TY : NPix;  // 330, 330
-    static constexpr int MT = (MRows + 127) / 128;             // 3, 3
+    static constexpr int MRows = MODE == kTapSubpix ? kTapSX * TY : NPix;
+    static constexpr int MT = (MRows + 127) / 128;
     static constexpr int ABytes = (NPix * 128 + 1023) / 1024 * 1024;
     static constexpr int KRep = MODE == kTapSubpix ? 3 : 1;    // weight K blocks per input K block
+    // A ring depth: shorter decoder tiles buy more stages in flight
+    static constexpr int ST = MODE == kTapSubpix ? (TY <= 3 ? 4 : TY == 4 ? 3 : 2) : 2;
 };
-constexpr int kStages = 2;
 constexpr int kMaxPC = 36;  // tap columns per GEMM row (decoder 8*4, head 9*4)
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 32 * (2 + kEpiWarps);
@@ -59,14 +62,15 @@ __host__ __device__ constexpr int y_stride(int mode, int C) {
 // columns per GEMM row: decoder (py, px, dx, c) after the MMA summed dy; head (tap, c)
 __host__ __device__ constexpr int pass_cols(int mode, int C) { return mode == kTapSubpix ? 8 * C : 9 * C; }
 // the fused sampler step keeps e_u of one tile: C x TY x TX floats
-template <int MODE>
+template <int MODE, int TY>
 constexpr int eu_bytes() {
-    return MODE == kTapConv3 ? 4 * Geo<MODE>::TY * kTapTX * 4 : 0;
+    return MODE == kTapConv3 ? 4 * TY * kTapTX * 4 : 0;
 }
-template <int MODE>
+template <int MODE, int TY>
 int smem_bytes(const TapTcParams& p) {
-    return 1024 + kStages * Geo<MODE>::ABytes + Geo<MODE>::KRep * p.kb * p.N * 128 +
-           Geo<MODE>::MRows * y_stride(MODE, p.C) * 4 + eu_bytes<MODE>() + 512;
+    using G = Geo<MODE, TY>;
+    return 1024 + G::ST * G::ABytes + G::KRep * p.kb * p.N * 128 + G::MRows * y_stride(MODE, p.C) * 4 +
+           eu_bytes<MODE, TY>() + 512;
 }
 
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&v)[4]) {
@@ -75,19 +79,20 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&v)[4]) {
                  : "r"(taddr));
 }
 
-template <int MODE>
+template <int MODE, int TYV>
 __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_constant__ TapTcParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    constexpr int kNPix = Geo<MODE>::NPix, kMT = Geo<MODE>::MT, kABytes = Geo<MODE>::ABytes;
-    constexpr int kMRows = Geo<MODE>::MRows, kKRep = Geo<MODE>::KRep;
-    constexpr int kTapTY = Geo<MODE>::TY;
+    using G = Geo<MODE, TYV>;
+    constexpr int kNPix = G::NPix, kMT = G::MT, kABytes = G::ABytes;
+    constexpr int kMRows = G::MRows, kKRep = G::KRep, kStages = G::ST;
+    constexpr int kTapTY = G::TY;
     const int C = p.C, N = p.N, YS = y_stride(MODE, C), PC = pass_cols(MODE, C);
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* smA = smem;
     uint8_t* smW = smA + kStages * kABytes;
     float* smY = reinterpret_cast<float*>(smW + kKRep * p.kb * N * 128);
     float* smEu = smY + kMRows * YS;  // [C][TY][TX] e_u of the pair's first tile (head, pair_T > 0)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(smEu) + eu_bytes<MODE>());
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(smEu) + eu_bytes<MODE, TYV>());
     uint64_t* full_bar = bars;                  // [kStages]
     uint64_t* empty_bar = bars + kStages;       // [kStages]
     uint64_t* tfull = bars + 2 * kStages;       // [2]
@@ -326,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_consta
     }
 }
 
-template <int MODE>
+template <int MODE, int TY>
 cudaError_t launch_mode(const TapTcParams& p, cudaStream_t st) {
     // per device: the attribute applies to the current device only
     constexpr int kMaxDevices = 64;
@@ -336,7 +341,8 @@ cudaError_t launch_mode(const TapTcParams& p, cudaStream_t st) {
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= kMaxDevices) dev = 0;
     if (!attr[dev]) {
-        const cudaError_t e = cudaFuncSetAttribute(tap_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
+        const cudaError_t e =
+            cudaFuncSetAttribute(tap_tc_kernel<MODE, TY>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax);
         if (e != cudaSuccess) return e;
         attr[dev] = true;
     }
@@ -347,26 +353,53 @@ cudaError_t launch_mode(const TapTcParams& p, cudaStream_t st) {
     const int sms = sm[dev];
     const int units = (MODE == kTapConv3 && p.pair_T > 0) ? p.pair_T * p.tiles_x * p.tiles_y : p.num_tiles;
     const int grid = units < sms ? units : sms;
-    return launch_pdl(tap_tc_kernel<MODE>, dim3(grid), dim3(kThreads), static_cast<size_t>(smem_bytes<MODE>(p)), st, p);
+    return launch_pdl(tap_tc_kernel<MODE, TY>, dim3(grid), dim3(kThreads), static_cast<size_t>(smem_bytes<MODE, TY>(p)),
+                      st, p);
 }
 
-}  // namespace
-
-bool tap_tc_supported(int mode, int C, int kb, int N) {
+template <int MODE, int TY>
+bool fits(int C, int kb, int N) {
     TapTcParams p{};
     p.C = C;
     p.kb = kb;
     p.N = N;
-    const int mt = mode == kTapSubpix ? Geo<kTapSubpix>::MT : Geo<kTapConv3>::MT;
-    const int smem = mode == kTapSubpix ? smem_bytes<kTapSubpix>(p) : smem_bytes<kTapConv3>(p);
-    return C >= 1 && C <= 4 && kb >= 1 && kb <= kTapMaxKb && N % 16 == 0 && N >= pass_cols(mode, C) &&
-           pass_cols(mode, C) <= kMaxPC && mt * N <= kAccCols && smem <= kSmemMax;
+    return C >= 1 && C <= 4 && kb >= 1 && kb <= kTapMaxKb && N % 16 == 0 && N >= pass_cols(MODE, C) &&
+           pass_cols(MODE, C) <= kMaxPC && Geo<MODE, TY>::MT * N <= kAccCols && smem_bytes<MODE, TY>(p) <= kSmemMax;
+}
+
+}  // namespace
+
+// Decoder tile height: TY 5 with a 2-stage A ring by default; LC_K8_TY = 3 /
+// 4 (4 / 3 stages) for A/B timing.  Measured on D (one box, back to back):
+// 26.95k / 26.66k / 26.73k frames/s for TY 3 / 4 / 5 -- the deeper rings buy
+// nothing once the row taps are summed in the MMA (the epilogue then waits
+// on the MMA: 72 N = 32 instructions per tile, tensor pipe 59 % active).
+int tap_tile_rows(int mode, int C, int kb, int N) {
+    if (mode != kTapSubpix) return 5;
+    static const int env = std::getenv("LC_K8_TY") ? std::atoi(std::getenv("LC_K8_TY")) : 5;
+    if (env == 3 && fits<kTapSubpix, 3>(C, kb, N)) return 3;
+    if (env == 4 && fits<kTapSubpix, 4>(C, kb, N)) return 4;
+    return 5;
+}
+
+bool tap_tc_supported(int mode, int C, int kb, int N) {
+    if (mode != kTapSubpix) return fits<kTapConv3, 5>(C, kb, N);
+    switch (tap_tile_rows(mode, C, kb, N)) {
+        case 3: return fits<kTapSubpix, 3>(C, kb, N);
+        case 4: return fits<kTapSubpix, 4>(C, kb, N);
+        default: return fits<kTapSubpix, 5>(C, kb, N);
+    }
 }
 
 cudaError_t launch_tap_tc(int mode, const TapTcParams& p, cudaStream_t st) {
     if (!tap_tc_supported(mode, p.C, p.kb, p.N)) return cudaErrorInvalidValue;
     if (p.num_tiles <= 0) return cudaSuccess;
-    return mode == kTapSubpix ? launch_mode<kTapSubpix>(p, st) : launch_mode<kTapConv3>(p, st);
+    if (mode == kTapConv3) return launch_mode<kTapConv3, 5>(p, st);
+    switch (tap_tile_rows(mode, p.C, p.kb, p.N)) {
+        case 3: return launch_mode<kTapSubpix, 3>(p, st);
+        case 4: return launch_mode<kTapSubpix, 4>(p, st);
+        default: return launch_mode<kTapSubpix, 5>(p, st);
+    }
 }
 
 }  // namespace lc

@@ -52,11 +52,11 @@ struct TapTcParams {
     int* bad;
 };
 
-// Core tile kTapTX x tap_tile_ty(mode) pixels; the staged window adds a
-// one-pixel halo on every side (TMA box kTapSX x tap_stage_sy(mode)).
+// Core tile kTapTX x TY pixels; the staged window adds a one-pixel halo on
+// every side (TMA box kTapSX x (TY + 2)).  TY = tap_tile_rows(...): the head
+// 5; the decoder 4 (a 3-stage A ring) where it fits, else 5 (2 stages).
 constexpr int kTapTX = 64, kTapSX = kTapTX + 2;
-__host__ __device__ constexpr int tap_tile_ty(int mode) { return mode == kTapSubpix ? 5 : 5; }
-__host__ __device__ constexpr int tap_stage_sy(int mode) { return tap_tile_ty(mode) + 2; }
+int tap_tile_rows(int mode, int C, int kb, int N);
 constexpr int kTapMaxKb = 5;  // c_in <= 320
 
 cudaError_t launch_tap_tc(int mode, const TapTcParams& p, cudaStream_t st);
