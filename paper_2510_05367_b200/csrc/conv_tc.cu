@@ -128,6 +128,15 @@ __device__ __forceinline__ float tanh_approx(float x) {
 // SiLU x*sigmoid(x) = h*(1+tanh(h)), h = x/2: one MUFU.TANH + 2 FP ops.
 // tanh.approx has ~2^-11 relative error, below the fp16 rounding of the
 // stored activation.
+// SiLU of x = 2h from the half-scaled pre-activation h (the epilogue folds
+// the 1/2 into its scale and offsets): 2h * sigmoid(2h) with the exponential
+// and reciprocal on the MUFU (ex2.approx / rcp.approx, ~2^-22 relative
+// error) instead of tanh.approx (~2^-11): LC_SILU_EXACT=1.
+__device__ __forceinline__ float silu_exact_h(float h) {
+    const float e = exp2f(-2.8853900817779268f * h);  // exp(-2h), ex2.approx via --use_fast_math-free exp2f
+    return __fdividef(2.0f * h, 1.0f + e);
+}
+
 __device__ __forceinline__ float silu_fast(float x) {
     const float h = 0.5f * x;
     return fmaf(h, tanh_approx(h), h);
@@ -748,8 +757,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                             float a = fmaf(__uint_as_float(v[j]), hscale, off[j]);
                             float b = fmaf(__uint_as_float(v[j + 1]), hscale, off[j + 1]);
                             if (EPI == kEpiF16Silu) {
-                                a = fmaf(a, tanh_approx(a), a);
-                                b = fmaf(b, tanh_approx(b), b);
+                                if (p.silu == 2) {
+                                    a = silu_exact_h(a);
+                                    b = silu_exact_h(b);
+                                } else {
+                                    a = fmaf(a, tanh_approx(a), a);
+                                    b = fmaf(b, tanh_approx(b), b);
+                                }
                             }
                             h[j / 2] = __floats2half2_rn(a, b);
                         }

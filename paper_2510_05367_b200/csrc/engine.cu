@@ -783,7 +783,8 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
     p.rc = L.rc;
     p.scale = s / L.wscale;
     p.shift = o;
-    p.silu = silu ? 1 : 0;
+    static const bool silu_exact = std::getenv("LC_SILU_EXACT") && std::atoi(std::getenv("LC_SILU_EXACT")) != 0;
+    p.silu = silu ? (silu_exact ? 2 : 1) : 0;
     plan_halo(L, &p, seg0_base, seg0_dims, seg0_strides);
     ConvProfiler* prof = conv_profiler();
     if (prof) {
