@@ -28,6 +28,8 @@ ncu --set full --clock-control none --import-source on -k regex:tap_tc --launch-
 ncu --set full --clock-control none --import-source on -k regex:tap_tc --launch-skip 55 --launch-count 1 \
     -o gpurun_out/full_c_dec python tools/profile_step.py C 2 > gpurun_out/ncu_full_c_dec.log 2>&1
 python tools/layer_report.py C gpurun_out/layers_c.json > gpurun_out/layers_c.txt 2>&1
+python tools/parity_report.py gpurun_out/parity.json > gpurun_out/parity.log 2>&1
+python tools/sweep.py C gpurun_out/sweep.json > gpurun_out/sweep.log 2>&1
 python tools/swap_timeline.py C > gpurun_out/swap_timeline_c.txt 2>&1
 ls -la gpurun_out
 # D: launch list with DRAM bytes (conv traffic per launch for bench's roofline.traffic)
