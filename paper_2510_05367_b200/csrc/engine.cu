@@ -1143,6 +1143,8 @@ int64_t Engine::dec_ws_bytes(int G, bool want_y) const {
 void Engine::alloc_activations(int64_t T) {
     const int64_t G = run_dec_group();
     if (T_alloc_ == T && arena_G_ == G) return;
+    if (async_pending_) (void)wait();  // queued runs still use the old arena
+    LC_CUDA(cudaDeviceSynchronize());
     invalidate_graph();
     z_key_.clear();
     act_bufs_.clear();
@@ -2302,6 +2304,7 @@ void Engine::enqueue_body(RunStats& st) {
 }
 
 RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host, bool resident_input) {
+    if (async_pending_) (void)wait();  // completes queued runs (and resets stats_)
     RunStats st;
     stats_ = &st;
     const int64_t T = cfg_.frames;
