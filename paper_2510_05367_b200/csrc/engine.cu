@@ -345,8 +345,9 @@ std::unique_ptr<TcLayer> pack_tc_layer(Ledger* l, const Bank& b, int c_split, in
                               (tiles >= 2 * 148 || (kb >= 64 && 4 * pair_units >= 3 * 74));
             const int64_t units = pair ? pair_units : tiles;
             const int slots = pair ? 74 : 148;
+            static const double ovh = std::getenv("LC_BN_OVERHEAD") ? std::atof(std::getenv("LC_BN_OVERHEAD")) : 32.0;
             const double cost = static_cast<double>((units + slots - 1) / slots) *
-                                (pair ? 0.95 : (kb >= 32 ? 1.35 : 1.0)) * (bn + 32);
+                                (pair ? 0.95 : (kb >= 32 ? 1.35 : 1.0)) * (bn + ovh);
             if (cost < best - 1e-9) {
                 best = cost;
                 best_bn = bn;
