@@ -291,6 +291,32 @@ class Context:
             lat = lat.reshape(1, T, int(cfg["codec.latent_channels"]), H // s, W // s)
         return video, lat, report
 
+    def run_result(self) -> dict:
+        """Typed RunResult of the last completed run (lc_get_run_result;
+        proj/include/stagecache/pipeline.hpp:18-39): StageWall (s),
+        StageReport peaks, timeline rows (kind, step, bytes, clock_ns), MAC
+        counters, cache_bytes_planned, makespan / stall (s), simulated."""
+        class _R(ctypes.Structure):
+            _fields_ = ([(n, ctypes.c_double) for n in ("wall_setup", "wall_encode", "wall_denoise", "wall_decode",
+                                                        "wall_total")] +
+                        [("peak_fast", ctypes.c_int64 * 4), ("peak_slow", ctypes.c_int64 * 4),
+                         ("current_fast", ctypes.c_int64), ("current_slow", ctypes.c_int64),
+                         ("events_per_stage", ctypes.c_int64 * 4), ("event_count", ctypes.c_int64)] +
+                        [(n, ctypes.c_int64) for n in ("denoiser_macs", "macs_per_full_step", "macs_per_cached_step",
+                                                       "full_steps", "cached_steps", "cache_bytes_planned")] +
+                        [("makespan_s", ctypes.c_double), ("stall_s", ctypes.c_double), ("simulated", ctypes.c_int),
+                         ("n_timeline", ctypes.c_int64)])
+        r = _R()
+        _check(lib().lc_get_run_result(self._h, ctypes.byref(r), None, I64(0)))
+        rows = np.empty((max(1, r.n_timeline), 4), np.int64)
+        _check(lib().lc_get_run_result(self._h, ctypes.byref(r), _p(rows), I64(r.n_timeline)))
+        out = {f: getattr(r, f) for f, _ in _R._fields_}
+        for f in ("peak_fast", "peak_slow", "events_per_stage"):
+            out[f] = list(out[f])
+        out["simulated"] = bool(out["simulated"])
+        out["timeline"] = rows[:r.n_timeline]
+        return out
+
     def upload_latent(self, x0: np.ndarray):
         _check(lib().lc_upload_latent(self._h, _p(_f32(x0))))
 

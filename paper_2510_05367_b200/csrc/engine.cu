@@ -1176,13 +1176,30 @@ void Engine::alloc_activations(int64_t T) {
     }
     const int64_t act0 = off;
     lv_.assign(static_cast<size_t>(M + 1), Level{});
+    // Lifetimes inside a step let two pairs share storage: the stem output
+    // dies with d0 (its only reader) before u0 writes U_0 (same shape), and
+    // the stem's patch rows die with the stem GEMM before d1 writes D_1
+    // (when they fit in it, e.g. base 320: 59 of 147 MB on C).
     place(&stem_out_, n, lh, lw, ch(0), round_up(ch(0), 64));
-    place(&patch_, n, lh, lw, stem_kp_, stem_kp_);
+    const int64_t stem_off = carve.back().second;
+    const int64_t patch_bytes = static_cast<int64_t>(n) * lh * lw * stem_kp_ * 2;
+    const bool patch_in_d1 =
+        M >= 2 && patch_bytes <= static_cast<int64_t>(n) * (lh >> 1) * (lw >> 1) * round_up(ch(1), 64) * 2;
+    if (!patch_in_d1) place(&patch_, n, lh, lw, stem_kp_, stem_kp_);
     for (int i = 0; i < M; ++i) {
         const int h = lh >> i, w = lw >> i;
         place(&lv_[i].D, n, h, w, ch(i), round_up(ch(i), 64));
+        if (i == 1 && patch_in_d1) {
+            patch_ = Act{nullptr, n, lh, lw, stem_kp_, stem_kp_};
+            carve.push_back({&patch_, carve.back().second});
+        }
         if (i >= 1) place(&lv_[i].P, n, h, w, ch(i - 1), round_up(ch(i - 1), 64));
-        if (!(cfg_.cache_enabled && i == m + 1)) place(&lv_[i].U, n, h, w, ch(i), round_up(ch(i), 64));
+        if (i == 0) {
+            lv_[0].U = Act{nullptr, n, h, w, round_up(ch(0), 64), ch(0)};
+            carve.push_back({&lv_[0].U, stem_off});
+        } else if (!(cfg_.cache_enabled && i == m + 1)) {
+            place(&lv_[i].U, n, h, w, ch(i), round_up(ch(i), 64));
+        }
         const int cu = (i == M - 1) ? ch(M - 1) : ch(i + 1);
         if (cfg_.kernel != 3 || (cfg_.chunk_enabled && cfg_.halo != HaloKind::Exact))
             place(&lv_[i].UP, n, h, w, cu, round_up(cu, 64));

@@ -209,6 +209,20 @@ def test_swap_issue_order(ctx):
     assert seq == want, " ".join(seq)
 
 
+def test_typed_run_result(ctx):
+    """lc_get_run_result: the reference's RunResult fields for the last run,
+    consistent with the JSON report (pipeline.hpp:18-39)."""
+    _, _, rep = _run(ctx, dict(TINY, **{"sampler.steps": 7, "cache.n": 3, "swap.mode": "sync"}))
+    r = ctx.run_result()
+    assert r["full_steps"] == rep["mac"]["full_steps"] == 3 and r["cached_steps"] == 4
+    assert r["denoiser_macs"] == rep["mac"]["denoiser_total"] and r["cache_bytes_planned"] == rep["cache_bytes"]
+    assert r["peak_fast"] == [rep["peaks"][s]["fast"] for s in ("setup", "encode", "denoise", "decode")]
+    assert abs(r["wall_total"] - rep["device_ms"]["total"] * 1e-3) < 1e-6 and r["wall_setup"] > 0
+    kinds = [k for k, *_ in rep["timeline"]["events"] if k in lc.TIMELINE_KINDS]
+    assert [lc.TIMELINE_KINDS[k] for k in r["timeline"][:, 0]] == kinds
+    assert abs(r["stall_s"] - rep["timeline"]["stall_ms"] * 1e-3) < 1e-9 and not r["simulated"]
+
+
 def test_swap_bytes_logical_and_moved(ctx):
     """Logical swap traffic is the reference's (one
     evict_all/prefetch_all call moves both entries; calls = 2 x full steps
