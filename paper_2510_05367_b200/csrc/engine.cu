@@ -1176,37 +1176,96 @@ void Engine::alloc_activations(int64_t T) {
     }
     const int64_t act0 = off;
     lv_.assign(static_cast<size_t>(M + 1), Level{});
-    // Lifetimes inside a step let two pairs share storage: the stem output
-    // dies with d0 (its only reader) before u0 writes U_0 (same shape), and
-    // the stem's patch rows die with the stem GEMM before d1 writes D_1
-    // (when they fit in it, e.g. base 320: 59 of 147 MB on C).
-    place(&stem_out_, n, lh, lw, ch(0), round_up(ch(0), 64));
-    const int64_t stem_off = carve.back().second;
-    const int64_t patch_bytes = static_cast<int64_t>(n) * lh * lw * stem_kp_ * 2;
-    const bool patch_in_d1 =
-        M >= 2 && patch_bytes <= static_cast<int64_t>(n) * (lh >> 1) * (lw >> 1) * round_up(ch(1), 64) * 2;
-    if (!patch_in_d1) place(&patch_, n, lh, lw, stem_kp_, stem_kp_);
+    // Denoise activations, packed by lifetime (interval first-fit): every
+    // buffer lives from its first write to its last read within one full
+    // step (whole-batch op order: patch, stem, d0, [down2, d_i]..., down2,
+    // mid, [up2, u_i]..., head); two buffers whose lifetimes are disjoint
+    // may share storage (e.g. the stem output, dead after d0, holds D_1, U_2
+    // and then U_0).  Cached steps run a sub-sequence of that order and the
+    // per-branch deep path keeps each deep buffer's two halves inside its
+    // branch's span, so disjoint here means disjoint there.  The cache
+    // entries live across steps and keep [0, cache).
+    struct Life {
+        Act* a;
+        int64_t bytes;
+        int t0, t1;
+        int64_t off;
+    };
+    std::vector<Life> lives;
+    auto def = [&](Act* a, int nn, int h, int w, int c, int cs) {
+        a->n = nn, a->h = h, a->w = w, a->c = c, a->cs = cs;
+        a->p = nullptr;
+        lives.push_back({a, al(a->elems() * 2), 1 << 30, -1, 0});
+        pad = pad || cs != c;
+    };
+    auto use = [&](Act* a, int t) {
+        for (Life& l : lives)
+            if (l.a == a) {
+                l.t0 = std::min(l.t0, t);
+                l.t1 = std::max(l.t1, t);
+            }
+    };
+    def(&patch_, n, lh, lw, stem_kp_, stem_kp_);
+    def(&stem_out_, n, lh, lw, ch(0), round_up(ch(0), 64));
     for (int i = 0; i < M; ++i) {
         const int h = lh >> i, w = lw >> i;
-        place(&lv_[i].D, n, h, w, ch(i), round_up(ch(i), 64));
-        if (i == 1 && patch_in_d1) {
-            patch_ = Act{nullptr, n, lh, lw, stem_kp_, stem_kp_};
-            carve.push_back({&patch_, carve.back().second});
-        }
-        if (i >= 1) place(&lv_[i].P, n, h, w, ch(i - 1), round_up(ch(i - 1), 64));
-        if (i == 0) {
-            lv_[0].U = Act{nullptr, n, h, w, round_up(ch(0), 64), ch(0)};
-            carve.push_back({&lv_[0].U, stem_off});
-        } else if (!(cfg_.cache_enabled && i == m + 1)) {
-            place(&lv_[i].U, n, h, w, ch(i), round_up(ch(i), 64));
-        }
+        def(&lv_[i].D, n, h, w, ch(i), round_up(ch(i), 64));
+        if (i >= 1) def(&lv_[i].P, n, h, w, ch(i - 1), round_up(ch(i - 1), 64));
+        if (!(cfg_.cache_enabled && i == m + 1)) def(&lv_[i].U, n, h, w, ch(i), round_up(ch(i), 64));
         const int cu = (i == M - 1) ? ch(M - 1) : ch(i + 1);
         if (cfg_.kernel != 3 || (cfg_.chunk_enabled && cfg_.halo != HaloKind::Exact))
-            place(&lv_[i].UP, n, h, w, cu, round_up(cu, 64));
+            def(&lv_[i].UP, n, h, w, cu, round_up(cu, 64));
     }
-    place(&lv_[M].P, n, lh >> M, lw >> M, ch(M - 1), round_up(ch(M - 1), 64));
+    def(&lv_[M].P, n, lh >> M, lw >> M, ch(M - 1), round_up(ch(M - 1), 64));
     mid_ = Act{};
-    if (!(cfg_.cache_enabled && m + 1 == M)) place(&mid_, n, lh >> M, lw >> M, ch(M - 1), round_up(ch(M - 1), 64));
+    if (!(cfg_.cache_enabled && m + 1 == M)) def(&mid_, n, lh >> M, lw >> M, ch(M - 1), round_up(ch(M - 1), 64));
+    {
+        auto U_at = [&](int l) -> Act* {
+            if (cfg_.cache_enabled && l == m + 1) return &cache_;
+            return l == M ? &mid_ : &lv_[l].U;
+        };
+        int t = 0;
+        use(&patch_, t++);
+        use(&patch_, t), use(&stem_out_, t++);
+        use(&stem_out_, t), use(&lv_[0].D, t++);
+        for (int i = 1; i <= M; ++i) {
+            use(&lv_[i - 1].D, t), use(&lv_[i].P, t++);  // down2
+            use(&lv_[i].P, t), use(i == M ? U_at(M) : &lv_[i].D, t++);
+        }
+        for (int i = M - 1; i >= 0; --i) {
+            if (lv_[i].UP.n) use(U_at(i + 1), t), use(&lv_[i].UP, t++);
+            use(&lv_[i].D, t), use(U_at(i + 1), t), use(&lv_[i].UP, t), use(i == 0 ? &lv_[0].U : U_at(i), t++);
+        }
+        use(&lv_[0].U, t++);  // head
+    }
+    std::vector<size_t> order(lives.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return lives[a].bytes > lives[b].bytes; });
+    std::vector<size_t> placed;
+    int64_t act_top = act0;
+    for (size_t k : order) {
+        Life& L = lives[k];
+        if (L.t1 < 0) continue;  // never used in this configuration
+        int64_t o = act0;
+        for (bool moved = true; moved;) {
+            moved = false;
+            for (size_t j : placed) {
+                const Life& P = lives[j];
+                const bool live_both = !(P.t1 < L.t0 || L.t1 < P.t0);
+                const bool overlap = !(P.off + P.bytes <= o || o + L.bytes <= P.off);
+                if (live_both && overlap) {
+                    o = P.off + P.bytes;
+                    moved = true;
+                }
+            }
+        }
+        L.off = o;
+        placed.push_back(k);
+        act_top = std::max(act_top, o + L.bytes);
+    }
+    for (const Life& L : lives)
+        if (L.t1 >= 0) carve.push_back({L.a, L.off});
+    off = act_top;
     const int64_t act_end = off;
     act_padding_ = pad;
     ai.act = act_end - act0;
