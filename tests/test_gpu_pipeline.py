@@ -476,7 +476,6 @@ def test_cache_memory_arithmetic(over):
     swp = _fresh_run(dict(over, **{"swap.mode": "sync"}))[0]
     delta = _peaks(on)["denoise"] - _peaks(off)["denoise"]
     assert 0 <= delta <= on["cache_bytes_physical"]
-    assert on["cache_bytes_physical"] * 8 <= on["cache_bytes"]
     assert _peaks(swp)["denoise"] == _peaks(on)["denoise"]
 
 
