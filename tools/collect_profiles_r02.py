@@ -78,7 +78,7 @@ for tag, (sel, desc) in WHAT.items():
         f"# ncu --set full --clock-control none --import-source on {sel} --launch-count 1 "
         f"python tools/profile_step.py C 2\n# {desc}\n\n" + det + "\n# selected raw metrics\n" +
         "\n".join(sel_rows) + "\n")
-for name in ("layers_c.txt", "swap_timeline_c.txt", "parity.json", "sweep.json"):
+for name in ("layers_c.txt", "swap_timeline_c.txt", "parity.json", "sweep.json", "ref_crosscheck.json"):
     src = os.path.join(G, name)
     if os.path.exists(src):
         base, ext = os.path.splitext(name)

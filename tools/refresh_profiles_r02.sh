@@ -35,3 +35,5 @@ ls -la gpurun_out
 # D: launch list with DRAM bytes (conv traffic per launch for bench's roofline.traffic)
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launch_d.csv python tools/profile_step.py D 2 > gpurun_out/ncu_d.log 2>&1
+# reference arm cross-check (B, full frames per core vs the bounded sample)
+timeout 1800 python tools/ref_crosscheck.py gpurun_out/ref_crosscheck.json > gpurun_out/ref_crosscheck.log 2>&1
