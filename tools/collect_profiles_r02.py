@@ -66,17 +66,21 @@ WHAT = {
     "dec": ("-k regex:tap_tc --launch-skip 55", "C decoder last stage: K8 tap_tc_kernel<0> (nearest 2x + 3x3 "
             "128 -> 3), 5-frame slice"),
 }
+WHAT["d_dec2"] = ("-k regex:conv_tc --launch-skip 17", "D dec2: sub-pixel up-conv 128 -> 128 to 288x512, "
+                   "halo-staged, weight-stationary, 5-frame slice (profile_step D 2, run 2)")
 for tag, (sel, desc) in WHAT.items():
-    rep = os.path.join(G, f"full_c_{tag}.ncu-rep")
+    rep = os.path.join(G, f"full_c_{tag}.ncu-rep" if not tag.startswith("d_") else f"full_{tag}.ncu-rep")
     if not os.path.exists(rep):
         continue
     det = run(["ncu", "-i", rep, "--page", "details"])
     raw = run(["ncu", "-i", rep, "--page", "raw", "--csv"])
     rows = list(csv.reader(raw.splitlines()))
     sel_rows = [f"{h} ({u}) = {v}" for h, u, v in zip(rows[0], rows[1], rows[2]) if h.startswith(KEEP)]
-    open(os.path.join(P, f"ncu_full_c_{tag}_{rnd}.txt"), "w").write(
+    name = f"ncu_full_c_{tag}_{rnd}.txt" if not tag.startswith("d_") else f"ncu_full_{tag}_{rnd}.txt"
+    wl = "D" if tag.startswith("d_") else "C"
+    open(os.path.join(P, name), "w").write(
         f"# ncu --set full --clock-control none --import-source on {sel} --launch-count 1 "
-        f"python tools/profile_step.py C 2\n# {desc}\n\n" + det + "\n# selected raw metrics\n" +
+        f"python tools/profile_step.py {wl} 2\n# {desc}\n\n" + det + "\n# selected raw metrics\n" +
         "\n".join(sel_rows) + "\n")
 for name in ("layers_c.txt", "swap_timeline_c.txt", "parity.json", "sweep.json", "ref_crosscheck.json"):
     src = os.path.join(G, name)

@@ -35,5 +35,8 @@ ls -la gpurun_out
 # D: launch list with DRAM bytes (conv traffic per launch for bench's roofline.traffic)
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launch_d.csv python tools/profile_step.py D 2 > gpurun_out/ncu_d.log 2>&1
+# D's dec2 (the 288x512 sub-pixel up-conv, halo-staged) of run 2's first slice
+ncu --set full --clock-control none --import-source on -k regex:conv_tc --launch-skip 17 --launch-count 1 \
+    -o gpurun_out/full_d_dec2 python tools/profile_step.py D 2 > gpurun_out/ncu_full_d_dec2.log 2>&1
 # reference arm cross-check (B, full frames per core vs the bounded sample)
 timeout 1800 python tools/ref_crosscheck.py gpurun_out/ref_crosscheck.json > gpurun_out/ref_crosscheck.log 2>&1
