@@ -696,3 +696,17 @@ def test_halo_staging_is_bit_identical(tmp_path, over):
     assert np.isfinite(outs[0]["v"]).all()
     assert np.array_equal(outs[0]["lat"], outs[1]["lat"])
     assert np.array_equal(outs[0]["v"], outs[1]["v"])
+
+
+def test_decode_edge_cases(ctx, oracle):
+    """decode_sliced edge cases: zero frames, a slice larger than the batch,
+    slices that do not divide it (ragged last slice)."""
+    over = dict(TINY, **{"run.frames": 5})
+    ctx.configure(lc.config_text(over, base=DEFAULT))
+    empty = ctx.decode(np.zeros((1, 0, 4, 8, 8), np.float32))
+    assert empty.shape == (1, 0, 3, 32, 32)
+    lat = np.random.default_rng(9).standard_normal((1, 5, 4, 8, 8)).astype(np.float32)
+    want = oracle.decode(_kv(over), lat)
+    for g in (3, 7):  # ragged tail, slice > frames
+        got = ctx.decode(lat, slice_frames=g)
+        assert lc.rel_l2(got, want) < TOL
