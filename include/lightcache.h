@@ -190,6 +190,11 @@ int lc_model_numbers(const char* config_text, int64_t* macs_full, int64_t* macs_
  * query n_events. */
 int lc_simulate_timeline(const char* config_text, int64_t* events, int64_t cap_events,
                          int64_t* n_events, int64_t* makespan_ns, int64_t* stall_ns);
+/* The denoise activations' arena plan (host only): every buffer's bytes,
+ * lifetime [t0, t1] within a full step and offset, packed first-fit by
+ * lifetime (the layout lc_run_pipeline uses), as JSON
+ * {cache_bytes, act_end, ops, buffers: [{name, bytes, t0, t1, off, c, cs}]}. */
+int lc_plan_arena(const char* config_text, char* out, int64_t cap);
 /* derive_seed / NormalStream (proj/include/stagecache/rng.hpp:11-45). */
 uint64_t lc_derive_seed(uint64_t seed, uint64_t stream);
 int lc_randn(uint64_t seed, int64_t n, float* out);

@@ -97,7 +97,7 @@ EXPORTS = [
     "lc_forward", "lc_decode", "lc_video_metrics", "lc_ledger_csv", "lc_ledger_summary", "lc_conv2d", "lc_up_conv2d", "lc_plan_steps", "lc_split",
     "lc_model_numbers", "lc_simulate_timeline", "lc_derive_seed", "lc_randn", "lc_shard_frames", "lc_nccl_unique_id",
     "lc_nccl_init", "lc_decode_sharded", "lc_gather_plan", "lc_host_register", "lc_host_unregister", "lc_mem_info",
-    "lc_get_run_result", "lc_last_error_stage",
+    "lc_get_run_result", "lc_last_error_stage", "lc_plan_arena",
     "lc_timer_start", "lc_timer_stop", "lc_set_conv_profile",
     "lc_conv_profile", "lc_conv_profile_records", "lc_kernel_launches", "lc_alloc_pinned", "lc_free_pinned",
 ]
@@ -183,6 +183,13 @@ def simulate_timeline(text: str):
     _check(lib().lc_simulate_timeline(text.encode(), _p(ev), I64(n.value), ctypes.byref(n), ctypes.byref(mk),
                                       ctypes.byref(st)))
     return ev[:n.value], mk.value, st.value
+
+
+def plan_arena(text: str) -> dict:
+    """lc_plan_arena: the lifetime-packed layout of the denoise activations."""
+    buf = ctypes.create_string_buffer(1 << 16)
+    _check(lib().lc_plan_arena(text.encode(), buf, I64(1 << 16)))
+    return json.loads(buf.value.decode())
 
 
 def plan_steps(total: int, n: int):

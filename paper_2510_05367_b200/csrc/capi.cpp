@@ -497,6 +497,25 @@ int lc_model_numbers(const char* text, int64_t* macs_full, int64_t* macs_cached,
     });
 }
 
+int lc_plan_arena(const char* text, char* out, int64_t cap) {
+    return guarded([&] {
+        const lc::RunConfig c = lc::parse_config_text(text ? text : "");
+        c.validate();
+        const lc::ArenaPlan p = lc::plan_arena(c);
+        std::ostringstream os;
+        os << "{\"cache_bytes\":" << p.cache_bytes << ",\"act_end\":" << p.act_end << ",\"ops\":" << p.steps_ops
+           << ",\"buffers\":[";
+        bool first = true;
+        for (const lc::ArenaBuf& b : p.bufs) {
+            os << (first ? "" : ",") << "{\"name\":\"" << b.name << "\",\"bytes\":" << b.bytes << ",\"t0\":" << b.t0
+               << ",\"t1\":" << b.t1 << ",\"off\":" << b.off << ",\"c\":" << b.c << ",\"cs\":" << b.cs << "}";
+            first = false;
+        }
+        os << "]}";
+        put(out, cap, os.str());
+    });
+}
+
 int lc_simulate_timeline(const char* text, int64_t* events, int64_t cap_events, int64_t* n_events,
                          int64_t* makespan_ns, int64_t* stall_ns) {
     return guarded([&] {

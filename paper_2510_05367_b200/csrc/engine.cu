@@ -1152,10 +1152,8 @@ void Engine::alloc_activations(int64_t T) {
     arena_.reset();
     cache_host_.reset();
     auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
-    const int n = static_cast<int>(2 * T);
     const int M = static_cast<int>(cfg_.depth), m = static_cast<int>(cfg_.cache_depth);
     const int lh = static_cast<int>(cfg_.latent_h()), lw = static_cast<int>(cfg_.latent_w());
-    auto ch = [&](int l) { return static_cast<int>(cfg_.base_channels << l); };
     // layout pass: offsets first, pointers once the arena exists
     std::vector<std::pair<Act*, int64_t>> carve;
     int64_t off = 0;
@@ -1169,103 +1167,43 @@ void Engine::alloc_activations(int64_t T) {
     };
     ArenaInfo ai;
     cache_ = Act{};
-    if (cfg_.cache_enabled) {
-        const int cc = static_cast<int>(cache_channels(cfg_));
-        place(&cache_, n, lh >> (m + 1), lw >> (m + 1), cc, round_up(cc, 64));
-        ai.cache = off;
-    }
-    const int64_t act0 = off;
     lv_.assign(static_cast<size_t>(M + 1), Level{});
-    // Denoise activations, packed by lifetime (interval first-fit): every
-    // buffer lives from its first write to its last read within one full
-    // step (whole-batch op order: patch, stem, d0, [down2, d_i]..., down2,
-    // mid, [up2, u_i]..., head); two buffers whose lifetimes are disjoint
-    // may share storage (e.g. the stem output, dead after d0, holds D_1, U_2
-    // and then U_0).  Cached steps run a sub-sequence of that order and the
-    // per-branch deep path keeps each deep buffer's two halves inside its
-    // branch's span, so disjoint here means disjoint there.  The cache
-    // entries live across steps and keep [0, cache).
-    struct Life {
-        Act* a;
-        int64_t bytes;
-        int t0, t1;
-        int64_t off;
-    };
-    std::vector<Life> lives;
-    auto def = [&](Act* a, int nn, int h, int w, int c, int cs) {
-        a->n = nn, a->h = h, a->w = w, a->c = c, a->cs = cs;
-        a->p = nullptr;
-        lives.push_back({a, al(a->elems() * 2), 1 << 30, -1, 0});
-        pad = pad || cs != c;
-    };
-    auto use = [&](Act* a, int t) {
-        for (Life& l : lives)
-            if (l.a == a) {
-                l.t0 = std::min(l.t0, t);
-                l.t1 = std::max(l.t1, t);
-            }
-    };
-    def(&patch_, n, lh, lw, stem_kp_, stem_kp_);
-    def(&stem_out_, n, lh, lw, ch(0), round_up(ch(0), 64));
-    for (int i = 0; i < M; ++i) {
-        const int h = lh >> i, w = lw >> i;
-        def(&lv_[i].D, n, h, w, ch(i), round_up(ch(i), 64));
-        if (i >= 1) def(&lv_[i].P, n, h, w, ch(i - 1), round_up(ch(i - 1), 64));
-        if (!(cfg_.cache_enabled && i == m + 1)) def(&lv_[i].U, n, h, w, ch(i), round_up(ch(i), 64));
-        const int cu = (i == M - 1) ? ch(M - 1) : ch(i + 1);
-        if (cfg_.kernel != 3 || (cfg_.chunk_enabled && cfg_.halo != HaloKind::Exact))
-            def(&lv_[i].UP, n, h, w, cu, round_up(cu, 64));
-    }
-    def(&lv_[M].P, n, lh >> M, lw >> M, ch(M - 1), round_up(ch(M - 1), 64));
     mid_ = Act{};
-    if (!(cfg_.cache_enabled && m + 1 == M)) def(&mid_, n, lh >> M, lw >> M, ch(M - 1), round_up(ch(M - 1), 64));
-    {
-        auto U_at = [&](int l) -> Act* {
-            if (cfg_.cache_enabled && l == m + 1) return &cache_;
-            return l == M ? &mid_ : &lv_[l].U;
-        };
-        int t = 0;
-        use(&patch_, t++);
-        use(&patch_, t), use(&stem_out_, t++);
-        use(&stem_out_, t), use(&lv_[0].D, t++);
-        for (int i = 1; i <= M; ++i) {
-            use(&lv_[i - 1].D, t), use(&lv_[i].P, t++);  // down2
-            use(&lv_[i].P, t), use(i == M ? U_at(M) : &lv_[i].D, t++);
-        }
-        for (int i = M - 1; i >= 0; --i) {
-            if (lv_[i].UP.n) use(U_at(i + 1), t), use(&lv_[i].UP, t++);
-            use(&lv_[i].D, t), use(U_at(i + 1), t), use(&lv_[i].UP, t), use(i == 0 ? &lv_[0].U : U_at(i), t++);
-        }
-        use(&lv_[0].U, t++);  // head
+    // Denoise activations, packed by lifetime (host.cpp plan_arena, checked
+    // on CPU by tests/test_host.py): every buffer lives from its first write
+    // to its last read within one full step; two buffers whose lifetimes are
+    // disjoint may share storage (e.g. the stem output, dead after d0, holds
+    // D_1, U_2, P_1 ... and then U_0).  Cached steps run a sub-sequence of
+    // that order, and the per-branch deep path keeps both halves of every
+    // deep buffer inside its branch's span, so disjoint there means disjoint
+    // in every schedule.  The cache entries live across steps at [0, cache).
+    if (stem_kp_ != static_cast<int>((cfg_.in_channels * cfg_.kernel * cfg_.kernel + 63) / 64 * 64))
+        throw_invariant("arena plan: stem patch width mismatch");
+    RunConfig pc = cfg_;
+    pc.frames = T;
+    const ArenaPlan plan = plan_arena(pc);
+    auto act_of = [&](const std::string& nm) -> Act* {
+        if (nm == "cache") return &cache_;
+        if (nm == "patch") return &patch_;
+        if (nm == "stem") return &stem_out_;
+        if (nm == "mid") return &mid_;
+        const int l = std::stoi(nm.substr(nm[0] == 'U' && nm[1] == 'P' ? 2 : 1));
+        if (nm[0] == 'D') return &lv_[l].D;
+        if (nm[0] == 'P') return &lv_[l].P;
+        if (nm[1] == 'P') return &lv_[l].UP;
+        return &lv_[l].U;
+    };
+    for (const ArenaBuf& b : plan.bufs) {
+        if (b.t1 < 0) continue;
+        Act* a = act_of(b.name);
+        a->n = b.n, a->h = b.h, a->w = b.w, a->c = b.c, a->cs = b.cs;
+        a->p = nullptr;
+        carve.push_back({a, b.off});
+        pad = pad || b.cs != b.c;
     }
-    std::vector<size_t> order(lives.size());
-    for (size_t i = 0; i < order.size(); ++i) order[i] = i;
-    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return lives[a].bytes > lives[b].bytes; });
-    std::vector<size_t> placed;
-    int64_t act_top = act0;
-    for (size_t k : order) {
-        Life& L = lives[k];
-        if (L.t1 < 0) continue;  // never used in this configuration
-        int64_t o = act0;
-        for (bool moved = true; moved;) {
-            moved = false;
-            for (size_t j : placed) {
-                const Life& P = lives[j];
-                const bool live_both = !(P.t1 < L.t0 || L.t1 < P.t0);
-                const bool overlap = !(P.off + P.bytes <= o || o + L.bytes <= P.off);
-                if (live_both && overlap) {
-                    o = P.off + P.bytes;
-                    moved = true;
-                }
-            }
-        }
-        L.off = o;
-        placed.push_back(k);
-        act_top = std::max(act_top, o + L.bytes);
-    }
-    for (const Life& L : lives)
-        if (L.t1 >= 0) carve.push_back({L.a, L.off});
-    off = act_top;
+    ai.cache = plan.cache_bytes;
+    const int64_t act0 = plan.cache_bytes;
+    off = plan.act_end;
     const int64_t act_end = off;
     act_padding_ = pad;
     ai.act = act_end - act0;

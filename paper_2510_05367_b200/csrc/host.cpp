@@ -773,6 +773,105 @@ StepCoeffs step_coeffs(const RunConfig& c, const Schedule& sc, int64_t s) {
     return k;
 }
 
+// ------------------------------------------------------------------ arena plan
+ArenaPlan plan_arena(const RunConfig& cfg) {
+    auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
+    auto r64 = [](int64_t v) { return static_cast<int>((v + 63) / 64 * 64); };
+    const int n = static_cast<int>(2 * cfg.frames);
+    const int M = static_cast<int>(cfg.depth), m = static_cast<int>(cfg.cache_depth);
+    const int lh = static_cast<int>(cfg.latent_h()), lw = static_cast<int>(cfg.latent_w());
+    auto ch = [&](int l) { return static_cast<int>(cfg.base_channels << l); };
+    const int kp = r64(cfg.in_channels * cfg.kernel * cfg.kernel);
+    ArenaPlan plan;
+    std::vector<ArenaBuf>& B = plan.bufs;
+    auto def = [&](const std::string& name, int h, int w, int c, int cs) {
+        B.push_back({name, n, h, w, c, cs, al(static_cast<int64_t>(n) * h * w * cs * 2), 1 << 30, -1, 0});
+    };
+    if (cfg.cache_enabled) {
+        const int cc = static_cast<int>(cache_channels(cfg));
+        def("cache", lh >> (m + 1), lw >> (m + 1), cc, r64(cc));
+    }
+    def("patch", lh, lw, kp, kp);
+    def("stem", lh, lw, ch(0), r64(ch(0)));
+    for (int i = 0; i < M; ++i) {
+        const int h = lh >> i, w = lw >> i;
+        def("D" + std::to_string(i), h, w, ch(i), r64(ch(i)));
+        if (i >= 1) def("P" + std::to_string(i), h, w, ch(i - 1), r64(ch(i - 1)));
+        if (!(cfg.cache_enabled && i == m + 1)) def("U" + std::to_string(i), h, w, ch(i), r64(ch(i)));
+        const int cu = (i == M - 1) ? ch(M - 1) : ch(i + 1);
+        if (cfg.kernel != 3 || (cfg.chunk_enabled && cfg.halo != HaloKind::Exact))
+            def("UP" + std::to_string(i), h, w, cu, r64(cu));
+    }
+    def("P" + std::to_string(M), lh >> M, lw >> M, ch(M - 1), r64(ch(M - 1)));
+    if (!(cfg.cache_enabled && m + 1 == M)) def("mid", lh >> M, lw >> M, ch(M - 1), r64(ch(M - 1)));
+    auto use = [&](const std::string& name, int t) {
+        for (ArenaBuf& b : B)
+            if (b.name == name) {
+                b.t0 = std::min(b.t0, t);
+                b.t1 = std::max(b.t1, t);
+            }
+    };
+    auto U_at = [&](int l) -> std::string {
+        if (cfg.cache_enabled && l == m + 1) return "cache";
+        return l == M ? "mid" : "U" + std::to_string(l);
+    };
+    auto has = [&](const std::string& name) {
+        for (const ArenaBuf& b : B)
+            if (b.name == name) return true;
+        return false;
+    };
+    int t = 0;
+    use("patch", t++);
+    use("patch", t), use("stem", t++);
+    use("stem", t), use("D0", t++);
+    for (int i = 1; i <= M; ++i) {
+        use("D" + std::to_string(i - 1), t), use("P" + std::to_string(i), t++);  // down2
+        use("P" + std::to_string(i), t), use(i == M ? U_at(M) : "D" + std::to_string(i), t++);
+    }
+    for (int i = M - 1; i >= 0; --i) {
+        const std::string up = "UP" + std::to_string(i);
+        if (has(up)) use(U_at(i + 1), t), use(up, t++);
+        use("D" + std::to_string(i), t), use(U_at(i + 1), t), use(up, t), use(U_at(i), t++);
+    }
+    use("U0", t++);  // head
+    plan.steps_ops = t;
+    // the cache lives across steps at [0, cache)
+    int64_t base = 0;
+    if (cfg.cache_enabled) {
+        B[0].t0 = 0, B[0].t1 = t;
+        B[0].off = 0;
+        base = plan.cache_bytes = B[0].bytes;
+    }
+    std::vector<size_t> order;
+    for (size_t i = 0; i < B.size(); ++i)
+        if (B[i].name != "cache") order.push_back(i);
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return B[a].bytes > B[b].bytes; });
+    std::vector<size_t> placed;
+    int64_t top = base;
+    for (size_t k : order) {
+        ArenaBuf& L = B[k];
+        if (L.t1 < 0) continue;  // not used in this configuration
+        int64_t o = base;
+        for (bool moved = true; moved;) {
+            moved = false;
+            for (size_t j : placed) {
+                const ArenaBuf& P = B[j];
+                const bool live_both = !(P.t1 < L.t0 || L.t1 < P.t0);
+                const bool overlap = !(P.off + P.bytes <= o || o + L.bytes <= P.off);
+                if (live_both && overlap) {
+                    o = P.off + P.bytes;
+                    moved = true;
+                }
+            }
+        }
+        L.off = o;
+        placed.push_back(k);
+        top = std::max(top, o + L.bytes);
+    }
+    plan.act_end = top;
+    return plan;
+}
+
 // ------------------------------------------------------------------ sharded decode
 ShardSpan shard_frames(int64_t T, int world, int rank) {
     if (world < 1 || rank < 0 || rank >= world) throw_config("bad world/rank");

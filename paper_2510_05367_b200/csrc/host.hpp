@@ -148,6 +148,29 @@ int64_t sim_stall_ns(const std::vector<SimEvent>& tl);     // swap.cpp:70-79
 // Virtual clock after the denoising loop's drain (pipeline.cpp:187).
 int64_t sim_denoise_end_ns(const RunConfig& cfg);
 
+// ------------------------------------------------------------------ arena plan
+// The denoise activations' lifetimes within one full step (whole-batch op
+// order: patch, stem, d0, [down2, d_i]..., down2, mid, [up2, u_i]...,
+// head) and their first-fit packing by lifetime (Engine::alloc_activations
+// lays the arena out from this plan).  Buffers: "patch", "stem", "D<i>",
+// "P<i>", "U<i>", "UP<i>", "mid"; the cache entries ("cache", U_{m+1}) keep
+// [0, cache_bytes) for the whole run.  Sizes are fp16 NHWC with 64-channel
+// strides, 256-byte aligned; t0/t1 the first write and last read.
+struct ArenaBuf {
+    std::string name;
+    int n, h, w, c, cs;
+    int64_t bytes;
+    int t0, t1;
+    int64_t off;
+};
+struct ArenaPlan {
+    std::vector<ArenaBuf> bufs;  // "cache" first when caching is on
+    int64_t cache_bytes = 0;     // [0, cache_bytes): the entries
+    int64_t act_end = 0;         // end of the packed activations
+    int steps_ops = 0;           // op slots of a full step (lifetime axis)
+};
+ArenaPlan plan_arena(const RunConfig& cfg);
+
 // ------------------------------------------------------------------ sharded decode
 // Multi-GPU sliced decode (the unit of work is
 // decode_sliced, proj/src/codec.cpp:126-145): rank r of g owns a contiguous

@@ -60,6 +60,7 @@ BVAR = {
 CHUNKVAR = {
     "b_frame0_fixed_k5": dict(B0, **{"unet.kernel": 5, "chunk.halo": "fixed", "chunk.halo_px": 1}),
     "c_frame0_none_s2": dict(C0, **{"sampler.steps": 2, "chunk.halo": "none"}),
+    "b_frame0_none": dict(B0, **{"chunk.halo": "none"}),
     "c_frame0_fixed_k5_s2": dict(C0, **{"sampler.steps": 2, "unet.kernel": 5, "chunk.halo": "fixed",
                                         "chunk.halo_px": 1}),
 }

@@ -114,3 +114,64 @@ def test_shard_frames_partition():
             for f0, c in spans:
                 covered += list(range(f0, f0 + c))
             assert covered == list(range(T))
+
+
+def _arena_configs():
+    rng = np.random.default_rng(77)
+    out = [{}, {"cache.enabled": "false"}, {"unet.cache_depth": 1}, {"unet.cache_depth": 2},
+           {"unet.kernel": 5}, {"chunk.halo": "none"},
+           {"run.frames": 25, "run.height": 576, "run.width": 1024, "codec.stages": 3, "codec.width": 128,
+            "unet.base_channels": 320, "unet.depth": 3}]
+    while len(out) < 40:
+        depth = int(rng.integers(1, 5))
+        unit = 1 << (depth + 2)
+        over = {"unet.depth": depth, "run.height": unit * int(rng.integers(1, 4)),
+                "run.width": unit * int(rng.integers(1, 4)), "unet.base_channels": int(rng.choice([8, 32, 320])),
+                "unet.cache_depth": int(rng.integers(0, depth)), "unet.kernel": int(rng.choice([1, 3, 5])),
+                "cache.enabled": str(rng.choice(["true", "false"])), "chunk.halo": str(rng.choice(["exact", "none"])),
+                "run.frames": int(rng.integers(1, 6))}
+        try:
+            lc.check_config(lc.config_text(over, base=lc.DEFAULT_CONFIG))
+        except lc.LightCacheError:
+            continue
+        out.append(over)
+    return out
+
+
+@pytest.mark.parametrize("over", _arena_configs())
+def test_arena_plan_never_overlaps_live_buffers(over):
+    """The lifetime packing of the denoise activations (host.cpp plan_arena,
+    the arena Engine::alloc_activations lays out): buffers whose lifetimes
+    within a full step overlap never share bytes, the cache keeps [0,
+    cache_bytes) for the whole step, every buffer used fits below act_end."""
+    p = lc.plan_arena(lc.config_text(over, base=lc.DEFAULT_CONFIG))
+    bufs = [b for b in p["buffers"] if b["t1"] >= 0]
+    names = [b["name"] for b in bufs]
+    for must in ("patch", "stem", "D0", "U0"):
+        assert must in names
+    assert ("cache" in names) == (over.get("cache.enabled", "true") == "true")
+    for b in bufs:
+        assert 0 <= b["t0"] <= b["t1"] < p["ops"] + 1 and b["off"] % 256 == 0
+        assert b["off"] + b["bytes"] <= p["act_end"]
+        if b["name"] == "cache":
+            assert b["off"] == 0 and b["bytes"] == p["cache_bytes"] and b["t0"] == 0 and b["t1"] >= p["ops"] - 1
+        else:
+            assert b["off"] >= p["cache_bytes"]
+    for i, a in enumerate(bufs):
+        for b in bufs[i + 1:]:
+            if a["t1"] < b["t0"] or b["t1"] < a["t0"]:
+                continue
+            assert a["off"] + a["bytes"] <= b["off"] or b["off"] + b["bytes"] <= a["off"], (a, b)
+
+
+def test_arena_plan_config_c():
+    """On config C the packing holds the 1.18 GB of activations in 0.6 GB:
+    the stem output's slot is reused by the deep levels and then by U_0."""
+    over = {"run.frames": 25, "run.height": 576, "run.width": 1024, "codec.stages": 3, "codec.width": 128,
+            "unet.base_channels": 320, "unet.depth": 3}
+    p = lc.plan_arena(lc.config_text(over, base=lc.DEFAULT_CONFIG))
+    bufs = {b["name"]: b for b in p["buffers"]}
+    total = sum(b["bytes"] for n, b in bufs.items() if n != "cache")
+    packed = p["act_end"] - p["cache_bytes"]
+    assert total > 1.1e9 and packed < 0.65e9
+    assert bufs["U0"]["off"] == bufs["stem"]["off"]  # U_0 reuses the stem output's storage
