@@ -819,6 +819,8 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
     LC_CUDA(launch_conv_tc(p, L.P, st));
 }
 
+static std::vector<Window> block_windows(const RunConfig& c, const std::string& name, int h, int w);
+
 // ---------------------------------------------------------------- engine
 Engine::Engine(int device) : device_(device) {
     LC_CUDA(cudaSetDevice(device));
@@ -966,7 +968,6 @@ void Engine::configure(const RunConfig& cfg) {
                 if (cfg.kernel == 3)
                     tc_[j] = pack_tc_layer(&ledger_, uw_.banks[j], c_skip, 1,
                                            est_m_tiles(n2, std::max(1, hl / 2), std::max(1, wl / 2)));
-                tc_fb_[j] = pack_tc_layer(&ledger_, uw_.banks[j], c_skip, 0, est_m_tiles(n2, hl, wl));
             } else {
                 tc_[j] = pack_tc_layer(&ledger_, uw_.banks[j], static_cast<int>(bp.c_in), 0, est_m_tiles(n2, hl, wl));
             }
@@ -1040,6 +1041,27 @@ void Engine::configure(const RunConfig& cfg) {
         for (int64_t i = 1; i < cfg.stages; ++i) dec_tc_.push_back(pack_tc_layer(&ledger_, cw_.dec[i], 0, 1));
         cfg_key_ = key;
         T_alloc_ = -1;
+    }
+    {
+        // materialised-upsample fallbacks of the up blocks (2-segment 3x3
+        // convs over the upsampled input): only where the fused sub-pixel
+        // form cannot run -- kernels other than 3x3, or chunk tiles whose
+        // readable windows are not parity-aligned (halos below the radius)
+        // -- so their weights (86 MB at base 320) are not resident otherwise
+        const auto plan = block_plans(cfg);
+        for (size_t j = 0; j < plan.size(); ++j) {
+            const auto& bp = plan[j];
+            if (bp.name[0] != 'u' || tc_fb_[j]) continue;
+            const int hl = static_cast<int>(cfg.latent_h() >> bp.level), wl = static_cast<int>(cfg.latent_w() >> bp.level);
+            bool need = cfg.kernel != 3;
+            for (const Window& wd : block_windows(cfg, bp.name, hl, wl))
+                if ((wd.vy0 | wd.vy1 | wd.vx0 | wd.vx1) & 1) need = true;
+            if (!need) continue;
+            const int i = std::stoi(bp.name.substr(1));
+            ledger_.enter(kSetup);
+            tc_fb_[j] = pack_tc_layer(&ledger_, uw_.banks[j], static_cast<int>(cfg.base_channels << i), 0,
+                                      est_m_tiles(static_cast<int>(2 * cfg.frames), hl, wl));
+        }
     }
     if (!same_geom || cfg.mode != cfg_prev_mode_ || cfg.slice_decode != cfg_prev_sliced_) T_alloc_ = -1;
     cfg_prev_mode_ = cfg.mode;
@@ -1359,6 +1381,7 @@ void Engine::up_block(int i, const Act& skip, const Act& u, const Act& out, floa
     LC_CUDA(launch_up2(u.p, up.p, u.n, u.h, u.w, u.cs, s_compute_));
     ++launches;
     const Act srcs[2] = {skip, up};
+    if (!tc_fb_[j]) throw_invariant("up block fallback weights not prepared by configure()");
     for (const Window& wd : wins) {
         run_tc_conv(*tc_fb_[j], srcs, out, wd, s, o, true, s_compute_);
         ++launches;
