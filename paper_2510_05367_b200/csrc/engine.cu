@@ -1119,12 +1119,12 @@ double Engine::probe_link_gbs() {
 // default (LC_BRANCH_DEEP=0 turns it off); the host link is probed once
 // (reported as swap_schedule.link_gbs_probe) for swaps of >= 32 MB entries.
 void Engine::decide_branch_deep() {
-    branch_deep_ = false;
+    branch_deep_ = 0;
     const bool swap_async = cfg_.cache_enabled && cfg_.swap_mode == SwapMode::Async &&
                             cfg_.cache_depth + 1 < cfg_.depth;
     if (!swap_async) return;
     const char* env = std::getenv("LC_BRANCH_DEEP");
-    branch_deep_ = !(env && std::atoi(env) == 0 && env[0] == '0');
+    branch_deep_ = env ? std::atoi(env) : 1;
     if (cache_.elems() * 2 >= (int64_t{32} << 20)) link_gbs_ = probe_link_gbs();
 }
 
@@ -1444,8 +1444,9 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
     // (and its eviction starts) half a deep path earlier, and entry 1's
     // eviction no longer queues behind it on the link.  Same per-image
     // arithmetic (bit-identical), same transfer issue points.
-    const bool branch_deep = writes_cache && seam == 3 && cfg_.swap_mode == SwapMode::Async && m + 1 < M &&
-                             branch_deep_;
+    const bool evicting = writes_cache && seam == 3 && cfg_.swap_mode == SwapMode::Async && m + 1 < M;
+    const bool branch_deep = evicting && branch_deep_ == 1;
+    const bool branch_up = evicting && branch_deep_ == 2;  // down path whole-batch, up path per branch
     const int deepest = full ? M - 1 : m;
     for (int i = 1; i <= (branch_deep ? m : deepest); ++i) {
         const Act& prev = lv_[i - 1].D;
@@ -1539,10 +1540,24 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
     // cond half.  Same per-image arithmetic (bit-identical), same transfer
     // issue points.
     const bool split_store = writes_cache && seam == 3 && cfg_.swap_mode == SwapMode::Async && m + 1 < M &&
-                             split_store_enabled() && !branch_deep;
+                             split_store_enabled() && !branch_deep && !branch_up;
     // Deeper up blocks stay whole-batch (their weight panels, up to 170 MB,
     // would be streamed twice); only the producing block u_{m+1} is split.
     int first = branch_deep ? m : top;
+    if (branch_up) {
+        // every up block below the seam per branch: entry 0 is complete
+        // after half of the deep up path
+        for (int b = 0; b < 2; ++b) {
+            for (int i = top; i >= m + 1; --i) {
+                const int j = static_cast<int>(block_index(cfg_, "u" + std::to_string(i)));
+                cond(j, &s, &o);
+                if (i == m + 1) await_store(b);
+                up_block(i, half(lv_[i].D, b), half(U_of(i + 1), b), half(U_of(i), b), s, o);
+            }
+            cache_ready(b);
+        }
+        first = m;
+    }
     if (split_store) {
         for (int i = top; i > m + 1; --i) {
             const int j = static_cast<int>(block_index(cfg_, "u" + std::to_string(i)));

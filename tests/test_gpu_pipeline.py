@@ -637,15 +637,16 @@ def test_branch_deep_path_is_bit_identical(tmp_path, over):
     import subprocess
     import sys
     outs = []
-    for bd in ("1", "0"):
+    for bd in ("1", "2", "0"):  # per-branch deep path, per-branch up path, whole batch
         path = str(tmp_path / f"bd_{bd}.npz")
         env = dict(os.environ, LC_BRANCH_DEEP=bd)
         r = subprocess.run([sys.executable, "-c", _K8_CHILD, repr(over), path], env=env, capture_output=True,
                            text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(path))
-    assert np.array_equal(outs[0]["lat"], outs[1]["lat"])
-    assert np.array_equal(outs[0]["v"], outs[1]["v"])
+    for o in outs[:2]:
+        assert np.array_equal(o["lat"], outs[2]["lat"])
+        assert np.array_equal(o["v"], outs[2]["v"])
 
 
 _HALO_CHILD = r"""
