@@ -9,7 +9,7 @@ import pytest
 
 HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 FRAME0 = ["b_frame0", "c_frame0", "b_frame0_ancestral", "b_frame0_ddim", "b_frame0_image", "b_frame0_fixed_k5",
-          "c_frame0_none_s2", "c_frame0_fixed_k5_s2"]
+          "c_frame0_none_s2", "c_frame0_fixed_k5_s2", "b_frame0_none"]
 
 
 @pytest.mark.parametrize("name", FRAME0)

@@ -355,7 +355,7 @@ def _gold(name):
 
 
 FRAME0_GOLDENS = ["b_frame0", "c_frame0", "b_frame0_ancestral", "b_frame0_ddim", "b_frame0_image",
-                  "b_frame0_fixed_k5", "c_frame0_none_s2", "c_frame0_fixed_k5_s2"]
+                  "b_frame0_fixed_k5", "c_frame0_none_s2", "c_frame0_fixed_k5_s2", "b_frame0_none"]
 
 
 @pytest.mark.parametrize("name", FRAME0_GOLDENS)

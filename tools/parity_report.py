@@ -18,7 +18,7 @@ out = {}
 ctx = lc.Context(0)
 for name in ["tiny", "tiny_ancestral", "tiny_ddim_m1", "tiny_halo_none", "tiny_k5", "tiny_image", "default", "config_a",
              "b_frame0", "b_frame0_ancestral", "b_frame0_ddim", "b_frame0_image", "b_frame0_fixed_k5", "c_frame0",
-             "c_frame0_none_s2", "c_frame0_fixed_k5_s2"]:
+             "c_frame0_none_s2", "c_frame0_fixed_k5_s2", "b_frame0_none"]:
     g = np.load(os.path.join(GOLD, f"{name}.npz"))
     text = str(g["config"])
     ctx.configure(text)
