@@ -1,9 +1,10 @@
-"""Un-extrapolated cross-check of bench.py's reference arm:
-every host core runs the reference's own run_pipeline (oracle/_ref) on ONE
-full-resolution frame of config B (frame 0 is bit-identical to the T-frame
-run's), so frames/s = cores / wall with no MAC scaling; the
-bench's bounded-sample estimate for B is measured in the same process pool
-beside it.  Writes a JSON summary.  Nothing of the product is imported."""
+"""Cross-check of bench.py's reference arm: every host core
+runs the reference's own run_pipeline (oracle/_ref) at FULL resolution --
+one frame of config B, and one frame of config C over the sample's 2-step
+refresh period -- and then the bench's bounded sample, in the same process
+pool; the two per-core MAC rates tell how far the sample's extrapolation is
+from the reference's speed at the real image size.  Writes a JSON summary.
+Nothing of the product is imported."""
 import json
 import multiprocessing as mp
 import os
@@ -20,22 +21,30 @@ def main():
     out_path = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out", "ref_crosscheck.json")
     import lco
     workers = max(1, min(os.cpu_count() or 1, 256))
-    full = bench._kv(dict(bench.WORKLOADS["B"], **{"run.frames": 1}))
-    samp, macs_s, macs_f, kind = bench.cpu_sample("B")
+    res = {"cores": workers}
+    lib, _ = bench._cpu_lib()
     with mp.get_context("spawn").Pool(workers) as pool:
-        t0 = time.time()
-        pool.map(bench._cpu_worker, [(lco.to_text(full), False)] * workers)
-        wall_full = time.time() - t0
-        t0 = time.time()
-        pool.map(bench._cpu_worker, [(lco.to_text(samp), False)] * workers)
-        wall_samp = time.time() - t0
-    res = {"kind": kind, "cores": workers,
-           "full_frame": {"frames_per_s": workers / wall_full, "wall_s": wall_full,
-                          "what": "one full-resolution frame of config B per core (512x512, 4 steps, N=2)"},
-           "sample_extrapolated": {"frames_per_s": workers * macs_s / macs_f / wall_samp, "wall_s": wall_samp,
-                                   "sample_gmac": macs_s / 1e9, "frame_gmac": macs_f / 1e9},
-           }
-    res["ratio_sample_over_full"] = res["sample_extrapolated"]["frames_per_s"] / res["full_frame"]["frames_per_s"]
+        for wl, full_over in (("B", {"run.frames": 1}),
+                              # C at full resolution over the sample's 2-step refresh period (a 25-step
+                              # C frame is ~55 min per core): the same work per step as the headline
+                              ("C", {"run.frames": 1, "sampler.steps": 2})):
+            full = bench._kv(dict(bench.WORKLOADS[wl], **full_over))
+            samp, macs_s, macs_f, kind = bench.cpu_sample(wl)
+            macs_full = bench.ref_run_macs(lib, full)
+            t0 = time.time()
+            pool.map(bench._cpu_worker, [(lco.to_text(full), False)] * workers)
+            wall_full = time.time() - t0
+            t0 = time.time()
+            pool.map(bench._cpu_worker, [(lco.to_text(samp), False)] * workers)
+            wall_samp = time.time() - t0
+            r = {"kind": kind,
+                 "full_resolution": {"gmac_per_s_per_core": macs_full / 1e9 / wall_full, "wall_s": wall_full,
+                                     "gmac": macs_full / 1e9, "config": {k: full[k] for k in full_over} |
+                                     {"run.height": full["run.height"], "run.width": full["run.width"]}},
+                 "sample": {"gmac_per_s_per_core": macs_s / 1e9 / wall_samp, "wall_s": wall_samp,
+                            "gmac": macs_s / 1e9, "latent": f"{samp['run.height']}x{samp['run.width']} px"}}
+            r["rate_ratio_sample_over_full"] = r["sample"]["gmac_per_s_per_core"] / r["full_resolution"]["gmac_per_s_per_core"]
+            res[wl] = r
     json.dump(res, open(out_path, "w"), indent=1)
     print(json.dumps(res))
 
