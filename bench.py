@@ -304,15 +304,27 @@ def cpu_measure(workload: str, reps: int = 1):
     per = statistics.median(times)
     fps = macs_s / macs_f / per
     return {"value": fps, "unit": "frames/s", "cores": 1, "kind": kind,
-            "sample": _sample_desc(workload, samp, macs_s, macs_f, kind) + f"; {per:.1f} s per sample, 1 core"}
+            "sample": _sample_desc(workload, samp, macs_s, macs_f, kind) + f"; {per:.1f} s per sample, 1 core "
+                      "(not size-calibrated: the --impl reference arm measures the full-resolution / sample rate "
+                      "ratio, 1.24 on C in profiles/ref_crosscheck_r02.json)"}
+
+
+# Full-resolution calibration job of the reference arm: one frame of the
+# real workload over one cache refresh period (the sample's step mix).  The
+# reference's MAC rate depends on the image size (tools/ref_crosscheck.py,
+# profiles/ref_crosscheck_r02.json: C at full resolution 1.22 GMAC/s per
+# core vs 0.98 for the 8x16 sample; B 0.96 vs 0.97), so the sample's
+# extrapolated frames/s is scaled by the ratio measured in the same run.
+CALIB = {"C": {"run.frames": 1, "sampler.steps": 2}, "B": {"run.frames": 1, "sampler.steps": 2}}
 
 
 def reference_arm(args, world, rank):
     """The reference's own CPU implementation of the path (oracle/_ref:
     the unmodified proj/src compiled in place; run_pipeline,
     proj/src/pipeline.cpp:64-228) on all host cores: each step runs one
-    bounded sample per core in a persistent process pool.  Nothing of the
-    product (paper_2510_05367_b200) is imported or loaded here."""
+    bounded sample per core in a persistent process pool; the warm-up runs
+    the full-resolution calibration job (CALIB) once per core.  Nothing of
+    the product (paper_2510_05367_b200) is imported or loaded here."""
     if rank != 0:
         return
     import multiprocessing as mp
@@ -320,26 +332,43 @@ def reference_arm(args, world, rank):
     samp, macs_s, macs_f, kind = cpu_sample(args.workload)
     workers = max(1, min(os.cpu_count() or 1, 256))
     job = (lco.to_text(samp), args.workload == "D")
+    calib = None
     with mp.get_context("spawn").Pool(workers) as pool:
-        for _ in range(args.warmup):
+        if args.workload in CALIB and args.warmup > 0:
+            lib, _ = _cpu_lib()
+            ckv = _kv(dict(WORKLOADS[args.workload], **CALIB[args.workload]))
+            cmacs = ref_run_macs(lib, ckv)
+            cwalls = pool.map(_cpu_worker, [(lco.to_text(ckv), False)] * workers)
+            calib = {"full_res_gmac_per_s_per_core": cmacs / 1e9 / statistics.median(cwalls),
+                     "job": f"1 frame at {ckv['run.height']}x{ckv['run.width']}, {ckv['sampler.steps']} steps, "
+                            f"{cmacs / 1e9:.1f} GMAC, {statistics.median(cwalls):.0f} s per core"}
+        for _ in range(max(0, args.warmup - (1 if calib else 0))):
             pool.map(_cpu_worker, [job] * workers)
-        walls = []
+        walls, per_proc = [], []
         for _ in range(args.steps):
             t0 = time.time()
-            pool.map(_cpu_worker, [job] * workers)
+            per_proc += pool.map(_cpu_worker, [job] * workers)
             walls.append(time.time() - t0)
     total = sum(walls)
     frames = workers * args.steps * macs_s / macs_f  # full-workload frame equivalents
-    fps = frames / total
+    fps_raw = frames / total
+    fps = fps_raw
     desc = _sample_desc(args.workload, samp, macs_s, macs_f, kind) + (
         f"; {workers} processes x {args.steps} steps, {total / args.steps:.2f} s per step")
+    if calib:
+        calib["sample_gmac_per_s_per_core"] = macs_s / 1e9 / statistics.median(per_proc)
+        calib["ratio"] = calib["full_res_gmac_per_s_per_core"] / calib["sample_gmac_per_s_per_core"]
+        fps = fps_raw * calib["ratio"]
+        desc += (f"; scaled by the reference's full-resolution / sample MAC-rate ratio {calib['ratio']:.3f} "
+                 f"measured in the warm-up ({calib['job']})")
     line = {"metric": "video_frames_per_sec", "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * total / args.steps,
             "higher_is_better": True, "scaling": "weak" if args.workload != "D" else "strong",
             "vs_baseline": None, "dtype": "fp32",
             "data": "synthetic (seeded randn latent, random-init weights of the reference architecture)",
             "config": workload_config(args, world), "impl": "reference",
-            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": workers, "kind": kind, "sample": desc},
+            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": workers, "kind": kind, "sample": desc,
+                             "uncalibrated_value": fps_raw, "calibration": calib},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
