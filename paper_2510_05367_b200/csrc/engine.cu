@@ -956,11 +956,20 @@ void Engine::configure(const RunConfig& cfg) {
         tc_.resize(plan.size());
         tc_fb_.clear();
         tc_fb_.resize(plan.size());
+        // Evicting full steps run the blocks below the seam level per CFG
+        // branch (forward_dev, branch_deep_): their tile-count hints then see
+        // T images, not 2T (the wave model picks BN for the half batch).
+        const char* bde = std::getenv("LC_BRANCH_DEEP");
+        const int bmode = bde ? std::atoi(bde) : 1;
+        const bool evicting = cfg.cache_enabled && cfg.swap_mode == SwapMode::Async &&
+                              cfg.cache_depth + 1 < cfg.depth && bmode != 0;
         for (size_t j = 0; j < plan.size(); ++j) {
             const auto& bp = plan[j];
             if (bp.name == "stem" || bp.name == "head") continue;
             // M-tile hints from the run geometry (2T images at the block's level)
-            const int n2 = static_cast<int>(2 * cfg.frames);
+            const bool half_batch = evicting && bp.level > cfg.cache_depth &&
+                                    (bmode == 1 || bp.name[0] == 'u');
+            const int n2 = static_cast<int>((half_batch ? 1 : 2) * cfg.frames);
             const int hl = static_cast<int>(cfg.latent_h() >> bp.level), wl = static_cast<int>(cfg.latent_w() >> bp.level);
             if (bp.name[0] == 'u') {
                 const int i = std::stoi(bp.name.substr(1));
