@@ -1,6 +1,6 @@
 """Multi-GPU sliced decode: the host-side partition and the frame gather.
 
-* world_size 2/3/4 over gloo on CPU: every rank takes its balanced frame
+* world_size 2/3/4/8 over gloo on CPU: every rank takes its balanced frame
   block (lc_shard_frames), decodes it slice by slice with the oracle
   decoder, and the ranks execute the product's gather schedule
   (lc_gather_plan: round i sends the i-th slice of every rank to rank 0)
@@ -71,7 +71,7 @@ def _worker(rank, world, port, lat, slice_frames, out_path):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,slice_frames", [(2, 2), (3, 1), (4, 2)])
+@pytest.mark.parametrize("world,slice_frames", [(2, 2), (3, 1), (4, 2), (8, 1)])
 def test_sharded_decode_gather_gloo(tmp_path, oracle, world, slice_frames):
     import lco
     import paper_2510_05367_b200 as lc
