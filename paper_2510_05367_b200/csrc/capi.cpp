@@ -95,7 +95,8 @@ std::string report_json(const lc::Engine& e, const lc::RunStats& st) {
            << ",\"decode\":" << ai.dec << ",\"encode\":" << ai.enc
            << ",\"decode_overlaps_cache\":" << (ai.dec_overlaps_cache ? "true" : "false") << "},";
         os << "\"swap_schedule\":{\"link_gbs_probe\":" << e.link_gbs()
-           << ",\"branch_deep\":" << e.branch_deep() << "},";
+           << ",\"branch_deep\":" << e.branch_deep() << ",\"branch_seam\":" << (e.branch_seam() ? "true" : "false")
+           << "},";
     }
     const auto& c = e.config();
     os << "\"video\":{\"frames\":" << c.frames << ",\"channels\":" << c.image_channels

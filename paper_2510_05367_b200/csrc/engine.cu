@@ -1129,12 +1129,23 @@ double Engine::probe_link_gbs() {
 // (reported as swap_schedule.link_gbs_probe) for swaps of >= 32 MB entries.
 void Engine::decide_branch_deep() {
     branch_deep_ = 0;
+    branch_seam_ = true;
+    link_gbs_ = 0;
     const bool swap_async = cfg_.cache_enabled && cfg_.swap_mode == SwapMode::Async &&
                             cfg_.cache_depth + 1 < cfg_.depth;
     if (!swap_async) return;
     const char* env = std::getenv("LC_BRANCH_DEEP");
     branch_deep_ = env ? std::atoi(env) : 1;
     if (cache_.elems() * 2 >= (int64_t{32} << 20)) link_gbs_ = probe_link_gbs();
+    // The branch-wise seam (the cached step's seam block per entry, first
+    // half of its images as soon as they landed) only pays when the prefetch
+    // is still in flight at the seam.  On a host link that moves a step's
+    // entries well inside the compute window the whole-batch seam block is
+    // one launch instead of four: C, one box, 3 interleaved runs each:
+    // 248.3 vs 246.9 frames/s at a 48-50 GB/s probe.  LC_BRANCH_SEAM=0/1
+    // forces it.
+    const char* bs = std::getenv("LC_BRANCH_SEAM");
+    branch_seam_ = bs ? std::atoi(bs) != 0 : !(link_gbs_ >= 45.0);
 }
 
 int64_t Engine::run_dec_group() const {
@@ -1532,10 +1543,8 @@ void Engine::forward_dev(const float* x_dev, bool stacked, int64_t T, int64_t ti
     // so the seam block starts on the uncond half as soon as that entry has
     // landed and overlaps the cond entry's transfer.  Same bytes, same order
     // of awaits and issue points as assemble() + evict_all().
-    static const bool branch_seam_on =
-        !(std::getenv("LC_BRANCH_SEAM") && std::atoi(std::getenv("LC_BRANCH_SEAM")) == 0);
     const bool branch_seam =
-        !full && seam > 0 && prefetch_pending_ && cfg_.swap_mode == SwapMode::Async && branch_seam_on;
+        !full && seam > 0 && prefetch_pending_ && cfg_.swap_mode == SwapMode::Async && branch_seam_;
     if (!full && seam > 0 && !branch_seam) {
         seam_await(step);
         // last consumer: evict_all right after assemble (pipeline.cpp:156-160)

@@ -272,6 +272,7 @@ public:
     ArenaInfo arena_info() const { return arena_info_; }
     double link_gbs() const { return link_gbs_; }  // host-link probe (GB/s per direction, 0 = not probed)
     int branch_deep() const { return branch_deep_; }
+    bool branch_seam() const { return branch_seam_; }
 
 private:
     // Decode workspace: per-stage activations of one slice of G frames, the
@@ -325,6 +326,7 @@ private:
     // per-branch deep path in full steps that evict (forward_dev): chosen
     // from the measured host-link bandwidth (LC_BRANCH_DEEP=0/1 forces it)
     int branch_deep_ = 0;  // 0 whole batch, 1 per-branch deep path, 2 per-branch up path
+    bool branch_seam_ = true;  // cached steps: seam block per CFG entry (see decide_branch_deep)
     void decide_branch_deep();
     double probe_link_gbs();
     void conv_block(int j, const Act& in, const Act& out, float s, float o, bool silu);
