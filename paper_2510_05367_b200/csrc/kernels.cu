@@ -253,15 +253,37 @@ __global__ void up2_kernel(const __half* __restrict__ in, __half* __restrict__ o
 }
 
 // ------------------------------------------------------------ step update
+// One element of the sampler update in the reference's two-rounding order
+// (cfg_combine + reverse_step_*, sampler.cpp:95-133).
+__device__ __forceinline__ float step_one(const StepArgs& a, float eu, float ec, float x, float z) {
+    const float eps = __fadd_rn(__fmul_rn(1.0f - a.g, eu), __fmul_rn(a.g, ec));
+    float xn = __fadd_rn(__fmul_rn(a.a, x), __fmul_rn(a.b, eps));
+    if (a.z) xn = __fadd_rn(__fmul_rn(1.0f, xn), __fmul_rn(a.c, z));
+    return xn;
+}
+
+// 16-byte vectors where every operand is 16-byte aligned (the engine's
+// buffers are), scalar tail; non-finite results voted per warp.
 __global__ void step_kernel(const StepArgs a) {
     pdl_wait();
     int f = 0;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < a.n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const float eu = a.eps2[i], ec = a.eps2[a.n + i];
-        const float eps = __fadd_rn(__fmul_rn(1.0f - a.g, eu), __fmul_rn(a.g, ec));
-        float xn = __fadd_rn(__fmul_rn(a.a, a.x[i]), __fmul_rn(a.b, eps));
-        if (a.z) xn = __fadd_rn(__fmul_rn(1.0f, xn), __fmul_rn(a.c, a.z[i]));
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    const bool vec = a.n % 4 == 0 && al16(a.eps2) && al16(a.x) && al16(a.x_out) && (!a.z || al16(a.z));
+    const int64_t n4 = vec ? a.n / 4 : 0;
+    for (int64_t i = tid; i < n4; i += stride) {
+        const float4 eu = reinterpret_cast<const float4*>(a.eps2)[i];
+        const float4 ec = reinterpret_cast<const float4*>(a.eps2 + a.n)[i];
+        const float4 x = reinterpret_cast<const float4*>(a.x)[i];
+        const float4 z = a.z ? reinterpret_cast<const float4*>(a.z)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 o = make_float4(step_one(a, eu.x, ec.x, x.x, z.x), step_one(a, eu.y, ec.y, x.y, z.y),
+                                     step_one(a, eu.z, ec.z, x.z, z.z), step_one(a, eu.w, ec.w, x.w, z.w));
+        reinterpret_cast<float4*>(a.x_out)[i] = o;
+        f |= !isfinite(o.x) | !isfinite(o.y) | !isfinite(o.z) | !isfinite(o.w);
+    }
+    for (int64_t i = 4 * n4 + tid; i < a.n; i += stride) {
+        const float xn = step_one(a, a.eps2[i], a.eps2[a.n + i], a.x[i], a.z ? a.z[i] : 0.0f);
         a.x_out[i] = xn;
         f |= !isfinite(xn);
     }
@@ -270,9 +292,18 @@ __global__ void step_kernel(const StepArgs a) {
 
 __global__ void linear_kernel(float a, const float* x, float b, const float* y, float* out, int64_t n) {
     pdl_wait();
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        out[i] = __fadd_rn(__fmul_rn(a, x[i]), __fmul_rn(b, y[i]));
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const bool vec = n % 4 == 0 && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+                                     reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    const int64_t n4 = vec ? n / 4 : 0;
+    for (int64_t i = tid; i < n4; i += stride) {
+        const float4 u = reinterpret_cast<const float4*>(x)[i], v = reinterpret_cast<const float4*>(y)[i];
+        reinterpret_cast<float4*>(out)[i] =
+            make_float4(__fadd_rn(__fmul_rn(a, u.x), __fmul_rn(b, v.x)), __fadd_rn(__fmul_rn(a, u.y), __fmul_rn(b, v.y)),
+                        __fadd_rn(__fmul_rn(a, u.z), __fmul_rn(b, v.z)), __fadd_rn(__fmul_rn(a, u.w), __fmul_rn(b, v.w)));
+    }
+    for (int64_t i = 4 * n4 + tid; i < n; i += stride) out[i] = __fadd_rn(__fmul_rn(a, x[i]), __fmul_rn(b, y[i]));
 }
 
 // all_finite (tensor.cpp:376): 16-byte loads, a per-thread flag and one
@@ -360,12 +391,12 @@ cudaError_t launch_up2(const __half* in, __half* out, int nimg, int H, int W, in
 }
 
 cudaError_t launch_step(const StepArgs& a, cudaStream_t st) {
-    return launch_pdl(step_kernel, dim3(grid_for(a.n, 256)), dim3(256), 0, st, a);
+    return launch_pdl(step_kernel, dim3(grid_for((a.n + 3) / 4, 256)), dim3(256), 0, st, a);
 }
 
 cudaError_t launch_linear(float a, const float* x, float b, const float* y, float* out, int64_t n,
                           cudaStream_t st) {
-    return launch_pdl(linear_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, a, x, b, y, out, n);
+    return launch_pdl(linear_kernel, dim3(grid_for((n + 3) / 4, 256)), dim3(256), 0, st, a, x, b, y, out, n);
 }
 
 cudaError_t launch_isfinite(const float* x, int64_t n, int* bad, cudaStream_t st) {
