@@ -561,13 +561,25 @@ def decode_sharded_leg(args, world, rank, local, steps=None):
     lat_p = lc.PinnedArray(lat.size)
     lat_p.array[:] = lat
     name = f"lc_bench_video_{os.environ.get('MASTER_PORT', '0')}"
+    host_shared = False
     if world > 1:
+        import shutil
         import torch.distributed as dist
-        if rank == 0:
-            shared = lc.SharedVideo(name, T * 3 * H * W, create=True)
-        dist.barrier()
-        if rank != 0:
-            shared = lc.SharedVideo(name, T * 3 * H * W, create=False)
+        # one shared page-locked video (every rank downloads its own frames)
+        # when /dev/shm can hold it; otherwise rank 0 downloads the gathered
+        # video into its own pinned buffer
+        try:
+            host_shared = shutil.disk_usage("/dev/shm").free > 2 * T * 3 * H * W * 4
+        except OSError:
+            host_shared = False
+        if host_shared:
+            if rank == 0:
+                shared = lc.SharedVideo(name, T * 3 * H * W, create=True)
+            dist.barrier()
+            if rank != 0:
+                shared = lc.SharedVideo(name, T * 3 * H * W, create=False)
+        else:
+            shared = lc.PinnedArray(T * 3 * H * W) if rank == 0 else None
     else:
         shared = lc.PinnedArray(T * 3 * H * W)
     sl = max(d for d in range(1, 6) if T % d == 0) if args.workload != "D" else args.decode_slice
@@ -582,17 +594,18 @@ def decode_sharded_leg(args, world, rank, local, steps=None):
         launches += ctx.kernel_launches()
     dev_ms = allmax(world, dev_ms)
     for _ in range(2):
-        ctx.decode_sharded(lat_p, sl, out=shared, host_shared=world > 1)
+        ctx.decode_sharded(lat_p, sl, out=shared, host_shared=host_shared)
     barrier(world)
     e2e_ms = 0.0
     for _ in range(steps):
-        _, ms = ctx.decode_sharded(lat_p, sl, out=shared, host_shared=world > 1)
+        _, ms = ctx.decode_sharded(lat_p, sl, out=shared, host_shared=host_shared)
         e2e_ms += ms
     e2e_ms = allmax(world, e2e_ms)
     barrier(world)
     finite = bool(np.isfinite(shared.array).all()) if rank == 0 else None
     barrier(world)
-    shared.free()
+    if shared is not None:
+        shared.free()
     lat_p.free()
     ctx.close()
     return {"workload": DESCR["D"], "n_gpus": world, "steps": steps, "decode_slice_frames": sl,
@@ -600,7 +613,8 @@ def decode_sharded_leg(args, world, rank, local, steps=None):
             "scaling": "strong",
             "e2e": {"value": T * steps / (e2e_ms / 1e3), "unit": "frames/s",
                     "h2d_bytes_per_step": T * 4 * (H // s) * (W // s) * 4, "d2h_bytes_per_step": T * 3 * H * W * 4,
-                    "note": "each rank H2Ds its latent block and D2Hs its own frames into one shared pinned video"},
+                    "note": ("each rank H2Ds its latent block and D2Hs its own frames into one shared pinned video"
+                             if host_shared else "each rank H2Ds its latent block; rank 0 D2Hs the gathered video")},
             "gpu_launches": launches, "video_finite": finite}
 
 
