@@ -45,7 +45,7 @@ template <int MODE, int TYV> struct Geo {
     static constexpr int ABytes = (NPix * 128 + 1023) / 1024 * 1024;
     static constexpr int KRep = MODE == kTapSubpix ? 3 : 1;    // weight K blocks per input K block
     // A ring depth: shorter decoder tiles buy more stages in flight
-    static constexpr int ST = MODE == kTapSubpix ? (TY <= 3 ? 4 : TY == 4 ? 3 : 2) : 2;
+    static constexpr int ST = MODE == kTapSubpix ? (TY <= 3 ? 4 : TY == 4 ? 3 : 2) : (TY <= 3 ? 3 : 2);
 };
 constexpr int kMaxPC = 36;  // tap columns per GEMM row (decoder 8*4, head 9*4)
 constexpr int kEpiWarps = 8;
@@ -375,7 +375,11 @@ bool fits(int C, int kb, int N) {
 // nothing once the row taps are summed in the MMA (the epilogue then waits
 // on the MMA: 72 N = 32 instructions per tile, tensor pipe 59 % active).
 int tap_tile_rows(int mode, int C, int kb, int N) {
-    if (mode != kTapSubpix) return 5;
+    if (mode != kTapSubpix) {
+        // head: TY 5 (2 stages) by default; LC_K8_HEAD_TY=3 (3 stages) for A/B timing
+        static const int henv = std::getenv("LC_K8_HEAD_TY") ? std::atoi(std::getenv("LC_K8_HEAD_TY")) : 5;
+        return henv == 3 && fits<kTapConv3, 3>(C, kb, N) ? 3 : 5;
+    }
     static const int env = std::getenv("LC_K8_TY") ? std::atoi(std::getenv("LC_K8_TY")) : 5;
     if (env == 3 && fits<kTapSubpix, 3>(C, kb, N)) return 3;
     if (env == 4 && fits<kTapSubpix, 4>(C, kb, N)) return 4;
@@ -383,7 +387,8 @@ int tap_tile_rows(int mode, int C, int kb, int N) {
 }
 
 bool tap_tc_supported(int mode, int C, int kb, int N) {
-    if (mode != kTapSubpix) return fits<kTapConv3, 5>(C, kb, N);
+    if (mode != kTapSubpix)
+        return tap_tile_rows(mode, C, kb, N) == 3 ? fits<kTapConv3, 3>(C, kb, N) : fits<kTapConv3, 5>(C, kb, N);
     switch (tap_tile_rows(mode, C, kb, N)) {
         case 3: return fits<kTapSubpix, 3>(C, kb, N);
         case 4: return fits<kTapSubpix, 4>(C, kb, N);
@@ -394,7 +399,8 @@ bool tap_tc_supported(int mode, int C, int kb, int N) {
 cudaError_t launch_tap_tc(int mode, const TapTcParams& p, cudaStream_t st) {
     if (!tap_tc_supported(mode, p.C, p.kb, p.N)) return cudaErrorInvalidValue;
     if (p.num_tiles <= 0) return cudaSuccess;
-    if (mode == kTapConv3) return launch_mode<kTapConv3, 5>(p, st);
+    if (mode == kTapConv3)
+        return tap_tile_rows(mode, p.C, p.kb, p.N) == 3 ? launch_mode<kTapConv3, 3>(p, st) : launch_mode<kTapConv3, 5>(p, st);
     switch (tap_tile_rows(mode, p.C, p.kb, p.N)) {
         case 3: return launch_mode<kTapSubpix, 3>(p, st);
         case 4: return launch_mode<kTapSubpix, 4>(p, st);
