@@ -57,22 +57,25 @@ KEEP = ("sm__pipe_tc_cycles_active.avg.pct", "sm__pipe_tensor_cycles_active.avg.
         "smsp__average_warps_issue_stalled_", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed")
 WHAT = {
-    "stem": ("-k regex:conv_tc --launch-skip 204", "C stem GEMM (K = 64 patch rows -> 320 ch, SiLU, TMA store), "
-             "run 2 step 0"),
-    "d0": ("-k regex:conv_tc --launch-skip 205", "C d0 (3x3 320 -> 320 on 72x128, halo ring, CTA pairs), run 2 "
-           "step 0"),
-    "head": ("-k regex:tap_tc --launch-skip 30", "C head: K8 tap_tc_kernel<1> with the fused CFG + Euler step, "
-             "run 2 step 0"),
-    "dec": ("-k regex:tap_tc --launch-skip 55", "C decoder last stage: K8 tap_tc_kernel<0> (nearest 2x + 3x3 "
-            "128 -> 3), 5-frame slice"),
+    "stem": ("-k regex:conv_tc --launch-skip 0", "C stem GEMM (K = 64 patch rows -> 320 ch, SiLU, TMA store), "
+             "run 1 step 0", "conv_tc_kernel<1, 1>"),
+    "d0": ("-k regex:conv_tc --launch-skip 1", "C d0 (3x3 320 -> 320 on 72x128, halo ring, CTA pairs), run 1 "
+           "step 0", "conv_tc_kernel<2, 1>"),
+    "head": ("-k regex:tap_tc --launch-skip 0", "C head: K8 tap_tc_kernel<1> with the fused CFG + Euler step, "
+             "run 1 step 0", "tap_tc_kernel<1"),
+    "dec": ("-k regex:tap_tc --launch-skip 25", "C decoder last stage: K8 tap_tc_kernel<0> (nearest 2x + 3x3 "
+            "128 -> 3), 5-frame slice", "tap_tc_kernel<0"),
 }
-WHAT["d_dec2"] = ("-k regex:conv_tc --launch-skip 17", "D dec2: sub-pixel up-conv 128 -> 128 to 288x512, "
-                   "halo-staged, weight-stationary, 5-frame slice (profile_step D 2, run 2)")
-for tag, (sel, desc) in WHAT.items():
+WHAT["d_dec2"] = ("-k regex:conv_tc --launch-skip 2", "D dec2: sub-pixel up-conv 128 -> 128 to 288x512, "
+                   "halo-staged, weight-stationary, 5-frame slice (profile_step D 1)", "conv_tc_kernel<1, 1>")
+for tag, (sel, desc, kname) in WHAT.items():
     rep = os.path.join(G, f"full_c_{tag}.ncu-rep" if not tag.startswith("d_") else f"full_{tag}.ncu-rep")
     if not os.path.exists(rep):
         continue
     det = run(["ncu", "-i", rep, "--page", "details"])
+    if kname not in det:  # the capture must be the kernel the file is named after
+        print(f"skip {tag}: captured kernel is not {kname}")
+        continue
     raw = run(["ncu", "-i", rep, "--page", "raw", "--csv"])
     rows = list(csv.reader(raw.splitlines()))
     sel_rows = [f"{h} ({u}) = {v}" for h, u, v in zip(rows[0], rows[1], rows[2]) if h.startswith(KEEP)]
@@ -80,7 +83,7 @@ for tag, (sel, desc) in WHAT.items():
     wl = "D" if tag.startswith("d_") else "C"
     open(os.path.join(P, name), "w").write(
         f"# ncu --set full --clock-control none --import-source on {sel} --launch-count 1 "
-        f"python tools/profile_step.py {wl} 2\n# {desc}\n\n" + det + "\n# selected raw metrics\n" +
+        f"python tools/profile_step.py {wl} 1\n# {desc}\n\n" + det + "\n# selected raw metrics\n" +
         "\n".join(sel_rows) + "\n")
 for name in ("layers_c.txt", "swap_timeline_c.txt", "parity.json", "sweep.json", "ref_crosscheck.json"):
     src = os.path.join(G, name)
