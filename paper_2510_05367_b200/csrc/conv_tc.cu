@@ -222,6 +222,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bfull + 1);
     // two epilogue offset tables [ncls + 1][BN] fp32 (see the header comment)
     const uint32_t tab_s = smem_u32(smB + b_blocks * b_bytes + 256);
+    // 256 B aligned (tab_s is 1024-aligned + 256): the fp16 staging slots are
+    // SWIZZLE_32B TMA-store boxes, whose atom is 256 B
     const uint32_t stage_out_s = tab_s + ((tab_bytes(tabf, b_res) + 1023) & ~1023);
 
     const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x) / 32, 0);  // warp-uniform
@@ -768,9 +770,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                             h[j / 2] = __floats2half2_rn(a, b);
                         }
                         if (p.tma_out) {
+                            // 32 B rows, SWIZZLE_32B (tmO): 16-byte unit u of row r sits at u ^ (r / 4 % 2)
                             const uint32_t sb = stage_out_s + static_cast<uint32_t>(((warp - 2) * slots + (ring ? (stage_it & 1) : hh)) * schunk + lane * 32);
-                            sts128u(sb, *reinterpret_cast<uint4*>(&h[0]));
-                            sts128u(sb + 16, *reinterpret_cast<uint4*>(&h[4]));
+                            const uint32_t sw = ((sb >> 7) & 1u) << 4;  // address bit 7 (= lane / 4 % 2)
+                            sts128u(sb + sw, *reinterpret_cast<uint4*>(&h[0]));
+                            sts128u(sb + (16u ^ sw), *reinterpret_cast<uint4*>(&h[4]));
                         } else {
                             __half* dst =
                                 p.out + ((static_cast<size_t>(img) * p.out_h + oy) * p.out_w + ox) * p.cs_out + nb;

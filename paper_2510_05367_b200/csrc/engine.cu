@@ -773,8 +773,12 @@ void run_tc_conv(const TcLayer& L, const Act* srcs, const Act& out, const Window
                                              static_cast<uint64_t>(out.h) * out.w * out.cs * esz};
                 const uint32_t box[4] = {16, bxd, byd, bid};
                 const uint32_t estr[4] = {1, 1, 1, 1};
+                // fp16: the 32 px x 16 ch staging box has 32 B rows, swizzled so the
+                // epilogue's 16-byte stores of 8 consecutive pixels hit distinct banks
+                // (the staging slots are 256 B aligned, the 32B-swizzle atom)
                 encode_map(&p.tmO[q], p.nhwc32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4,
-                           base, dims, strides, box, estr, CU_TENSOR_MAP_SWIZZLE_NONE);
+                           base, dims, strides, box, estr,
+                           p.nhwc32 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_32B);
             }
         }
     }
