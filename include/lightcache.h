@@ -165,6 +165,21 @@ int lc_conv2d(lc_ctx* ctx, const float* x, int64_t b, int64_t t, int64_t c_in, i
 int lc_up_conv2d(lc_ctx* ctx, const float* skip, const float* u, int64_t b, int64_t t,
                  int64_t c_a, int64_t c_b, int64_t h, int64_t w, const float* taps,
                  const float* bias, int64_t c_out, float s, float o, float* out);
+/* cfg_combine + reverse_step_{ancestral,ddim,euler} (proj/src/sampler.cpp:
+ * 95-133) as one device update at index t of the context's configured
+ * (spaced) schedule, the t argument of the reference's reverse_step_*:
+ *   eps = (1-g) e_u + g e_c;  x' = a x + b eps  [+ sqrt(beta_t) z,
+ *   z = randn(n, noise_seed), ancestral with t > 0 only].
+ * sampler: 0 ancestral, 1 ddim, 2 euler (SamplerKind).  eps2 holds e_u then
+ * e_c (2n floats, select_batch(eps2, 0/1)); x, x_out n floats (host).
+ * *nonfinite (nullable) = 1 if x' holds a non-finite value.  Errors:
+ * guidance < 0, then t outside [0, steps) -> 2 (ConfigError, sampler.cpp:130,
+ * :79-84). */
+int lc_sampler_step(lc_ctx* ctx, int sampler, int64_t t, const float* x, const float* eps2, int64_t n,
+                    double guidance, uint64_t noise_seed, float* x_out, int* nonfinite);
+/* all_finite (proj/src/tensor.cpp:376) of n host floats on the device:
+ * *finite = 1 when every value is finite. */
+int lc_all_finite(lc_ctx* ctx, const float* x, int64_t n, int* finite);
 
 /* Host logic (bit-exact contracts) ---------------------------------------- */
 /* plan_steps (proj/src/cache.cpp:25-33): kinds[s] 1 = Full; flags bit0

@@ -168,6 +168,29 @@ public:
         check(lc_video_metrics(ctx_, a, b, t, c, h, w, data_range, psnr->data(), ssim->data()));
     }
 
+    // cfg_combine + reverse_step_{ancestral,ddim,euler} (proj/src/sampler.cpp:
+    // 95-133) at index t of the configured schedule; kind follows SamplerKind
+    // (0 ancestral, 1 ddim, 2 euler).  Returns x'.
+    std::vector<float> sampler_step(int kind, int64_t t, const std::vector<float>& x,
+                                    const std::vector<float>& eps_uncond, const std::vector<float>& eps_cond,
+                                    double guidance, uint64_t noise_seed = 0) {
+        if (eps_uncond.size() != x.size() || eps_cond.size() != x.size())
+            throw ShapeError("cfg_combine: operand shapes differ");
+        std::vector<float> eps2(eps_uncond);
+        eps2.insert(eps2.end(), eps_cond.begin(), eps_cond.end());
+        std::vector<float> out(x.size());
+        check(lc_sampler_step(ctx_, kind, t, x.data(), eps2.data(), static_cast<int64_t>(x.size()), guidance,
+                              noise_seed, out.data(), nullptr));
+        return out;
+    }
+
+    // all_finite (proj/src/tensor.cpp:376) on the device.
+    bool all_finite(const std::vector<float>& x) {
+        int f = 0;
+        check(lc_all_finite(ctx_, x.data(), static_cast<int64_t>(x.size()), &f));
+        return f != 0;
+    }
+
     // write_ledger_csv content (proj/src/ledger.cpp:224-242) of this engine.
     std::string ledger_csv() {
         int64_t need = 0;

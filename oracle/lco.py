@@ -349,6 +349,16 @@ class Reference:
                                       ctypes.c_int(int(sliced)), _p(out)))
         return out
 
+    def sampler_step(self, kv: dict, kind: int, t: int, x, eps_u, eps_c, guidance: float, noise_seed: int = 0):
+        """cfg_combine + reverse_step_* (proj/src/sampler.cpp:95-133) at index t
+        of the config's spaced schedule; kind 0 ancestral, 1 ddim, 2 euler."""
+        x, eps_u, eps_c = _f32(x), _f32(eps_u), _f32(eps_c)
+        out = np.empty_like(x)
+        self._chk(self.lib.ref_sampler_step(to_text(kv).encode(), ctypes.c_int(kind), ctypes.c_int64(t), _p(x),
+                                            _p(eps_u), _p(eps_c), ctypes.c_int64(x.size), ctypes.c_double(guidance),
+                                            ctypes.c_uint64(noise_seed), _p(out)))
+        return out
+
     def conv2d_window(self, x, taps, bias, k, win=None):
         x = _f32(x)
         taps, bias = _f32(taps), _f32(bias)

@@ -17,6 +17,7 @@
 #include "stagecache/config.hpp"
 #include "stagecache/metrics.hpp"
 #include "stagecache/pipeline.hpp"
+#include "stagecache/sampler.hpp"
 #include "stagecache/unet.hpp"
 
 using namespace stagecache;
@@ -178,6 +179,34 @@ int ref_decode(const char* config_text, const float* lat, int64_t n, int64_t h, 
         LatentBatch lb = merge_bt(std::move(l));
         Tensor5 v = sliced ? decode_sliced(lb, cw, cfg.codec) : decode_batch(lb, cw, cfg.codec);
         copy_out(v, video);
+    });
+}
+
+// cfg_combine + reverse_step_{ancestral,ddim,euler} (proj/src/sampler.cpp:
+// 95-133) at index t of the config's spaced schedule (pipeline.cpp:90-93);
+// kind follows SamplerKind (0 ancestral, 1 ddim, 2 euler); x, eps_u, eps_c
+// and out hold n floats.
+int ref_sampler_step(const char* config_text, int kind, int64_t t, const float* x, const float* eps_u,
+                     const float* eps_c, int64_t n, double guidance, uint64_t noise_seed, float* out) {
+    return guarded([&] {
+        RunConfig cfg = parse_text(config_text);
+        const NoiseSchedule train = make_linear_schedule(cfg.train_steps, cfg.beta_min, cfg.beta_max);
+        const SampledSchedule sub = spaced_schedule(train, cfg.inference_steps);
+        auto load = [n](const float* src) {
+            Tensor5 v = Tensor5::uninit({1, 1, 1, 1, n});
+            std::memcpy(v.data(), src, static_cast<size_t>(v.bytes()));
+            return v;
+        };
+        const Tensor5 xt = load(x), eu = load(eps_u), ec = load(eps_c);
+        const Tensor5 eps = cfg_combine({eu, ec, guidance});
+        Tensor5 r;
+        switch (kind) {
+            case 0: r = reverse_step_ancestral(xt, t, eps, sub.schedule, noise_seed); break;
+            case 1: r = reverse_step_ddim(xt, t, eps, sub.schedule); break;
+            case 2: r = reverse_step_euler(xt, t, eps, sub.schedule); break;
+            default: throw ConfigError("sampler kind");
+        }
+        copy_out(r, out);
     });
 }
 

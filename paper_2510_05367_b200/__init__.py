@@ -100,6 +100,7 @@ EXPORTS = [
     "lc_get_run_result", "lc_last_error_stage", "lc_plan_arena",
     "lc_timer_start", "lc_timer_stop", "lc_set_conv_profile",
     "lc_conv_profile", "lc_conv_profile_records", "lc_kernel_launches", "lc_alloc_pinned", "lc_free_pinned",
+    "lc_sampler_step", "lc_all_finite",
 ]
 
 # ----------------------------------------------------------------- config
@@ -449,6 +450,31 @@ class Context:
         _check(lib().lc_up_conv2d(self._h, _p(skip), _p(u), I64(b), I64(t), I64(ca), I64(cb), I64(h), I64(w),
                                   _p(taps), _p(bias), I64(c_out), ctypes.c_float(s), ctypes.c_float(o), _p(out)))
         return out
+
+    SAMPLER_KINDS = {"ancestral": 0, "ddim": 1, "euler": 2}  # SamplerKind order
+
+    def sampler_step(self, sampler, t: int, x, eps_uncond, eps_cond, guidance: float, noise_seed: int = 0):
+        """cfg_combine + reverse_step_<sampler> (proj/src/sampler.cpp:95-133) at
+        index t of the configured (spaced) schedule, on the device.  Returns
+        (x', nonfinite)."""
+        kind = self.SAMPLER_KINDS[sampler] if isinstance(sampler, str) else int(sampler)
+        x, eu, ec = _f32(x), _f32(eps_uncond), _f32(eps_cond)
+        if eu.shape != x.shape or ec.shape != x.shape:
+            raise ShapeError("cfg_combine: operand shapes differ")
+        eps2 = np.ascontiguousarray(np.concatenate([eu.ravel(), ec.ravel()]))
+        out = np.empty_like(x)
+        bad = ctypes.c_int(0)
+        _check(lib().lc_sampler_step(self._h, ctypes.c_int(kind), I64(t), _p(x), _p(eps2), I64(x.size),
+                                     ctypes.c_double(guidance), ctypes.c_uint64(noise_seed), _p(out),
+                                     ctypes.byref(bad)))
+        return out, bool(bad.value)
+
+    def all_finite(self, x) -> bool:
+        """all_finite (proj/src/tensor.cpp:376) on the device."""
+        x = _f32(x)
+        f = ctypes.c_int(0)
+        _check(lib().lc_all_finite(self._h, _p(x), I64(x.size), ctypes.byref(f)))
+        return bool(f.value)
 
     # -- multi-GPU sliced decode
     def nccl_init(self, uid: bytes, world: int, rank: int):

@@ -459,6 +459,75 @@ int lc_up_conv2d(lc_ctx* ctx, const float* skip, const float* u, int64_t b, int6
     });
 }
 
+int lc_sampler_step(lc_ctx* ctx, int sampler, int64_t t, const float* x, const float* eps2, int64_t n,
+                    double guidance, uint64_t noise_seed, float* x_out, int* nonfinite) {
+    return guarded_on(ctx, [&] {
+        if (sampler < 0 || sampler > 2) lc::throw_config("sampler must be 0 (ancestral), 1 (ddim) or 2 (euler)");
+        if (n < 0) lc::throw_shape("sampler step: negative element count");
+        // cfg_combine's check first, then reverse_step's check_t (pipeline order)
+        if (guidance < 0.0) lc::throw_config("cfg_combine: guidance scale must be >= 0");
+        const lc::Schedule sc = lc::make_schedule(ctx->engine.config());
+        const lc::StepCoeffs k = lc::step_coeffs_at(static_cast<lc::Sampler>(sampler), sc, t, noise_seed);
+        if (nonfinite) *nonfinite = 0;
+        if (n == 0) return;
+        std::vector<float> z;
+        if (k.has_noise) {
+            z.resize(static_cast<size_t>(n));
+            lc::randn(k.noise_seed, n, z.data());
+        }
+        // one buffer: e_u e_c | x | z | x' | flag, each 16-byte aligned
+        const int64_t seg = (n + 3) / 4 * 4;
+        lc::DevBuf d = lc::dev_alloc(nullptr, (5 * seg + 4) * 4, false);
+        float* e_d = d.as<float>();
+        float* x_d = e_d + 2 * seg;
+        float* z_d = x_d + seg;
+        float* o_d = z_d + seg;
+        int* bad_d = reinterpret_cast<int*>(o_d + seg);
+        cudaStream_t st = ctx->engine.stream();
+        LC_CUDA(cudaMemcpyAsync(e_d, eps2, n * 4, cudaMemcpyHostToDevice, st));
+        LC_CUDA(cudaMemcpyAsync(e_d + n, eps2 + n, n * 4, cudaMemcpyHostToDevice, st));
+        LC_CUDA(cudaMemcpyAsync(x_d, x, n * 4, cudaMemcpyHostToDevice, st));
+        if (k.has_noise) LC_CUDA(cudaMemcpyAsync(z_d, z.data(), n * 4, cudaMemcpyHostToDevice, st));
+        LC_CUDA(cudaMemsetAsync(bad_d, 0, 4, st));
+        lc::StepArgs a{};
+        a.eps2 = e_d;
+        a.x = x_d;
+        a.x_out = o_d;
+        a.z = k.has_noise ? z_d : nullptr;
+        a.n = n;
+        a.g = static_cast<float>(guidance);
+        a.a = k.a;
+        a.b = k.b;
+        a.c = k.noise;
+        a.bad = bad_d;
+        LC_CUDA(lc::launch_step(a, st));
+        int bad = 0;
+        LC_CUDA(cudaMemcpyAsync(x_out, o_d, n * 4, cudaMemcpyDeviceToHost, st));
+        LC_CUDA(cudaMemcpyAsync(&bad, bad_d, 4, cudaMemcpyDeviceToHost, st));
+        LC_CUDA(cudaStreamSynchronize(st));
+        if (nonfinite) *nonfinite = bad;
+    });
+}
+
+int lc_all_finite(lc_ctx* ctx, const float* x, int64_t n, int* finite) {
+    return guarded_on(ctx, [&] {
+        if (n < 0 || !finite) lc::throw_shape("all_finite: negative element count or null result");
+        *finite = 1;
+        if (n == 0) return;
+        lc::DevBuf d = lc::dev_alloc(nullptr, (n + 3) / 4 * 16 + 4, false);
+        float* x_d = d.as<float>();
+        int* bad_d = reinterpret_cast<int*>(x_d + (n + 3) / 4 * 4);
+        cudaStream_t st = ctx->engine.stream();
+        LC_CUDA(cudaMemcpyAsync(x_d, x, n * 4, cudaMemcpyHostToDevice, st));
+        LC_CUDA(cudaMemsetAsync(bad_d, 0, 4, st));
+        LC_CUDA(lc::launch_isfinite(x_d, n, bad_d, st));
+        int bad = 0;
+        LC_CUDA(cudaMemcpyAsync(&bad, bad_d, 4, cudaMemcpyDeviceToHost, st));
+        LC_CUDA(cudaStreamSynchronize(st));
+        *finite = !bad;
+    });
+}
+
 int lc_plan_steps(int64_t total, int64_t n, int8_t* kinds, int8_t* flags) {
     return guarded([&] {
         const lc::StepPlan p = lc::plan_steps(total, n);

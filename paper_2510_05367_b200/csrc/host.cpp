@@ -735,11 +735,12 @@ Schedule make_schedule(const RunConfig& c) {
     return s;
 }
 
-StepCoeffs step_coeffs(const RunConfig& c, const Schedule& sc, int64_t s) {
-    const int64_t S = c.steps;
-    const int64_t j = S - 1 - s;
+StepCoeffs step_coeffs_at(Sampler kind, const Schedule& sc, int64_t j, uint64_t noise_seed) {
+    if (j < 0 || j >= static_cast<int64_t>(sc.betas.size()))  // check_t, sampler.cpp:78-83
+        throw_config("reverse_step: t=" + std::to_string(j) + " outside [0, " +
+                     std::to_string(sc.betas.size()) + ")");
     StepCoeffs k;
-    switch (c.sampler) {
+    switch (kind) {
         case Sampler::Euler: {  // sampler.cpp:119-125
             const double drift = 2.0 - std::sqrt(sc.alphas[j]);
             const double diff = -0.5 * sc.betas[j] / std::sqrt(1.0 - sc.abar[j]);
@@ -765,12 +766,17 @@ StepCoeffs step_coeffs(const RunConfig& c, const Schedule& sc, int64_t s) {
             if (j != 0) {
                 k.has_noise = true;
                 k.noise = static_cast<float>(std::sqrt(sc.betas[j]));
-                k.noise_seed = derive_seed(c.seed, 0x1000 + static_cast<uint64_t>(s));
+                k.noise_seed = noise_seed;
             }
             break;
         }
     }
     return k;
+}
+
+StepCoeffs step_coeffs(const RunConfig& c, const Schedule& sc, int64_t s) {
+    // step s of the loop runs schedule index S-1-s (pipeline.cpp:160-185)
+    return step_coeffs_at(c.sampler, sc, c.steps - 1 - s, derive_seed(c.seed, 0x1000 + static_cast<uint64_t>(s)));
 }
 
 // ------------------------------------------------------------------ arena plan

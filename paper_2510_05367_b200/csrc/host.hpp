@@ -229,5 +229,8 @@ struct StepCoeffs {
     uint64_t noise_seed = 0;
 };
 StepCoeffs step_coeffs(const RunConfig& cfg, const Schedule& sc, int64_t s);
+// The same at schedule index t (the reference's reverse_step_* t argument),
+// ancestral noise drawn from noise_seed; ConfigError outside [0, steps).
+StepCoeffs step_coeffs_at(Sampler kind, const Schedule& sc, int64_t t, uint64_t noise_seed);
 
 }  // namespace lc

@@ -12,7 +12,7 @@ run_pipeline on the same config (about 5 min for B, 65 min for C, single
 thread), assert the restatement's video is bit-identical and record
 `video_source = "oracle/_ref"` plus the reference's wall time in the npz.
 
-Usage:  python tests/golden/make_golden.py [small|b0|c0|bvar|chunkvar|pin_b0|pin_c0|pin_bvar|pin_chunkvar|metrics|timelines]...
+Usage:  python tests/golden/make_golden.py [small|b0|c0|bvar|chunkvar|pin_b0|pin_c0|pin_bvar|pin_chunkvar|metrics|timelines|sampler]...
 """
 import json
 import os
@@ -164,6 +164,43 @@ def metrics():
     np.savez_compressed(os.path.join(HERE, "metrics.npz"), **out)
 
 
+# sampler operator cases: (config overrides, kind, t, guidance); the schedule
+# is the config's spaced one (train_steps 50 -> sampler.steps)
+SAMPLER_CASES = {
+    "euler_t24": ({}, 2, 24, 1.5),
+    "euler_t0": ({}, 2, 0, 1.5),
+    "ddim_t12": ({}, 1, 12, 2.0),
+    "ddim_t0": ({}, 1, 0, 0.0),
+    "ancestral_t7": ({}, 0, 7, 1.5),
+    "ancestral_t0": ({}, 0, 0, 1.5),
+    "euler_s6_t5": ({"sampler.steps": 6}, 2, 5, 7.5),
+    "ancestral_s6_t3": ({"sampler.steps": 6, "schedule.train_steps": 1000, "schedule.beta_min": 0.00085,
+                         "schedule.beta_max": 0.012}, 0, 3, 1.0),
+}
+
+
+def sampler():
+    """cfg_combine + reverse_step_* (proj/src/sampler.cpp:95-133) from the
+    reference on seeded operands: n = 1027 (a 16-byte vector body and a
+    scalar tail on the device)."""
+    ref = lco.Reference()
+    rng = np.random.default_rng(23)
+    n = 1027
+    out = {}
+    for name, (over, kind, t, g) in SAMPLER_CASES.items():
+        kv = kv_of(over)
+        x = rng.standard_normal(n).astype(np.float32)
+        eu = rng.standard_normal(n).astype(np.float32)
+        ec = rng.standard_normal(n).astype(np.float32)
+        seed = int(rng.integers(1, 1 << 62))
+        out[name + "_x"], out[name + "_eu"], out[name + "_ec"] = x, eu, ec
+        out[name + "_args"] = np.array([kind, t, seed], np.uint64)
+        out[name + "_g"] = np.array(g, np.float64)
+        out[name + "_config"] = np.array(lco.to_text(kv))
+        out[name + "_out"] = ref.sampler_step(kv, kind, t, x, eu, ec, g, seed)
+    np.savez_compressed(os.path.join(HERE, "sampler.npz"), **out)
+
+
 SIM_TINY = {"run.frames": 2, "run.height": 32, "run.width": 32, "sampler.steps": 6, "run.seed": 7,
             "swap.simulate": "true"}
 SIM = {
@@ -227,5 +264,7 @@ if __name__ == "__main__":
             pin(name, over)
     if "metrics" in what:
         metrics()
+    if "sampler" in what:
+        sampler()
     if "timelines" in what:
         timelines()
