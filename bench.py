@@ -179,7 +179,8 @@ def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d.get("bf16_tflops_sustained", 1392.2), "measured (MEASURED_PEAKS.json bf16 sustained; fp16 same rate)"
+        if "bf16_tflops_sustained" in d:
+            return d["bf16_tflops_sustained"], "measured (MEASURED_PEAKS.json bf16 sustained; fp16 same rate)"
     return 1400.0, "fallback (B200_PROFILING.md sustained)"
 
 
