@@ -8,6 +8,7 @@
 #include <cstring>
 
 #include <chrono>
+#include <thread>
 
 namespace lc {
 
@@ -2427,13 +2428,21 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
     // second, and replayed from then on: the host no longer paces ~70
     // launches per video (tensor-map encoding, parameter setup).
     const bool can_graph = use_graphs && conv_profiler() == nullptr;
-    // Pinned destination: the decoded slices stream out inside the body.
+    // Pinned destination: the decoded slices stream out inside the body.  A
+    // pageable destination (the reference's host RunResult::video) gets a
+    // pinned staging buffer that the slices stream into the same way; the
+    // host copies it out with several threads once the run completes.
     float* pinned = nullptr;
     if (video_host) {
         cudaPointerAttributes pa{};
         if (cudaPointerGetAttributes(&pa, video_host) == cudaSuccess && pa.type == cudaMemoryTypeHost)
             pinned = video_host;
         cudaGetLastError();  // clear a "not a CUDA pointer" status for pageable memory
+        if (!pinned) {
+            const int64_t vbytes = video_elems() * 4;
+            if (!vid_stage_.p || vid_stage_.bytes < vbytes) vid_stage_ = host_alloc(nullptr, vbytes);
+            pinned = vid_stage_.as<float>();
+        }
     }
     if (graph_exec_ && graph_slice_ != decode_slice) invalidate_graph();
     video_host_pinned_ = pinned;
@@ -2487,7 +2496,29 @@ RunStats Engine::run(const float* x0_host, float* video_host, float* latent_host
     if (pinned) enqueue_video_out(pinned);
     if (cfg_.swap_simulate) ledger_.virt = sim_decode_s_;
     ledger_.enter(kDecode);
-    return finish_run(st, video_host, latent_host);
+    RunStats out = finish_run(st, pinned == video_host ? video_host : nullptr, latent_host);
+    if (video_host && pinned != video_host) copy_out_parallel(video_host, pinned, video_elems());
+    return out;
+}
+
+// Pinned staging -> the caller's pageable video: a memory-bound host copy
+// split over up to 8 threads (first-touch page faults of a fresh caller
+// buffer are spread the same way).
+void Engine::copy_out_parallel(float* dst, const float* src, int64_t n) {
+    const int64_t kMin = 1 << 20;  // floats per thread at least
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int nt = static_cast<int>(std::min<int64_t>(std::min<unsigned>(hw, 8u), (n + kMin - 1) / kMin));
+    if (nt <= 1) {
+        std::memcpy(dst, src, static_cast<size_t>(n) * 4);
+        return;
+    }
+    std::vector<std::thread> th;
+    const int64_t per = (n + nt - 1) / nt;
+    for (int i = 0; i < nt; ++i) {
+        const int64_t a = i * per, b = std::min(n, a + per);
+        if (a < b) th.emplace_back([=] { std::memcpy(dst + a, src + a, static_cast<size_t>(b - a) * 4); });
+    }
+    for (auto& t : th) t.join();
 }
 
 // Throughput form of run() with pinned host buffers: H2D of the latent, the

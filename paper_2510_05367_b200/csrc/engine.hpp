@@ -306,6 +306,7 @@ private:
     void prepare_noise();
     void invalidate_graph();
     RunStats finish_run(RunStats st, float* video_host, float* latent_host);
+    static void copy_out_parallel(float* dst, const float* src, int64_t n);
     bool async_pending_ = false;
     bool host_valid_ = false;  // the pinned host copy equals the device cache (clean entries)
     RunStats last_async_;
@@ -422,6 +423,7 @@ private:
     int dl_gate_step_ = 0;
     std::string dl_gate_where_ = "stem";  // measured: 0:stem ~ 0:d0 > off > later gates (B e2e)
     DevBuf dl_scratch_;                    // pinned capture placeholder of the node's destination
+    DevBuf vid_stage_;                     // pinned staging of a pageable run() video destination
     cudaGraph_t graph_ = nullptr;          // kept alive: dl_node_ belongs to it
     cudaGraphNode_t dl_node_ = nullptr;
     float* dl_pending_ = nullptr;          // pinned destination of a not yet issued download
