@@ -586,8 +586,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         uint32_t stage_it = 0;  // TMA-store staging ring position
+        int rot = 0;            // column-group rotation of this tile (ConvParams::epi_rot)
         for (int u = unit0; u < total_units; u += unit_step) {
             const TileCoord tc = coord(u);
+            const int egr = kCh == 1 ? (eg + rot) % kEpiGroups : eg;
+            rot = (rot + p.epi_rot) % kEpiGroups;
             bool next_switch = false;
             int next_key = cur_key;
             if (tabf) {
@@ -646,9 +649,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t t_row = tmem_base + acc * acc_stride + (static_cast<uint32_t>(q * 32) << 16);
-            // this warp owns the 16-column chunks eg, eg+G, eg+2G, ... (G =
+            // this warp owns the 16-column chunks egr, egr+G, egr+2G, ... (G =
             // kEpiGroups); two TMEM loads in flight per wait
-            for (int c00 = 16 * eg; c00 < p.BN; c00 += kCh * kPair) {
+            for (int c00 = 16 * egr; c00 < p.BN; c00 += kCh * kPair) {
                 const bool two = kCh == 2 && c00 + kPair < p.BN;
                 uint32_t vv[16 * kCh];
                 tmem_ld16(t_row + c00, *reinterpret_cast<uint32_t(*)[16]>(&vv[0]));
@@ -885,6 +888,12 @@ cudaError_t launch_variant(const ConvParams& p0, int parities, cudaStream_t stre
         p.fd_tx.init(static_cast<uint32_t>(p.tiles_x));
         p.fd_ty.init(static_cast<uint32_t>(p.tiles_y));
     }
+    // BN / 16 chunks over kEpiGroups warps per lane quarter leave some warps
+    // one chunk more per tile (BN 160: 3, 3, 2, 2); rotating the assignment
+    // by BN/16 mod kEpiGroups each tile evens the load over consecutive
+    // tiles (two accumulators of slack)
+    static const int rot_env = std::getenv("LC_EPI_ROT") ? std::atoi(std::getenv("LC_EPI_ROT")) : 1;
+    p.epi_rot = rot_env ? (p.BN / 16) % kEpiGroups : 0;
     static bool attr_set[kMaxDevices] = {};
     const int dev = current_device();
     if (!attr_set[dev]) {

@@ -91,6 +91,7 @@ struct alignas(64) ConvParams {
     int cg;                       // 1: one CTA per M=128 tile; 2: CTA pair, M=256 (cta_group::2)
     int nparity;                  // parity classes (grid z of the schedule): 1 or 4
     int m_fastest;                // tile order: 1 weight-stationary (M fastest), 0 activation-stationary
+    int epi_rot;                  // epilogue column-group rotation per tile (set at launch)
     int planar32;                 // with nhwc32: channel-planar [channel][img][y][x] instead of NHWC
     int nhwc32;                   // with out32: raw fp32 NHWC (channel stride cs_out), value
                                   // = scale * acc, no offsets/activation (tap-to-N GEMMs whose
