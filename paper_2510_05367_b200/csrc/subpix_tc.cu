@@ -224,6 +224,8 @@ __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_consta
         const int OH = MODE == kTapSubpix ? 2 * p.H : p.H, OW = MODE == kTapSubpix ? 2 * p.W : p.W;
         const size_t plane = static_cast<size_t>(OH) * OW;
         constexpr int kTilePx = kTapTY * kTapTX;
+        // i / C as a multiply-high (exact for i < 2^31, C <= 4; C == 1 separately)
+        const uint32_t cmag = C > 1 ? 0xFFFFFFFFu / static_cast<uint32_t>(C) + 1u : 0u;
         int lt = 0;
         int bad = 0;
         for (int tile; (tile = tile_at(lt)) >= 0; ++lt) {
@@ -261,8 +263,14 @@ __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_consta
                 // task (c, py, ry, rx): out(2Y+py, 2X+px) = bias + sum_dx y[(ry, rx+px+dx)][((py*2+px)*2+dx)*C + c]
                 // (the row taps dy are already summed by the MMA)
                 for (int i = et; i < kTilePx * 2 * C; i += 32 * kEpiWarps) {
-                    const int c = i / (2 * kTilePx);
-                    const int r = i - c * 2 * kTilePx;
+                    int c, r;
+                    if (p.cfast) {
+                        r = C == 1 ? i : static_cast<int>(__umulhi(static_cast<uint32_t>(i), cmag));
+                        c = i - r * C;
+                    } else {
+                        c = i / (2 * kTilePx);
+                        r = i - c * 2 * kTilePx;
+                    }
                     const int py = r / kTilePx, r2 = r - py * kTilePx;
                     const int ry = r2 / kTapTX, rx = r2 - ry * kTapTX;
                     const int Y = Y0 + ry, X = X0 + rx;
@@ -280,8 +288,14 @@ __global__ void __launch_bounds__(kThreads, 1) tap_tc_kernel(const __grid_consta
             } else {
                 // task (c, ry, rx): out(Y, X) = sum_in s*y + (o * sum_in wsum + bias)
                 for (int i = et; i < kTilePx * C; i += 32 * kEpiWarps) {
-                    const int c = i / kTilePx;
-                    const int r = i - c * kTilePx;
+                    int c, r;
+                    if (p.cfast) {
+                        r = C == 1 ? i : static_cast<int>(__umulhi(static_cast<uint32_t>(i), cmag));
+                        c = i - r * C;
+                    } else {
+                        c = i / kTilePx;
+                        r = i - c * kTilePx;
+                    }
                     const int ry = r / kTapTX, rx = r - ry * kTapTX;
                     const int Y = Y0 + ry, X = X0 + rx;
                     if (Y >= p.win.oy1 || X >= p.win.ox1) continue;
@@ -353,8 +367,15 @@ cudaError_t launch_mode(const TapTcParams& p, cudaStream_t st) {
     const int sms = sm[dev];
     const int units = (MODE == kTapConv3 && p.pair_T > 0) ? p.pair_T * p.tiles_x * p.tiles_y : p.num_tiles;
     const int grid = units < sms ? units : sms;
+    // LC_TAP_CFAST=1: channel-fastest epilogue tasks, so a warp's 32 reads of
+    // the staged tap columns cover 32 / C pixels x C channels in distinct
+    // banks (the pixel-fastest order strides by the 28 / 36-float row: 4-way
+    // conflicts).  8x fewer conflicts, same kernel time: off.
+    static const int cfast = std::getenv("LC_TAP_CFAST") ? std::atoi(std::getenv("LC_TAP_CFAST")) : 0;
+    TapTcParams q = p;
+    q.cfast = cfast;
     return launch_pdl(tap_tc_kernel<MODE, TY>, dim3(grid), dim3(kThreads), static_cast<size_t>(smem_bytes<MODE, TY>(p)),
-                      st, p);
+                      st, q);
 }
 
 template <int MODE, int TY>

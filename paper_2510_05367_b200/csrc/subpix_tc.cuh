@@ -44,6 +44,7 @@ struct TapTcParams {
     //   x_out = a*x + b*((1-g)*e_u + g*e_c)  [+ c*z]
     // instead of eps (which never reaches HBM); non-finite results raise
     // *bad (the next step's check_input, unet.cpp:134).
+    int cfast;  // epilogue task order: 1 channel fastest (set at launch, LC_TAP_CFAST)
     int pair_T;
     const float* x;
     float* x_out;
