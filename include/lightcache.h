@@ -98,7 +98,8 @@ int lc_run_resident_async(lc_ctx* ctx);
 /* Same with pinned host buffers (the lc_run_pipeline contract): the H2D of
  * x0, the run and the per-slice D2H of the video are queued without a host
  * round trip, so run k+1 computes while run k's video downloads; lc_wait
- * completes them.  x0 / video must stay valid until lc_wait returns. */
+ * completes them.  x0 / video must stay valid until lc_wait returns.
+ * Pageable buffers are accepted but run synchronously (lc_run_pipeline). */
 int lc_run_pipeline_async(lc_ctx* ctx, const float* x0, float* video);
 int lc_wait(lc_ctx* ctx, char* report, int64_t report_cap);
 int lc_download_video(lc_ctx* ctx, float* video);

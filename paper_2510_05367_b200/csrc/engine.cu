@@ -2525,8 +2525,17 @@ void Engine::copy_out_parallel(float* dst, const float* src, int64_t n) {
 // graph, and the per-slice video download are queued without a host round
 // trip, so run k+1's denoise overlaps run k's download; wait() completes.
 void Engine::run_e2e_async(const float* x0_pinned, float* video_pinned) {
+    // page-locked buffers only: the graph's download node and the queued H2D
+    // must not see pageable memory (such a call runs synchronously instead)
+    auto is_pinned = [](const void* ptr) {
+        cudaPointerAttributes pa{};
+        const bool ok = ptr && cudaPointerGetAttributes(&pa, ptr) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        return ok;
+    };
     const bool ready = use_graphs && conv_profiler() == nullptr && graph_exec_ && graph_slice_ == decode_slice &&
-                       T_alloc_ == cfg_.frames && cfg_.mode != "image";
+                       T_alloc_ == cfg_.frames && cfg_.mode != "image" && is_pinned(x0_pinned) &&
+                       is_pinned(video_pinned);
     if (!ready) {
         last_async_ = run(x0_pinned, video_pinned, nullptr, false);
         async_pending_ = false;

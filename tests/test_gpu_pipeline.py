@@ -339,6 +339,18 @@ def test_graph_replay_is_bit_identical(ctx, oracle, kind, extra):
     v_sync, _, _ = ctx.run_pipeline()  # synchronous run after a queued one
     assert np.array_equal(vids[1].array, want_b)
     assert np.array_equal(v_sync.reshape(-1), want_a)
+    # pageable buffers through the async entry point run synchronously (no
+    # graph download node may point at pageable memory); a pinned run queued
+    # before completes first
+    vids[2].array[:] = -1.0
+    ctx.run_e2e_async(x0, vids[2])
+    xp = np.array(x0b.array)
+    vp = np.full(ctx.video_elems(), -1.0, np.float32)
+    import ctypes
+    assert lc.lib().lc_run_pipeline_async(ctx._h, ctypes.c_void_p(xp.ctypes.data), ctypes.c_void_p(vp.ctypes.data)) == 0
+    ctx.wait()
+    assert np.array_equal(vids[2].array, want_a)
+    assert np.array_equal(vp, want_b)
     for v in vids:
         v.free()
     x0b.free()
